@@ -1,0 +1,194 @@
+/*
+ * memo.h — C ABI of the B200-native MEMO training-step hot path (libmemo.so).
+ *
+ * Plain C types only: pointers, sizes, PODs.  Every function returns an
+ * integer status with the reference CLI's exit-code meaning
+ * (proj/tools/actmem.cpp:351-371, README.md:100-108):
+ *   0 ok, 1 unexpected/internal (incl. CUDA errors), 2 bad input
+ *   (ConfigError / TraceParseError), 3 infeasible plan (InfeasibleError,
+ *   PlanningError, arena > HBM), 4 out of host memory (CpuInfeasibleError,
+ *   pinned allocation failure).
+ * The text of the last error on the calling thread is memo_last_error().
+ * Nothing throws across this boundary.
+ *
+ * Each declaration cites the reference interface it replaces.
+ */
+#ifndef MEMO_H_
+#define MEMO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MEMO_OK = 0,
+  MEMO_ERR_INTERNAL = 1,
+  MEMO_ERR_INPUT = 2,
+  MEMO_ERR_INFEASIBLE = 3,
+  MEMO_ERR_HOST_MEMORY = 4
+};
+
+#define MEMO_NUM_SKELETAL 10
+
+/* proj/include/actmem/types.hpp:80-123 (ModelConfig).  skeletal_weight[i]
+ * overrides default_skeletal_components()[i] (swap.hpp:38-45) when it is not
+ * NaN; component order: layer_input, input_norm, q, k, v, attn_out,
+ * attn_proj, post_attn_norm, ffn_fc1, ffn_act. */
+typedef struct memo_model_config {
+  uint64_t n_layers, hidden, ffn_hidden, n_heads, vocab, batch, seq_len, dtype_bytes,
+      tp_degree, sp_or_cp_degree;
+  int32_t untied_classifier;
+  double skeletal_weight[MEMO_NUM_SKELETAL];
+} memo_model_config;
+
+/* types.hpp:126-141 (HardwareConfig) */
+typedef struct memo_hardware_config {
+  double pcie_bandwidth;
+  uint64_t cpu_mem;
+  uint64_t gpu_mem;
+  double peak_flops;
+  double efficiency;
+} memo_hardware_config;
+
+/* swap.hpp:75-89 (SkeletalSizes); component bytes in emission order. */
+typedef struct memo_skeletal_sizes {
+  uint64_t s_input, s_attn, s_others, total;
+  uint64_t component_bytes[MEMO_NUM_SKELETAL];
+} memo_skeletal_sizes;
+
+/* swap.hpp:94-103 (SwapPlan) */
+typedef struct memo_swap_plan {
+  double alpha;
+  uint64_t mandatory_bytes, swapped_bytes_per_layer, cpu_footprint, swapped_layers;
+  int32_t has_mandatory_stall;
+  double mandatory_stall;
+} memo_swap_plan;
+
+/* swap.hpp:164-188 (TokenSplit) */
+typedef struct memo_token_split {
+  uint64_t swap_tokens, recompute_tokens;
+} memo_token_split;
+
+/* schedule.hpp:31-53 (ParamCount) */
+typedef struct memo_param_count {
+  uint64_t embedding, per_layer, final_norm, classifier, total;
+} memo_param_count;
+
+/* schedule.hpp:74-95 (TimingModel) */
+typedef struct memo_timing_model {
+  double t_fwd_layer, t_bwd_layer, t_attn_fwd, t_embedding_fwd, t_embedding_bwd,
+      t_classifier_fwd, t_classifier_bwd, bwd_ratio;
+} memo_timing_model;
+
+/* schedule.hpp:124-175 (StreamId, EventKind, ScheduleEvent); enum values
+ * follow the reference declaration order. */
+typedef struct memo_schedule_event {
+  int32_t stream; /* 0 compute, 1 offload, 2 prefetch */
+  int32_t kind;   /* 0 emb_fwd,1 layer_fwd,2 cls_fwd,3 cls_bwd,4 recompute,5 layer_bwd,
+                     6 emb_bwd,7 offload,8 prefetch */
+  int32_t layer;
+  double start, end;
+} memo_schedule_event;
+
+/* schedule.hpp:250-258 (SimReport) */
+typedef struct memo_sim_report {
+  double iteration_time, compute_blocked, forward_blocked, offload_stream_busy,
+      prefetch_stream_busy, tgs, mfu;
+} memo_sim_report;
+
+/* ---------------------------------------------------------------- misc */
+const char* memo_last_error(void);
+const char* memo_version(void);
+void memo_free(void* p); /* frees strings returned by this library */
+
+/* ---------------------------------------------------------------- planner
+ * (host C++, bit-exact restatement of the reference's planning path) */
+
+/* json_io.hpp:141-176 run_config_from_json: parse the reference's RunConfig JSON. */
+int memo_parse_run_config(const char* json_text, memo_model_config* model,
+                          memo_hardware_config* hw, uint64_t* planner_cap,
+                          uint64_t* planner_alignment, double* planner_time_budget,
+                          uint64_t* token_granularity, double* t_layer, uint64_t* synth_seed);
+/* types.hpp:104-122, 133-140 validate(); fills defaults for NaN weights. */
+int memo_model_config_default(memo_model_config* cfg);
+int memo_hardware_config_default(memo_hardware_config* hw);
+/* swap.hpp:75 skeletal_sizes */
+int memo_skeletal_sizes_of(const memo_model_config* cfg, memo_skeletal_sizes* out);
+/* swap.hpp:105 solve_alpha */
+int memo_solve_alpha(const memo_skeletal_sizes* sz, const memo_hardware_config* hw,
+                     double t_layer_fwd, uint64_t n_layers, memo_swap_plan* out);
+/* schedule.hpp:409 make_swap_plan_with_alpha */
+int memo_swap_plan_with_alpha(const memo_skeletal_sizes* sz, const memo_hardware_config* hw,
+                              double alpha, uint64_t n_layers, memo_swap_plan* out);
+/* swap.hpp:177 token_split */
+int memo_token_split_of(double alpha, uint64_t seq_len_local, uint64_t granularity,
+                        memo_token_split* out);
+/* schedule.hpp:44 count_params (+ ParamCount::total) */
+int memo_count_params(const memo_model_config* cfg, memo_param_count* out);
+/* schedule.hpp:57 estimate_flops_per_sample */
+double memo_flops_per_sample(const memo_model_config* cfg, uint64_t param_count);
+/* schedule.hpp:64 mfu_from_tgs */
+double memo_mfu_from_tgs(const memo_model_config* cfg, const memo_hardware_config* hw,
+                         uint64_t param_count, double tgs);
+/* schedule.hpp:100 analytic_timing */
+int memo_analytic_timing(const memo_model_config* cfg, const memo_hardware_config* hw,
+                         memo_timing_model* out);
+/* bilevel.hpp:189 plan_model on a trace in the reference text format
+ * (trace.hpp:262-350); *plan_json receives json_io.hpp:189 to_json(GlobalPlan).dump(). */
+int memo_plan_model(const char* trace_text, uint64_t cap, double time_budget,
+                    uint64_t alignment, char** plan_json);
+/* dsa.hpp:391 solve_exact on the lifespans of one segment-free request list; JSON
+ * {"status":..,"peak":..,"addresses":{..}} */
+int memo_solve_dsa(const char* trace_text, uint64_t cap, double time_budget,
+                   uint64_t alignment, char** result_json);
+/* trace.hpp:272 parse_trace + :352 serialize_trace round trip (validation). */
+int memo_trace_roundtrip(const char* trace_text, char** out_text);
+/* schedule.hpp:186 build_schedule; *n_out = event count (events may be NULL to query). */
+int memo_build_schedule(const memo_model_config* cfg, const memo_hardware_config* hw,
+                        const memo_skeletal_sizes* sz, const memo_swap_plan* swap,
+                        const memo_timing_model* tm, memo_schedule_event* events,
+                        size_t capacity, size_t* n_out);
+/* schedule.hpp:301 validate_schedule; violations joined by '\n' (empty = valid). */
+int memo_validate_schedule(const memo_schedule_event* events, size_t n, uint64_t n_layers,
+                           const memo_swap_plan* swap, char** violations);
+/* schedule.hpp:260 simulate */
+int memo_simulate(const memo_schedule_event* events, size_t n, const memo_model_config* cfg,
+                  const memo_hardware_config* hw, uint64_t param_count, memo_sim_report* out);
+/* json_io.hpp:265 fnv1a_hex */
+int memo_fnv1a_hex(const char* data, size_t len, char out[19]);
+
+/* ---------------------------------------------------------------- kernels
+ * Direct entry points to the sm_100a kernels, device pointers, for tests and
+ * benchmarks.  `stream` is a cudaStream_t (NULL = legacy default stream). */
+
+/* C = A . B^T, see csrc/kernels/gemm_tc.h for the layout/epilogue codes. */
+typedef struct memo_gemm_args {
+  int32_t M, N, K;
+  const void* a;
+  int64_t lda;
+  int32_t a_mn_major;
+  const void* b;
+  int64_t ldb;
+  int32_t b_mn_major;
+  int32_t epilogue;
+  void* c;
+  int64_t ldc;
+  float* out_f32;
+  const float* resid;
+  int64_t ld_f32;
+  void* q;
+  void* k;
+  void* v;
+  int32_t hidden, head_dim;
+  const void* rope;
+  int64_t pos0;
+} memo_gemm_args;
+int memo_gemm(const memo_gemm_args* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEMO_H_ */

@@ -1,0 +1,397 @@
+// gemm_tc.cu — persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[m, n] = sum_k A[m, k] * B[n, k]          (bf16 x bf16 -> f32 in TMEM)
+//
+// A and B may each be K-major (row-major with K contiguous) or MN-major
+// (K rows, M/N contiguous), which covers the three GEMMs of a linear layer:
+//   fwd    Y  = X  . W^T   A=X  K-major,  B=W  K-major
+//   dgrad  dX = dY . W     A=dY K-major,  B=W  MN-major
+//   wgrad  dW = dY^T . X   A=dY MN-major, B=X  MN-major
+// Operands are staged by TMA (128-byte swizzle) into a 4-deep shared-memory
+// ring; one thread issues tcgen05.mma (M=128, N=256, K=16) into a
+// double-buffered TMEM accumulator so the epilogue of tile i overlaps the
+// main loop of tile i+1.  Epilogues are fused: bf16/f32 store, f32
+// accumulate, residual add, and the RoPE-rotating Q/K/V split.
+//
+// The K loop order is the same for every output row, so recomputing a token
+// suffix reproduces the full-pass rows bit for bit (MEMO's recompute must be
+// indistinguishable from the swapped tensors; see swap.hpp:172-188).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "gemm_tc.h"
+#include "sm100.cuh"
+
+namespace memo {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_TILE_BYTES = BM * BK * 2;  // 16 KiB
+constexpr int B_TILE_BYTES = BN * BK * 2;  // 32 KiB
+constexpr int STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
+constexpr int NUM_THREADS = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int TMEM_COLS = 2 * BN;
+constexpr int GROUP_M = 16;  // rasterisation: 16 M-tiles share a B panel in L2
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct EpiParams {
+  int kind;
+  void* c;
+  long long ldc;
+  float* out_f32;
+  const float* resid;
+  long long ld_f32;
+  __nv_bfloat16* q;
+  __nv_bfloat16* k;
+  __nv_bfloat16* v;
+  int hidden;
+  int head_dim;
+  const float2* rope;
+  long long pos0;
+};
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* x) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 u;
+    u.x = dev::pack_bf16(x[8 * i + 0], x[8 * i + 1]);
+    u.y = dev::pack_bf16(x[8 * i + 2], x[8 * i + 3]);
+    u.z = dev::pack_bf16(x[8 * i + 4], x[8 * i + 5]);
+    u.w = dev::pack_bf16(x[8 * i + 6], x[8 * i + 7]);
+    d[i] = u;
+  }
+}
+
+// One thread owns one row; `x` holds 32 consecutive accumulator columns.
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n0, int N,
+                                               float (&x)[32]) {
+  if (n0 >= N) return;
+  switch (ep.kind) {
+    case GEMM_EPI_BF16: {
+      store_bf16x32(reinterpret_cast<__nv_bfloat16*>(ep.c) + m * ep.ldc + n0, x);
+      break;
+    }
+    case GEMM_EPI_F32: {
+      float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.c) + m * ep.ldc + n0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+      break;
+    }
+    case GEMM_EPI_F32_ACC: {
+      float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.c) + m * ep.ldc + n0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 o = d[i];
+        o.x += x[4 * i];
+        o.y += x[4 * i + 1];
+        o.z += x[4 * i + 2];
+        o.w += x[4 * i + 3];
+        d[i] = o;
+      }
+      break;
+    }
+    case GEMM_EPI_RESID: {
+      // The projection output is a bf16 tensor; the residual stream is f32.
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = dev::bf16_round(x[i]);
+      if (ep.c) store_bf16x32(reinterpret_cast<__nv_bfloat16*>(ep.c) + m * ep.ldc + n0, x);
+      const float4* r = reinterpret_cast<const float4*>(ep.resid + m * ep.ld_f32 + n0);
+      float4* o = reinterpret_cast<float4*>(ep.out_f32 + m * ep.ld_f32 + n0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 a = r[i];
+        a.x += x[4 * i];
+        a.y += x[4 * i + 1];
+        a.z += x[4 * i + 2];
+        a.w += x[4 * i + 3];
+        o[i] = a;
+      }
+      break;
+    }
+    case GEMM_EPI_QKV_ROPE: {
+      const int which = n0 / ep.hidden;
+      const int col = n0 - which * ep.hidden;
+      __nv_bfloat16* base = which == 0 ? ep.q : (which == 1 ? ep.k : ep.v);
+      if (which < 2) {
+        // Interleaved-pair rotary embedding on absolute token position.
+        const int j0 = col % ep.head_dim;  // multiple of 32
+        const float2* cs = ep.rope + (ep.pos0 + m) * (ep.head_dim / 2) + j0 / 2;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          const float2 t = cs[p];
+          // Round to bf16 first: the rotation applies to the bf16 projection.
+          const float a = dev::bf16_round(x[2 * p]);
+          const float b = dev::bf16_round(x[2 * p + 1]);
+          x[2 * p] = a * t.x - b * t.y;
+          x[2 * p + 1] = a * t.y + b * t.x;
+        }
+      }
+      store_bf16x32(base + static_cast<long long>(m) * ep.hidden + col, x);
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, int M, int N, int K,
+                   EpiParams ep) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_a);
+    dev::tma_prefetch_desc(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      dev::mbar_init(&full_bar[s], 1);
+      dev::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      dev::mbar_init(&tfull_bar[b], 1);
+      dev::mbar_init(&tempty_bar[b], 128);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, TMEM_COLS);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int t, int& mb, int& nb) {
+    const int group_size = GROUP_M * n_tiles;
+    const int g = t / group_size;
+    const int first_m = g * GROUP_M;
+    const int gm = min(GROUP_M, m_tiles - first_m);
+    const int local = t - g * group_size;
+    mb = first_m + local % gm;
+    nb = local / gm;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, mb, nb);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_TILE_BYTES;
+          dev::mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+          if (!A_MN) {
+            dev::tma_load_2d(sa, &map_a, &full_bar[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              dev::tma_load_2d(sa + j * 8192, &map_a, &full_bar[stage], mb * BM + j * 64,
+                               kb * BK);
+          }
+          if (!B_MN) {
+            dev::tma_load_2d(sb, &map_b, &full_bar[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              dev::tma_load_2d(sb + j * 8192, &map_b, &full_bar[stage], nb * BN + j * 64,
+                               kb * BK);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = dev::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        dev::mbar_wait(&tempty_bar[buf], acc_phase ^ 1);
+        dev::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait(&full_bar[stage], phase);
+          dev::tc_fence_after();
+          const uint32_t sa = dev::smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_TILE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? dev::umma_desc_sw128(sa + k * 2048, 8192, 1024)
+                                     : dev::umma_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? dev::umma_desc_sw128(sb + k * 2048, 8192, 1024)
+                                     : dev::umma_desc_sw128(sb + k * 32, 16, 1024);
+            dev::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          dev::mma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        dev::mma_commit(&tfull_bar[buf]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 ; TMEM lane quarter = warp % 4
+    const uint32_t q = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, mb, nb);
+      const int buf = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      dev::mbar_wait(&tfull_bar[buf], acc_phase);
+      dev::tc_fence_after();
+      const int m = mb * BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        dev::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * BN + c * 32, r);
+        dev::tmem_ld_wait();
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
+        if (m < M) epilogue_chunk(ep, m, nb * BN + c * 32, N, x);
+      }
+      dev::tc_fence_before();
+      dev::mbar_arrive(&tempty_bar[buf]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map, inner dimension contiguous, 128-byte swizzle.
+bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
+                 uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+
+template <bool A_MN, bool B_MN>
+cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  bool ok;
+  if (!A_MN)
+    ok = make_map_2d(&ma, d.a, d.K, d.M, d.lda, BK, BM);
+  else
+    ok = make_map_2d(&ma, d.a, d.M, d.K, d.lda, 64, BK);
+  if (!B_MN)
+    ok = ok && make_map_2d(&mb, d.b, d.K, d.N, d.ldb, BK, BN);
+  else
+    ok = ok && make_map_2d(&mb, d.b, d.N, d.K, d.ldb, 64, BK);
+  if (!ok) return cudaErrorInvalidValue;
+  EpiParams ep;
+  ep.kind = d.epi;
+  ep.c = d.c;
+  ep.ldc = d.ldc;
+  ep.out_f32 = d.out_f32;
+  ep.resid = d.resid;
+  ep.ld_f32 = d.ld_f32;
+  ep.q = d.q;
+  ep.k = d.k;
+  ep.v = d.v;
+  ep.hidden = d.hidden;
+  ep.head_dim = d.head_dim;
+  ep.rope = reinterpret_cast<const float2*>(d.rope);
+  ep.pos0 = d.pos0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_set = true;
+  }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = ((d.M + BM - 1) / BM) * ((d.N + BN - 1) / BN);
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  gemm_tc_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, d.M, d.N,
+                                                                       d.K, ep);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gemm_tc(const GemmDesc& d, cudaStream_t stream) {
+  if (d.M <= 0 || d.N <= 0 || d.K <= 0) return cudaSuccess;
+  if (d.N % 32 != 0 || d.K % 8 != 0) return cudaErrorInvalidValue;
+  if (d.a_mn_major) {
+    if (d.b_mn_major) return launch<true, true>(d, stream);
+    return launch<true, false>(d, stream);
+  }
+  if (d.b_mn_major) return launch<false, true>(d, stream);
+  return launch<false, false>(d, stream);
+}
+
+}  // namespace memo

@@ -1,0 +1,41 @@
+// capi_kernels.cu — C-ABI entry points for the individual sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "host/status.hpp"
+#include "kernels/gemm_tc.h"
+#include "memo.h"
+
+using memo::set_error;
+
+extern "C" int memo_gemm(const memo_gemm_args* a, void* stream) {
+  if (!a) return set_error(MEMO_ERR_INPUT, "memo_gemm: null args");
+  memo::GemmDesc d;
+  d.M = a->M;
+  d.N = a->N;
+  d.K = a->K;
+  d.a = a->a;
+  d.lda = a->lda;
+  d.a_mn_major = a->a_mn_major;
+  d.b = a->b;
+  d.ldb = a->ldb;
+  d.b_mn_major = a->b_mn_major;
+  d.epi = a->epilogue;
+  d.c = a->c;
+  d.ldc = a->ldc;
+  d.out_f32 = a->out_f32;
+  d.resid = a->resid;
+  d.ld_f32 = a->ld_f32;
+  d.q = static_cast<__nv_bfloat16*>(a->q);
+  d.k = static_cast<__nv_bfloat16*>(a->k);
+  d.v = static_cast<__nv_bfloat16*>(a->v);
+  d.hidden = a->hidden;
+  d.head_dim = a->head_dim;
+  d.rope = a->rope;
+  d.pos0 = a->pos0;
+  cudaError_t e = memo::gemm_tc(d, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess)
+    return set_error(MEMO_ERR_INTERNAL, std::string("memo_gemm: ") + cudaGetErrorString(e));
+  return MEMO_OK;
+}

@@ -1,0 +1,97 @@
+"""tcgen05 GEMM (csrc/kernels/gemm_tc.cu) vs a plain PyTorch fp32 reference."""
+import ctypes as C
+
+import pytest
+import torch
+
+from paper_2407_12117_b200 import _abi
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(M, N, K, a, lda, a_mn, b, ldb, b_mn, epi, c=None, ldc=0, **kw):
+    args = _abi.GemmArgsC()
+    args.M, args.N, args.K = M, N, K
+    args.a, args.lda, args.a_mn_major = a.data_ptr(), lda, a_mn
+    args.b, args.ldb, args.b_mn_major = b.data_ptr(), ldb, b_mn
+    args.epilogue = epi
+    args.c = c.data_ptr() if c is not None else None
+    args.ldc = ldc
+    for k, v in kw.items():
+        setattr(args, k, v.data_ptr() if isinstance(v, torch.Tensor) else v)
+    _abi.check(_abi.lib.memo_gemm(C.byref(args), None))
+    torch.cuda.synchronize()
+
+
+def _rand(*shape):
+    return (torch.randn(*shape, device="cuda") * 0.5).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (384, 768, 4096),
+                                   (200, 256, 192), (1024, 2048, 1024)])
+@pytest.mark.parametrize("layout", ["fwd", "dgrad", "wgrad"])
+def test_gemm_layouts(M, N, K, layout):
+    torch.manual_seed(0)
+    if layout == "fwd":      # A [M,K] K-major, B [N,K] K-major
+        A = _rand(M, K); B = _rand(N, K)
+        ref = A.float() @ B.float().t()
+        a, lda, amn, b, ldb, bmn = A, K, 0, B, K, 0
+    elif layout == "dgrad":  # A [M,K] K-major, B stored [K,N] (N contiguous)
+        A = _rand(M, K); Bs = _rand(K, N)
+        ref = A.float() @ Bs.float()
+        a, lda, amn, b, ldb, bmn = A, K, 0, Bs, N, 1
+    else:                    # A stored [K,M], B stored [K,N]
+        As = _rand(K, M); Bs = _rand(K, N)
+        ref = As.float().t() @ Bs.float()
+        a, lda, amn, b, ldb, bmn = As, M, 1, Bs, N, 1
+    out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    _gemm(M, N, K, a, lda, amn, b, ldb, bmn, 1, out, N)
+    err = (out - ref).abs().max().item()
+    assert err <= 1e-3 * (1 + ref.abs().max().item()), err
+    outb = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(M, N, K, a, lda, amn, b, ldb, bmn, 0, outb, N)
+    torch.testing.assert_close(outb.float(), ref.to(torch.bfloat16).float(), rtol=1e-2, atol=1e-2)
+
+
+def test_gemm_f32_accumulate_and_resid():
+    torch.manual_seed(1)
+    M, N, K = 256, 512, 320
+    A = _rand(M, K); B = _rand(N, K)
+    ref = A.float() @ B.float().t()
+    acc = torch.full((M, N), 2.0, device="cuda")
+    _gemm(M, N, K, A, K, 0, B, K, 0, 2, acc, N)
+    torch.testing.assert_close(acc, ref + 2.0, rtol=1e-4, atol=1e-3)
+    resid = torch.randn(M, N, device="cuda")
+    out = torch.empty(M, N, device="cuda")
+    cb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(M, N, K, A, K, 0, B, K, 0, 3, cb, N, out_f32=out, resid=resid, ld_f32=N)
+    refb = ref.to(torch.bfloat16)
+    torch.testing.assert_close(cb.float(), refb.float(), rtol=1e-2, atol=1e-2)
+    torch.testing.assert_close(out, resid + cb.float(), rtol=0, atol=0)
+
+
+def test_gemm_qkv_rope_epilogue():
+    torch.manual_seed(2)
+    S, h, d = 256, 512, 128
+    X = _rand(S, h); W = _rand(3 * h, h)
+    pos0 = 17
+    half = d // 2
+    inv = torch.tensor([10000.0 ** (-2.0 * p / d) for p in range(half)], dtype=torch.float64)
+    pos = torch.arange(pos0 + S, dtype=torch.float64)
+    ang = pos[:, None] * inv[None, :]
+    rope = torch.stack([ang.cos(), ang.sin()], -1).float().cuda().contiguous()
+    q = torch.empty(S, h, device="cuda", dtype=torch.bfloat16)
+    k = torch.empty_like(q); v = torch.empty_like(q)
+    _gemm(S, 3 * h, h, X, h, 0, W, h, 0, 4, None, 0, q=q, k=k, v=v, hidden=h, head_dim=d,
+          rope=rope, pos0=pos0)
+    y = (X.float() @ W.float().t()).to(torch.bfloat16).float()
+    cs = rope[pos0:pos0 + S]
+
+    def rot(t):
+        t = t.view(S, h // d, half, 2)
+        c, s_ = cs[:, None, :, 0], cs[:, None, :, 1]
+        a, b = t[..., 0], t[..., 1]
+        return torch.stack([a * c - b * s_, a * s_ + b * c], -1).view(S, h)
+    torch.testing.assert_close(q.float(), rot(y[:, :h]).to(torch.bfloat16).float(), rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(k.float(), rot(y[:, h:2 * h]).to(torch.bfloat16).float(), rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(v.float(), y[:, 2 * h:], rtol=1e-2, atol=1e-2)

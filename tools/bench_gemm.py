@@ -1,0 +1,66 @@
+"""Micro-benchmark of the tcgen05 GEMM at the cfg2 layer shapes (CUDA events)."""
+import ctypes as C
+import json
+import sys
+import os
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2407_12117_b200 import _abi  # noqa: E402
+
+
+def run(M, N, K, layout, iters=10):
+    if layout == "fwd":
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16); B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        lda, amn, ldb, bmn = K, 0, K, 0
+    elif layout == "dgrad":
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16); B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
+        lda, amn, ldb, bmn = K, 0, N, 1
+    else:
+        A = torch.randn(K, M, device="cuda").to(torch.bfloat16); B = torch.randn(K, N, device="cuda").to(torch.bfloat16)
+        lda, amn, ldb, bmn = M, 1, N, 1
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16 if layout != "wgrad" else torch.float32)
+    args = _abi.GemmArgsC()
+    args.M, args.N, args.K = M, N, K
+    args.a, args.lda, args.a_mn_major = A.data_ptr(), lda, amn
+    args.b, args.ldb, args.b_mn_major = B.data_ptr(), ldb, bmn
+    args.epilogue = 0 if layout != "wgrad" else 1
+    args.c, args.ldc = out.data_ptr(), N
+    for _ in range(3):
+        _abi.check(_abi.lib.memo_gemm(C.byref(args), None))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        _abi.lib.memo_gemm(C.byref(args), None)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    tf = 2.0 * M * N * K / ms / 1e9
+    # torch/cuBLAS reference for context
+    if layout == "fwd":
+        f = lambda: torch.matmul(A, B.t())
+    elif layout == "dgrad":
+        f = lambda: torch.matmul(A, B)
+    else:
+        f = lambda: torch.matmul(A.t(), B)
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_ref = e0.elapsed_time(e1) / iters
+    return {"M": M, "N": N, "K": K, "layout": layout, "ms": ms, "tflops": tf,
+            "cublas_ms": ms_ref, "cublas_tflops": 2.0 * M * N * K / ms_ref / 1e9}
+
+
+if __name__ == "__main__":
+    S = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+    for (M, N, K, lay) in [(S, 12288, 4096, "fwd"), (S, 22016, 4096, "fwd"), (S, 4096, 11008, "fwd"),
+                           (S, 4096, 12288, "dgrad"), (S, 4096, 22016, "dgrad"),
+                           (4096, 11008, S, "wgrad"), (12288, 4096, S, "wgrad")]:
+        print(json.dumps(run(M, N, K, lay)), flush=True)
