@@ -164,18 +164,18 @@ Json goldens_configs() {
   ModelConfig c1p = c1;
   c1p.n_layers = 4;
   add("cfg1p", c1p, b200_hw(), 0.5, true);
-  add("cfg2", llama(4, 4096, 11008, 32, 32000, 131072, 1, true), b200_hw(), -1, false);
-  add("cfg3", llama(32, 4096, 11008, 32, 32000, 1048576, 8, true), b200_hw(), -1, false);
+  add("cfg2", llama(4, 4096, 11008, 32, 32000, 131072, 1, true), b200_hw(), -1, true);
+  add("cfg3", llama(32, 4096, 11008, 32, 32000, 1048576, 8, true), b200_hw(), -1, true);
   for (int tp : {2, 4, 8})
     add("cfg4_tp" + std::to_string(tp), llama(40, 5120, 13824, 40, 32000, 524288, tp, true),
-        b200_hw(tp == 2 ? 1024 * kGiB : 256 * kGiB), -1, false);
+        b200_hw(tp == 2 ? 1024 * kGiB : 256 * kGiB), -1, true);
   for (int k = 0; k <= 8; ++k)
     add("cfg5_a" + std::to_string(k), llama(32, 4096, 11008, 32, 32000, 262144, 1, true),
-        b200_hw(1024 * kGiB), k / 8.0, false);
+        b200_hw(1024 * kGiB), k / 8.0, k == 0);
   // The reference's own config files.
   for (const char* f : {"toy", "7b-1m"}) {
     RunConfig rc = load_run_config(std::string("/root/reference/proj/configs/") + f + ".json");
-    out[std::string("ref_") + f] = report(rc, -1, std::string(f) == "toy");
+    out[std::string("ref_") + f] = report(rc, -1, true);
   }
   return out;
 }
