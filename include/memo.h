@@ -188,6 +188,19 @@ typedef struct memo_gemm_args {
 } memo_gemm_args;
 int memo_gemm(const memo_gemm_args* args, void* stream);
 
+/* Causal FlashAttention forward (tcgen05).  q/k/v/o token-major [S, H*D] bf16,
+ * lse [H, S] f32 (natural log).  D in {64, 128}, S a multiple of 128. */
+int memo_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int32_t S,
+                  int32_t H, int32_t D, float softmax_scale, void* stream);
+/* Causal FlashAttention backward (deterministic).  Writes dq/dk/dv with row
+ * pitch ld_dqkv; when rope != NULL the inverse rotary rotation (float2 table
+ * [pos][D/2], positions pos0..pos0+S-1) is applied to dq and dk.  delta is a
+ * 2*H*S f32 workspace. */
+int memo_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                  const void* dout, float* delta, void* dq, void* dk, void* dv, int64_t ld_dqkv,
+                  const void* rope, int64_t pos0, int32_t S, int32_t H, int32_t D,
+                  float softmax_scale, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,751 @@
+// attention.cu — causal FlashAttention forward/backward on tcgen05 (sm_100a).
+//
+// Layout: Q, K, V, O are token-major [S, H*D] bf16 (head hh occupies columns
+// [hh*D, hh*D+D)); LSE is [H, S] f32 (natural log).  Tiles are 128 tokens.
+//
+// Forward (one CTA per (query tile, head)), warp roles:
+//   warp 0  TMA producer: Q once, K/V tiles into two 2-stage rings
+//   warp 1  single-thread tcgen05.mma issuer: S = Q K^T into a double-buffered
+//           TMEM S, then O += P V with P read straight from TMEM (it
+//           overwrites the S buffer it came from)
+//   warps 4-7  softmax: one thread per query row (TMEM lane); online softmax
+//           in the exp2 domain with lazy rescaling (O is only touched when a
+//           row max grows by more than 2^8), then the normalising epilogue.
+// S(j+1) is issued before P(j)V(j), so QK^T of the next tile overlaps the
+// softmax of the current one; tcgen05 ops of one thread execute in order,
+// which is what makes reusing S's buffer for P safe.
+//
+// Backward is deterministic (no atomics), so swap+recompute and no-swap
+// gradients are bit-identical:
+//   attn_bwd_dkdv  one CTA per (key tile, head), loops over query tiles:
+//                  S^T = K Q^T, dP^T = V dO^T, dV += P^T dO, dK += dS^T Q
+//   attn_bwd_dq    one CTA per (query tile, head), loops over key tiles:
+//                  S = Q K^T, dP = dO V^T, dQ += dS K
+// with P^T/dS^T kept in TMEM as the A operand.  RoPE's inverse rotation is
+// fused into the dQ/dK epilogues.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "attention.h"
+#include "sm100.cuh"
+#include "tma_util.h"
+
+namespace memo {
+namespace {
+
+constexpr int TILE = 128;
+constexpr int CHUNK_BYTES = TILE * 64 * 2;  // one [128 rows][64 cols] bf16 TMA box = 16 KiB
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct FwdSmem {
+  static constexpr int NC = D / 64;  // 64-col chunks per tile
+  static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;
+  static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
+  // K-major tile split in 64-col chunks of 16 KiB; k-step of 16 elements.
+  return dev::umma_desc_sw128(base + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
+  // MN-major tile: 128 K-rows of 128 B per 64-wide MN chunk; k-step of 16 rows.
+  return dev::umma_desc_sw128(base + kk * 2048, CHUNK_BYTES, 1024);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q,
+                    const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
+                    float* __restrict__ lse, int S, int H, float scale_log2) {
+  using L = FwdSmem<D>;
+  constexpr int NC = L::NC;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2]
+  uint64_t* p_full = bars + 11;  // [2]
+  uint64_t* o_done = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int n_tiles = S / TILE;
+  const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
+  const int hh = blockIdx.y;
+  const int n_kv = qt + 1;
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_k);
+    dev::tma_prefetch_desc(&map_v);
+    dev::mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      dev::mbar_init(&k_full[s], 1);
+      dev::mbar_init(&k_empty[s], 1);
+      dev::mbar_init(&v_full[s], 1);
+      dev::mbar_init(&v_empty[s], 1);
+      dev::mbar_init(&s_full[s], 1);
+      dev::mbar_init(&p_full[s], 128);
+    }
+    dev::mbar_init(o_done, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s[2] = {tmem, tmem + 128};
+  const uint32_t t_o = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint8_t* sq = smem + L::Q_OFF;
+      dev::mbar_expect_tx(q_full, L::TILE_BYTES);
+      for (int c = 0; c < NC; ++c)
+        dev::tma_load_2d(sq + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, qt * TILE);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        uint8_t* sk = smem + L::K_OFF + st * L::TILE_BYTES;
+        uint8_t* sv = smem + L::V_OFF + st * L::TILE_BYTES;
+        dev::mbar_wait(&k_empty[st], ph ^ 1);
+        dev::mbar_expect_tx(&k_full[st], L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c)
+          dev::tma_load_2d(sk + c * CHUNK_BYTES, &map_k, &k_full[st], hh * D + c * 64, j * TILE);
+        dev::mbar_wait(&v_empty[st], ph ^ 1);
+        dev::mbar_expect_tx(&v_full[st], L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c)
+          dev::tma_load_2d(sv + c * CHUNK_BYTES, &map_v, &v_full[st], hh * D + c * 64, j * TILE);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
+      const uint32_t sq = dev::smem_u32(smem + L::Q_OFF);
+      dev::mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        dev::mbar_wait(&k_full[st], (j >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t sk = dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss(t_s[st], kmajor_desc(sq, kk), kmajor_desc(sk, kk), idesc_s, kk > 0);
+        dev::mma_commit(&s_full[st]);
+        dev::mma_commit(&k_empty[st]);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_s(j + 1);
+        const int st = j & 1;
+        dev::mbar_wait(&p_full[st], (j >> 1) & 1);
+        dev::mbar_wait(&v_full[st], (j >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t sv = dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ts(t_o, t_s[st] + kk * 8, mnmajor_desc(sv, kk), idesc_o, (j | kk) != 0);
+        dev::mma_commit(o_done);
+        dev::mma_commit(&v_empty[st]);
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int row = q4 * 32 + lane;                 // TMEM lane == query row in tile
+    const int qidx = qt * TILE + row;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      dev::mbar_wait(&s_full[st], (j >> 1) & 1);
+      dev::tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        dev::tmem_ld32(t_s[st] + lane_off + c * 32, r);
+        dev::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * scale_log2;
+      }
+      if (j == qt) {  // diagonal tile: causal mask
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i > row) s[i] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      const float cand = fmaxf(m, mx);
+      const bool need = j == 0 || cand > m + kRescaleThreshold;
+      const bool any = __any_sync(0xffffffffu, need);
+      float factor = 1.f;
+      float m_new = m;
+      if (any) {
+        m_new = cand;
+        factor = j == 0 ? 0.f : exp2f(m - m_new);
+      }
+      float sum = 0.f;
+      uint32_t p[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float a = exp2f(s[2 * i] - m_new);
+        const float b = exp2f(s[2 * i + 1] - m_new);
+        sum += a + b;
+        p[i] = dev::pack_bf16(a, b);
+      }
+      l = l * factor + sum;
+      m = m_new;
+      {
+        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&p[0]);
+        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&p[32]);
+        dev::tmem_st32(t_s[st] + lane_off, p0);
+        dev::tmem_st32(t_s[st] + lane_off + 32, p1);
+      }
+      if (any && j > 0) {
+        // O must hold P(j-1)V(j-1) before it is rescaled.
+        dev::mbar_wait(o_done, (j - 1) & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          dev::tmem_ld32(t_o + lane_off + c * 32, r);
+          dev::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
+          dev::tmem_st32(t_o + lane_off + c * 32, r);
+        }
+      }
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_full[st]);
+    }
+    // epilogue
+    dev::mbar_wait(o_done, (n_kv - 1) & 1);
+    dev::tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      dev::tmem_ld32(t_o + lane_off + c * 32, r);
+      dev::tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 u;
+        u.x = dev::pack_bf16(__uint_as_float(r[8 * i + 0]) * inv, __uint_as_float(r[8 * i + 1]) * inv);
+        u.y = dev::pack_bf16(__uint_as_float(r[8 * i + 2]) * inv, __uint_as_float(r[8 * i + 3]) * inv);
+        u.z = dev::pack_bf16(__uint_as_float(r[8 * i + 4]) * inv, __uint_as_float(r[8 * i + 5]) * inv);
+        u.w = dev::pack_bf16(__uint_as_float(r[8 * i + 6]) * inv, __uint_as_float(r[8 * i + 7]) * inv);
+        dst[i] = u;
+      }
+    }
+    lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(l)) * kLn2;
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
+
+// ============================================================== backward
+// delta[h][t] = sum_d dO*O ; lse2[h][t] = lse * log2(e)
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
+                                     const __nv_bfloat16* __restrict__ dout,
+                                     const float* __restrict__ lse, float* __restrict__ delta,
+                                     float* __restrict__ lse2, int S, int H, int D) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);  // row = t*H + hh
+  const int lane = threadIdx.x & 31;
+  if (row >= S * H) return;
+  const int t = row / H, hh = row - t * H;
+  const __nv_bfloat16* op = o + static_cast<long long>(t) * H * D + hh * D;
+  const __nv_bfloat16* dp = dout + static_cast<long long>(t) * H * D + hh * D;
+  float acc = 0.f;
+  for (int d = lane * 2; d < D; d += 64) {
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(op + d);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(dp + d);
+    acc += __bfloat162float(a.x) * __bfloat162float(b.x) + __bfloat162float(a.y) * __bfloat162float(b.y);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    const long long i = static_cast<long long>(hh) * S + t;
+    delta[i] = acc;
+    lse2[i] = lse[i] * kLog2e;
+  }
+}
+
+template <int D>
+struct BwdSmem {
+  static constexpr int NC = D / 64;
+  static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
+  static constexpr int A0_OFF = 0;                      // K (dkdv) | Q (dq)
+  static constexpr int A1_OFF = A0_OFF + TILE_BYTES;    // V (dkdv) | dO (dq)
+  static constexpr int R0_OFF = A1_OFF + TILE_BYTES;    // ring: Q (dkdv) | K (dq)  [2]
+  static constexpr int R1_OFF = R0_OFF + 2 * TILE_BYTES;  // ring: dO (dkdv) | V (dq) [2]
+  static constexpr int VEC_OFF = R1_OFF + 2 * TILE_BYTES;  // [2][2][128] f32 (lse2, delta)
+  static constexpr int BAR_OFF = VEC_OFF + 2 * 2 * 128 * 4;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+// Writes 32 consecutive columns of a dq/dk row: scale, inverse RoPE, bf16.
+__device__ __forceinline__ void store_grad32(__nv_bfloat16* dst, float (&x)[32], float scale,
+                                             const float2* cs) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] *= scale;
+  if (cs) {
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const float2 t = cs[p];
+      const float a = x[2 * p], b = x[2 * p + 1];
+      x[2 * p] = a * t.x + b * t.y;
+      x[2 * p + 1] = -a * t.y + b * t.x;
+    }
+  }
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 u;
+    u.x = dev::pack_bf16(x[8 * i + 0], x[8 * i + 1]);
+    u.y = dev::pack_bf16(x[8 * i + 2], x[8 * i + 3]);
+    u.z = dev::pack_bf16(x[8 * i + 4], x[8 * i + 5]);
+    u.w = dev::pack_bf16(x[8 * i + 6], x[8 * i + 7]);
+    d[i] = u;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_q,
+                         const __grid_constant__ CUtensorMap map_k,
+                         const __grid_constant__ CUtensorMap map_v,
+                         const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                         const float* __restrict__ delta, __nv_bfloat16* __restrict__ dk,
+                         __nv_bfloat16* __restrict__ dv, long long ld, const float2* __restrict__ rope,
+                         long long pos0, int S, float scale, float scale_log2) {
+  using L = BwdSmem<D>;
+  constexpr int NC = L::NC;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* in_full = bars + 1;   // [2]
+  uint64_t* in_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_ready = bars + 6;
+  uint64_t* fin = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  float* vec = reinterpret_cast<float*>(smem + L::VEC_OFF);  // [stage][lse2|delta][128]
+
+  const int n_tiles = S / TILE;
+  const int kt = blockIdx.x;  // key tile
+  const int hh = blockIdx.y;
+  const int n_q = n_tiles - kt;  // query tiles kt..n_tiles-1
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_k);
+    dev::tma_prefetch_desc(&map_v);
+    dev::tma_prefetch_desc(&map_do);
+    dev::mbar_init(kv_full, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      dev::mbar_init(&in_full[s2], 1);
+      dev::mbar_init(&in_empty[s2], 1);
+    }
+    dev::mbar_init(s_full, 1);
+    dev::mbar_init(p_ready, 128);
+    dev::mbar_init(fin, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_expect_tx(kv_full, 2 * L::TILE_BYTES);
+      for (int c = 0; c < NC; ++c) {
+        dev::tma_load_2d(smem + L::A0_OFF + c * CHUNK_BYTES, &map_k, kv_full, hh * D + c * 64, kt * TILE);
+        dev::tma_load_2d(smem + L::A1_OFF + c * CHUNK_BYTES, &map_v, kv_full, hh * D + c * 64, kt * TILE);
+      }
+      for (int i = 0; i < n_q; ++i) {
+        const int qt = kt + i, st = i & 1;
+        dev::mbar_wait(&in_empty[st], ((i >> 1) & 1) ^ 1);
+        dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::R0_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q,
+                           &in_full[st], hh * D + c * 64, qt * TILE);
+          dev::tma_load_2d(smem + L::R1_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_do,
+                           &in_full[st], hh * D + c * 64, qt * TILE);
+        }
+        const long long off = static_cast<long long>(hh) * S + qt * TILE;
+        dev::bulk_load(vec + st * 256, lse2 + off, 512, &in_full[st]);
+        dev::bulk_load(vec + st * 256 + 128, delta + off, 512, &in_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
+      const uint32_t sk = dev::smem_u32(smem + L::A0_OFF);
+      const uint32_t sv = dev::smem_u32(smem + L::A1_OFF);
+      dev::mbar_wait(kv_full, 0);
+      for (int i = 0; i < n_q; ++i) {
+        const int st = i & 1;
+        dev::mbar_wait(&in_full[st], (i >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t sq = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES);
+        const uint32_t sdo = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss(t_st, kmajor_desc(sk, kk), kmajor_desc(sq, kk), idesc_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss(t_dpt, kmajor_desc(sv, kk), kmajor_desc(sdo, kk), idesc_s, kk > 0);
+        dev::mma_commit(s_full);
+        dev::mbar_wait(p_ready, i & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ts(t_dv, t_st + kk * 8, mnmajor_desc(sdo, kk), idesc_g, (i | kk) != 0);
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ts(t_dk, t_dpt + kk * 8, mnmajor_desc(sq, kk), idesc_g, (i | kk) != 0);
+        dev::mma_commit(&in_empty[st]);
+      }
+      dev::mma_commit(fin);
+    }
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int r = q4 * 32 + lane;  // key row in tile
+    const int kidx = kt * TILE + r;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    for (int i = 0; i < n_q; ++i) {
+      const int st = i & 1;
+      const bool diag = i == 0;
+      dev::mbar_wait(&in_full[st], (i >> 1) & 1);
+      dev::mbar_wait(s_full, i & 1);
+      dev::tc_fence_after();
+      const float* l2 = vec + st * 256;
+      const float* dl = l2 + 128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sr[32], dr[32];
+        dev::tmem_ld32(t_st + lane_off + c * 32, sr);
+        dev::tmem_ld32(t_dpt + lane_off + c * 32, dr);
+        dev::tmem_ld_wait();
+        uint32_t pp[16], dd[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float p2[2], d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int qc = c * 32 + 2 * j + e;
+            float p = exp2f(__uint_as_float(sr[2 * j + e]) * scale_log2 - l2[qc]);
+            if (diag && qc < r) p = 0.f;
+            p2[e] = p;
+            d2[e] = p * (__uint_as_float(dr[2 * j + e]) - dl[qc]);
+          }
+          pp[j] = dev::pack_bf16(p2[0], p2[1]);
+          dd[j] = dev::pack_bf16(d2[0], d2[1]);
+        }
+        dev::tmem_st16(t_st + lane_off + c * 16, pp);
+        dev::tmem_st16(t_dpt + lane_off + c * 16, dd);
+      }
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(p_ready);
+    }
+    dev::mbar_wait(fin, 0);
+    dev::tc_fence_after();
+    __nv_bfloat16* dvrow = dv + static_cast<long long>(kidx) * ld + hh * D;
+    __nv_bfloat16* dkrow = dk + static_cast<long long>(kidx) * ld + hh * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r32[32];
+      float x[32];
+      dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
+      dev::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dvrow + c * 32, x, 1.f, nullptr);
+      dev::tmem_ld32(t_dk + lane_off + c * 32, r32);
+      dev::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dkrow + c * 32, x, scale,
+                   rope ? rope + (pos0 + kidx) * (D / 2) + c * 16 : nullptr);
+    }
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_q,
+                       const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v,
+                       const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                       const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq, long long ld,
+                       const float2* __restrict__ rope, long long pos0, int S, float scale,
+                       float scale_log2) {
+  using L = BwdSmem<D>;
+  constexpr int NC = L::NC;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* qd_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* ds_ready = bars + 6;
+  uint64_t* fin = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int n_tiles = S / TILE;
+  const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
+  const int hh = blockIdx.y;
+  const int n_kv = qt + 1;
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_k);
+    dev::tma_prefetch_desc(&map_v);
+    dev::tma_prefetch_desc(&map_do);
+    dev::mbar_init(qd_full, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      dev::mbar_init(&kv_full[s2], 1);
+      dev::mbar_init(&kv_empty[s2], 1);
+    }
+    dev::mbar_init(s_full, 1);
+    dev::mbar_init(ds_ready, 128);
+    dev::mbar_init(fin, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_expect_tx(qd_full, 2 * L::TILE_BYTES);
+      for (int c = 0; c < NC; ++c) {
+        dev::tma_load_2d(smem + L::A0_OFF + c * CHUNK_BYTES, &map_q, qd_full, hh * D + c * 64, qt * TILE);
+        dev::tma_load_2d(smem + L::A1_OFF + c * CHUNK_BYTES, &map_do, qd_full, hh * D + c * 64, qt * TILE);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        dev::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        dev::mbar_expect_tx(&kv_full[st], 2 * L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::R0_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_k,
+                           &kv_full[st], hh * D + c * 64, j * TILE);
+          dev::tma_load_2d(smem + L::R1_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_v,
+                           &kv_full[st], hh * D + c * 64, j * TILE);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
+      const uint32_t sq = dev::smem_u32(smem + L::A0_OFF);
+      const uint32_t sdo = dev::smem_u32(smem + L::A1_OFF);
+      dev::mbar_wait(qd_full, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        dev::mbar_wait(&kv_full[st], (j >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t sk = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES);
+        const uint32_t sv = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss(t_s, kmajor_desc(sq, kk), kmajor_desc(sk, kk), idesc_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss(t_dp, kmajor_desc(sdo, kk), kmajor_desc(sv, kk), idesc_s, kk > 0);
+        dev::mma_commit(s_full);
+        dev::mbar_wait(ds_ready, j & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ts(t_dq, t_s + kk * 8, mnmajor_desc(sk, kk), idesc_g, (j | kk) != 0);
+        dev::mma_commit(&kv_empty[st]);
+      }
+      dev::mma_commit(fin);
+    }
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const int qidx = qt * TILE + r;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const long long vi = static_cast<long long>(hh) * S + qidx;
+    const float my_lse2 = lse2[vi];
+    const float my_delta = delta[vi];
+    for (int j = 0; j < n_kv; ++j) {
+      const bool diag = j == qt;
+      dev::mbar_wait(s_full, j & 1);
+      dev::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sr[32], dr[32];
+        dev::tmem_ld32(t_s + lane_off + c * 32, sr);
+        dev::tmem_ld32(t_dp + lane_off + c * 32, dr);
+        dev::tmem_ld_wait();
+        uint32_t dd[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          float d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int kc = c * 32 + 2 * jj + e;
+            float p = exp2f(__uint_as_float(sr[2 * jj + e]) * scale_log2 - my_lse2);
+            if (diag && kc > r) p = 0.f;
+            d2[e] = p * (__uint_as_float(dr[2 * jj + e]) - my_delta);
+          }
+          dd[jj] = dev::pack_bf16(d2[0], d2[1]);
+        }
+        dev::tmem_st16(t_s + lane_off + c * 16, dd);
+      }
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(ds_ready);
+    }
+    dev::mbar_wait(fin, 0);
+    dev::tc_fence_after();
+    __nv_bfloat16* dqrow = dq + static_cast<long long>(qidx) * ld + hh * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r32[32];
+      float x[32];
+      dev::tmem_ld32(t_dq + lane_off + c * 32, r32);
+      dev::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dqrow + c * 32, x, scale,
+                   rope ? rope + (pos0 + qidx) * (D / 2) + c * 16 : nullptr);
+    }
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
+  const int h = a.H * a.D;
+  CUtensorMap mq, mk, mv, mdo;
+  bool ok = make_tma_2d_bf16(&mq, a.q, h, a.S, h, 64, TILE) &&
+            make_tma_2d_bf16(&mk, a.k, h, a.S, h, 64, TILE) &&
+            make_tma_2d_bf16(&mv, a.v, h, a.S, h, 64, TILE) &&
+            make_tma_2d_bf16(&mdo, a.dout, h, a.S, h, 64, TILE);
+  if (!ok) return cudaErrorInvalidValue;
+  static std::once_flag f;
+  std::call_once(f, [] {
+    cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         BwdSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         BwdSmem<D>::BYTES);
+  });
+  float* delta = a.delta;
+  float* lse2 = a.delta + static_cast<long long>(a.H) * a.S;
+  const int rows = a.S * a.H;
+  attn_bwd_prep_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S,
+                                                            a.H, D);
+  const float scale_log2 = a.softmax_scale * kLog2e;
+  const float2* rope = reinterpret_cast<const float2*>(a.rope);
+  dim3 grid(a.S / TILE, a.H);
+  attn_bwd_dkdv_kernel<D><<<grid, 256, BwdSmem<D>::BYTES, stream>>>(
+      mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
+      scale_log2);
+  attn_bwd_dq_kernel<D><<<grid, 256, BwdSmem<D>::BYTES, stream>>>(
+      mq, mk, mv, mdo, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
+      scale_log2);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
+  if (a.S % TILE != 0 || (a.D != 64 && a.D != 128)) return cudaErrorInvalidValue;
+  const int h = a.H * a.D;
+  CUtensorMap mq, mk, mv;
+  bool ok = make_tma_2d_bf16(&mq, a.q, h, a.S, h, 64, TILE) &&
+            make_tma_2d_bf16(&mk, a.k, h, a.S, h, 64, TILE) &&
+            make_tma_2d_bf16(&mv, a.v, h, a.S, h, 64, TILE);
+  if (!ok) return cudaErrorInvalidValue;
+  const float scale_log2 = a.softmax_scale * kLog2e;
+  dim3 grid(a.S / TILE, a.H);
+  if (a.D == 128) {
+    static std::once_flag f;
+    std::call_once(f, [] {
+      cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           FwdSmem<128>::BYTES);
+    });
+    attn_fwd_kernel<128><<<grid, 256, FwdSmem<128>::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
+                                                                      a.H, scale_log2);
+  } else {
+    static std::once_flag f;
+    std::call_once(f, [] {
+      cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           FwdSmem<64>::BYTES);
+    });
+    attn_fwd_kernel<64><<<grid, 256, FwdSmem<64>::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
+                                                                    a.H, scale_log2);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace memo
+
+namespace memo {
+cudaError_t attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
+  if (a.S % TILE != 0) return cudaErrorInvalidValue;
+  if (a.D == 128) return launch_bwd<128>(a, stream);
+  if (a.D == 64) return launch_bwd<64>(a, stream);
+  return cudaErrorInvalidValue;
+}
+}  // namespace memo

@@ -25,6 +25,7 @@
 
 #include "gemm_tc.h"
 #include "sm100.cuh"
+#include "tma_util.h"
 
 namespace memo {
 namespace {
@@ -298,56 +299,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                  CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-// 2-D bf16 tensor map, inner dimension contiguous, 128-byte swizzle.
-bool make_map_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
-                 uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld_elems * 2};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-int g_num_sms = 0;
-
 template <bool A_MN, bool B_MN>
 cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   CUtensorMap ma, mb;
   bool ok;
   if (!A_MN)
-    ok = make_map_2d(&ma, d.a, d.K, d.M, d.lda, BK, BM);
+    ok = make_tma_2d_bf16(&ma, d.a, d.K, d.M, d.lda, BK, BM);
   else
-    ok = make_map_2d(&ma, d.a, d.M, d.K, d.lda, 64, BK);
+    ok = make_tma_2d_bf16(&ma, d.a, d.M, d.K, d.lda, 64, BK);
   if (!B_MN)
-    ok = ok && make_map_2d(&mb, d.b, d.K, d.N, d.ldb, BK, BN);
+    ok = ok && make_tma_2d_bf16(&mb, d.b, d.K, d.N, d.ldb, BK, BN);
   else
-    ok = ok && make_map_2d(&mb, d.b, d.N, d.K, d.ldb, 64, BK);
+    ok = ok && make_tma_2d_bf16(&mb, d.b, d.N, d.K, d.ldb, 64, BK);
   if (!ok) return cudaErrorInvalidValue;
   EpiParams ep;
   ep.kind = d.epi;
@@ -363,17 +326,12 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   ep.head_dim = d.head_dim;
   ep.rope = reinterpret_cast<const float2*>(d.rope);
   ep.pos0 = d.pos0;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr_set = true;
-  }
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  });
+  const int g_num_sms = num_sms();
   const int tiles = ((d.M + BM - 1) / BM) * ((d.N + BN - 1) / BN);
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   gemm_tc_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, d.M, d.N,

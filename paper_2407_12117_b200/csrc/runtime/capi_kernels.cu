@@ -4,6 +4,7 @@
 #include <string>
 
 #include "host/status.hpp"
+#include "kernels/attention.h"
 #include "kernels/gemm_tc.h"
 #include "memo.h"
 
@@ -37,5 +38,51 @@ extern "C" int memo_gemm(const memo_gemm_args* a, void* stream) {
   cudaError_t e = memo::gemm_tc(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess)
     return set_error(MEMO_ERR_INTERNAL, std::string("memo_gemm: ") + cudaGetErrorString(e));
+  return MEMO_OK;
+}
+
+extern "C" int memo_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                             int32_t S, int32_t H, int32_t D, float scale, void* stream) {
+  memo::AttnFwdArgs a;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.k = static_cast<const __nv_bfloat16*>(k);
+  a.v = static_cast<const __nv_bfloat16*>(v);
+  a.o = static_cast<__nv_bfloat16*>(o);
+  a.lse = lse;
+  a.S = S;
+  a.H = H;
+  a.D = D;
+  a.softmax_scale = scale;
+  cudaError_t e = memo::attn_fwd(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess)
+    return set_error(MEMO_ERR_INTERNAL, std::string("memo_attn_fwd: ") + cudaGetErrorString(e));
+  return MEMO_OK;
+}
+
+extern "C" int memo_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                             const float* lse, const void* dout, float* delta, void* dq, void* dk,
+                             void* dv, int64_t ld, const void* rope, int64_t pos0, int32_t S,
+                             int32_t H, int32_t D, float scale, void* stream) {
+  memo::AttnBwdArgs a;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.k = static_cast<const __nv_bfloat16*>(k);
+  a.v = static_cast<const __nv_bfloat16*>(v);
+  a.o = static_cast<const __nv_bfloat16*>(o);
+  a.lse = lse;
+  a.dout = static_cast<const __nv_bfloat16*>(dout);
+  a.delta = delta;
+  a.dq = static_cast<__nv_bfloat16*>(dq);
+  a.dk = static_cast<__nv_bfloat16*>(dk);
+  a.dv = static_cast<__nv_bfloat16*>(dv);
+  a.ld_dqkv = ld;
+  a.rope = rope;
+  a.pos0 = pos0;
+  a.S = S;
+  a.H = H;
+  a.D = D;
+  a.softmax_scale = scale;
+  cudaError_t e = memo::attn_bwd(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess)
+    return set_error(MEMO_ERR_INTERNAL, std::string("memo_attn_bwd: ") + cudaGetErrorString(e));
   return MEMO_OK;
 }

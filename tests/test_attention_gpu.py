@@ -1,0 +1,129 @@
+"""tcgen05 causal FlashAttention (csrc/kernels/attention.cu) vs a PyTorch fp32 reference."""
+import ctypes as C
+import math
+
+import pytest
+import torch
+
+from paper_2407_12117_b200 import _abi
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_attention(q, k, v, H, D):
+    S = q.shape[0]
+    qf = q.float().view(S, H, D).transpose(0, 1)
+    kf = k.float().view(S, H, D).transpose(0, 1)
+    vf = v.float().view(S, H, D).transpose(0, 1)
+    s = qf @ kf.transpose(1, 2) / math.sqrt(D)
+    mask = torch.triu(torch.ones(S, S, dtype=torch.bool, device=q.device), 1)
+    s = s.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    p = torch.softmax(s, -1)
+    o = (p @ vf).transpose(0, 1).reshape(S, H * D)
+    return o, lse
+
+
+def run_fwd(q, k, v, H, D):
+    S = q.shape[0]
+    o = torch.empty_like(q)
+    lse = torch.empty(H, S, device="cuda", dtype=torch.float32)
+    _abi.check(_abi.lib.memo_attn_fwd(C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
+                                      C.c_void_p(v.data_ptr()), C.c_void_p(o.data_ptr()),
+                                      C.c_void_p(lse.data_ptr()), S, H, D,
+                                      C.c_float(1.0 / math.sqrt(D)), None))
+    torch.cuda.synchronize()
+    return o, lse
+
+
+@pytest.mark.parametrize("S,H,D", [(128, 1, 128), (256, 2, 128), (512, 2, 64), (1024, 3, 128),
+                                   (768, 4, 64)])
+def test_attn_fwd(S, H, D):
+    torch.manual_seed(S + H + D)
+    q = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    k = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    v = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    o, lse = run_fwd(q, k, v, H, D)
+    o_ref, lse_ref = ref_attention(q, k, v, H, D)
+    torch.testing.assert_close(lse, lse_ref, rtol=1e-3, atol=2e-3)
+    torch.testing.assert_close(o.float(), o_ref, rtol=2e-2, atol=2e-2)
+
+
+def test_attn_fwd_large_logits():
+    # Rows whose max grows late exercise the lazy O rescale.
+    torch.manual_seed(7)
+    S, H, D = 1024, 2, 128
+    q = (torch.randn(S, H * D, device="cuda") * 3).to(torch.bfloat16)
+    k = (torch.randn(S, H * D, device="cuda") * 3).to(torch.bfloat16)
+    k[-256:] *= 2
+    v = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    o, lse = run_fwd(q, k, v, H, D)
+    o_ref, lse_ref = ref_attention(q, k, v, H, D)
+    torch.testing.assert_close(lse, lse_ref, rtol=1e-3, atol=5e-3)
+    torch.testing.assert_close(o.float(), o_ref, rtol=2e-2, atol=2e-2)
+
+
+def run_bwd(q, k, v, o, lse, do, H, D, rope=None, pos0=0):
+    S = q.shape[0]
+    h = H * D
+    dqkv = torch.zeros(S, 3 * h, device="cuda", dtype=torch.bfloat16)
+    ws = torch.empty(2 * H * S, device="cuda", dtype=torch.float32)
+    base = dqkv.data_ptr()
+    _abi.check(_abi.lib.memo_attn_bwd(
+        C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()),
+        C.c_void_p(o.data_ptr()), C.c_void_p(lse.data_ptr()), C.c_void_p(do.data_ptr()),
+        C.c_void_p(ws.data_ptr()), C.c_void_p(base), C.c_void_p(base + 2 * h), C.c_void_p(base + 4 * h),
+        C.c_int64(3 * h), C.c_void_p(rope.data_ptr() if rope is not None else None), C.c_int64(pos0),
+        S, H, D, C.c_float(1.0 / math.sqrt(D)), None))
+    torch.cuda.synchronize()
+    return dqkv[:, :h], dqkv[:, h:2 * h], dqkv[:, 2 * h:]
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm()).item()
+
+
+@pytest.mark.parametrize("S,H,D", [(128, 1, 128), (256, 2, 128), (512, 2, 64), (1024, 2, 128)])
+def test_attn_bwd(S, H, D):
+    torch.manual_seed(11 + S + D)
+    q = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    k = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    v = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    do = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    o, lse = run_fwd(q, k, v, H, D)
+    dq, dk, dv = run_bwd(q, k, v, o, lse, do, H, D)
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    o_ref, _ = ref_attention(qf, kf, vf, H, D)
+    o_ref.backward(do.float())
+    assert _rel(dv, vf.grad) < 1e-2, _rel(dv, vf.grad)
+    assert _rel(dk, kf.grad) < 1e-2, _rel(dk, kf.grad)
+    assert _rel(dq, qf.grad) < 1e-2, _rel(dq, qf.grad)
+
+
+def test_attn_bwd_rope_and_determinism():
+    torch.manual_seed(5)
+    S, H, D = 512, 2, 128
+    pos0 = 128
+    half = D // 2
+    inv = torch.tensor([10000.0 ** (-2.0 * p / D) for p in range(half)], dtype=torch.float64)
+    ang = torch.arange(pos0 + S, dtype=torch.float64)[:, None] * inv[None, :]
+    rope = torch.stack([ang.cos(), ang.sin()], -1).float().cuda().contiguous()
+    q = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    k = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    v = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    do = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
+    o, lse = run_fwd(q, k, v, H, D)
+    dq0, dk0, dv0 = run_bwd(q, k, v, o, lse, do, H, D)
+    dq, dk, dv = run_bwd(q, k, v, o, lse, do, H, D, rope, pos0)
+    dq2, dk2, dv2 = run_bwd(q, k, v, o, lse, do, H, D, rope, pos0)
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+    cs = rope[pos0:pos0 + S]
+
+    def inv_rot(t):
+        t = t.float().view(S, H, half, 2)
+        c, s_ = cs[:, None, :, 0], cs[:, None, :, 1]
+        a, b = t[..., 0], t[..., 1]
+        return torch.stack([a * c + b * s_, -a * s_ + b * c], -1).view(S, H * D)
+    assert _rel(dq, inv_rot(dq0)) < 1e-2
+    assert _rel(dk, inv_rot(dk0)) < 1e-2
+    assert torch.equal(dv, dv0)
