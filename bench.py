@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py — MEMO training-step throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+N=1 workload (BASELINE configs[1]): Llama-7B architecture, 4 layers, seq 131072,
+one B200, alpha tuned by the planner (solve_alpha with the MEASURED host-link
+bandwidth and MEASURED forward-layer time).  A step = embedding -> 4 layers fwd
+(offload of the swapped layers' activations) -> classifier + CE -> 4 layers bwd
+(prefetch + suffix recompute) -> embedding grad -> AdamW.  Synthetic tokens,
+random-init weights (counter hash).  N>1 under torchrun: every rank runs an
+independent replica (weak scaling, "replicas only" this round — see DESIGN.md).
+
+Prints ONE JSON line (rank 0).  `value` is device-resident tokens/s over all
+ranks; `e2e` is the same metric through the C-ABI step with host token buffers
+(H2D of the batch and D2H of the loss inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MFU and tokens/sec/GPU, 7B train step at 128K–1M seq, 1/2/4/8 B200"
+B200_SPEC_BF16 = 2.25e15
+
+CONFIGS = {
+    # name: (n_layers, hidden, heads, intermediate, vocab, seq, description)
+    "cfg2": (4, 4096, 32, 11008, 32000, 131072,
+             "Llama-7B arch, 4 layers, seq 131072, 1xB200, alpha tuned by planner"),
+    "cfg1p": (4, 256, 4, 768, 512, 4096, "tiny 4-layer (h256, 4 heads, seq 4096), alpha=0.5"),
+    "cfg5": (32, 4096, 32, 11008, 32000, 262144, "Llama-7B arch, 32 layers, seq 262144, 1xB200"),
+}
+
+
+def splitmix64(x):
+    x = (x + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+    return x ^ (x >> 31)
+
+
+def synthetic_batch(seed, vocab, seq):
+    import numpy as np
+    idx = np.arange(seq, dtype=np.uint64) + np.uint64(seed)
+    with np.errstate(over="ignore"):
+        x = idx + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    toks = (x % np.uint64(vocab)).astype(np.int32)
+    labels = np.empty_like(toks)
+    labels[:-1] = toks[1:]
+    labels[-1] = -1
+    return toks, labels
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, name in enumerate(names):
+                if r[4 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops", 1678.8), d.get("bf16_tflops_sustained", 1409.0), d.get("hbm_gbs", 6459.0), "measured"
+    except OSError:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def host_link_bandwidth(torch, nbytes=1 << 31):
+    """Pinned D2H and H2D GB/s on this GPU (CUDA events)."""
+    dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    out = {}
+    for name, fn in (("d2h", lambda: host.copy_(dev, non_blocking=True)),
+                     ("h2d", lambda: dev.copy_(host, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = 3 * nbytes / (e0.elapsed_time(e1) * 1e-3)
+    del dev, host
+    return out
+
+
+def cpu_baseline(n_cfg, repeat=1):
+    """CPU oracle (oracle/llama_cpu.c, OpenMP on all host cores) on a bounded sample:
+    one layer of the workload's width at 256 tokens, full vocab; converted to the
+    workload's tokens/s through the reference FLOP model (schedule.hpp:57-61)."""
+    from oracle import oracle as O
+    n, h, H, inter, V, S, _ = n_cfg
+    s_sample = 256
+    ocfg = O.make_cfg(1, h, H, inter, V, s_sample)
+    params = O.init_params(ocfg, 1234)
+    toks, labels = synthetic_batch(1234, V, s_sample)
+    t0 = time.perf_counter()
+    for _ in range(repeat):
+        O.step(ocfg, params, toks, labels)
+    dt = (time.perf_counter() - t0) / repeat
+    from paper_2407_12117_b200 import planner as P
+    sample_cfg = P.ModelConfig(n_layers=1, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
+                               seq_len=s_sample, untied_classifier=True)
+    work_cfg = P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
+                             seq_len=S, untied_classifier=True)
+    f_sample = P.estimate_flops_per_sample(sample_cfg, P.count_params(sample_cfg)["total"])
+    f_work = P.estimate_flops_per_sample(work_cfg, P.count_params(work_cfg)["total"])
+    cpu_flops = f_sample / dt
+    tokens_per_s = cpu_flops / (f_work / S)
+    cores = os.cpu_count()
+    return {"value": tokens_per_s, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": (f"oracle/llama_cpu.c fwd+bwd of 1 layer (h={h}, heads={H}, f={inter}, V={V}) at "
+                       f"{s_sample} tokens on {cores} OpenMP threads took {dt:.2f} s = "
+                       f"{cpu_flops / 1e9:.1f} GFLOP/s (reference FLOP model); value = that rate / "
+                       f"FLOPs-per-token of the workload"),
+            "sample_seconds": dt}
+
+
+def reference_planner_ms(name):
+    """The reference's own CPU path (actmem report pipeline) on this config, if built."""
+    probe = os.path.join(ROOT, "oracle", "_ref", "ref_probe")
+    if not os.path.exists(probe):
+        return None
+    n, h, H, inter, V, S, _ = CONFIGS[name]
+    cfg = {"model": {"n_layers": n, "hidden": h, "ffn_hidden": inter * 3 // 2, "n_heads": H,
+                     "vocab": V, "batch": 1, "seq_len": S, "dtype_bytes": 2, "tp_degree": 1,
+                     "sp_or_cp_degree": 1, "untied_classifier": True},
+           "hardware": {"pcie_bandwidth": 50e9, "cpu_mem": 96 * 2 ** 30, "gpu_mem": 180 * 10 ** 9,
+                        "peak_flops": 2.25e15, "efficiency": 0.5}}
+    import tempfile
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+        json.dump(cfg, f)
+    try:
+        out = subprocess.check_output([probe, "bench_report", f.name, "20"], text=True, timeout=120)
+        return json.loads(out)["per_iter_s"] * 1e3
+    except Exception:  # noqa: BLE001
+        return None
+    finally:
+        os.unlink(f.name)
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    n_cfg = CONFIGS[args.config]
+    vals = []
+    for _ in range(max(1, args.warmup and 0) + args.steps):
+        vals.append(cpu_baseline(n_cfg)["value"])
+    base = cpu_baseline(n_cfg)
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": n_cfg[6], "cpu": "oracle port"},
+            "cpu_baseline": {**base, "value": v},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    rp = reference_planner_ms(args.config)
+    if rp is not None:
+        line["reference_planner_ms"] = rp
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_2407_12117_b200 import planner as P
+    from paper_2407_12117_b200.executor import Executor
+
+    n, h, H, inter, V, S, desc = CONFIGS[args.config]
+    cfg = P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
+                        batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True)
+    link = host_link_bandwidth(torch)
+    host_mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    gpus_on_node = max(torch.cuda.device_count(), world)
+    cpu_mem = int(min(host_mem * 0.6 / gpus_on_node, 2 ** 40))  # per-GPU pinned budget
+    hw = P.HardwareConfig(pcie_bandwidth=link["d2h"], cpu_mem=cpu_mem,
+                          gpu_mem=torch.cuda.get_device_properties(local).total_memory,
+                          peak_flops=B200_SPEC_BF16, efficiency=0.5)
+    toks, labels = synthetic_batch(1234 + rank, V, S)
+    forced_alpha = 0.5 if args.config == "cfg1p" else -1.0
+
+    # Calibrate: one step with the analytic layer time, then re-solve alpha with
+    # the measured forward-layer time (swap.hpp:105 with SwapOptions.t_layer).
+    with Executor(cfg, hw, alpha=forced_alpha, op_timing=0) as ex:
+        ex.step(toks, labels)
+        tl = ex.timeline()
+    t_fwd = [e.end - e.start for e in tl if e.kind == "layer_fwd"]
+    t_layer = float(np.median(t_fwd))
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    ex = Executor(cfg, hw, alpha=forced_alpha, t_layer=t_layer, op_timing=1)
+    free1, _ = torch.cuda.mem_get_info()
+    info0 = ex.info()
+    stream = torch.cuda.ExternalStream(ex.stream)
+
+    # ---- device-resident timing
+    ex.load_batch(toks, labels)
+    for _ in range(args.warmup):
+        ex.step_resident()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            ex.step_resident()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    tl = ex.timeline()  # last step
+    info = ex.info()
+    launches = info["kernel_launches"] * args.steps
+    t_max = ms
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = t.item()
+    value = world * S / (t_max * 1e-3)
+
+    # ---- end to end through the C ABI with host buffers
+    e2e_ms = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ex.step(toks, labels)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e = statistics.mean(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = t.item()
+
+    # ---- MEMO report on the measured timeline (reference validator + simulator)
+    swap = info0["swap"]
+    violations = P.validate_schedule(tl, n, swap)
+    p_total = P.count_params(cfg)["total"]
+    sim = P.simulate(tl, cfg, hw, p_total)
+    flops = P.estimate_flops_per_sample(cfg, p_total)
+    mfu = flops / (ms * 1e-3) / B200_SPEC_BF16
+    burst, sustained, hbm, peak_src = measured_peaks()
+    off = [e for e in tl if e.kind == "offload"]
+    pre = [e for e in tl if e.kind == "prefetch"]
+    off_s = sum(e.end - e.start for e in off)
+    pre_s = sum(e.end - e.start for e in pre)
+    ops = info["ops"]
+    dk = ops["attn_bwd_dkdv"]
+    achieved = dk["flops"] / dk["count"] / (dk["ms"] / dk["count"] * 1e-3) / 1e12 if dk["count"] else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            traffic = json.load(f).get("attn_bwd_dkdv", {}).get("dram_bytes_per_launch")
+    except OSError:
+        pass
+    kernels = {k: {"ms_per_step": v["ms"], "launches": v["count"],
+                   "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] and v["flops"] else None}
+               for k, v in ops.items()}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (splitmix64 tokens, counter-hash random-init weights)",
+        "config": {"workload": desc, "model": "llama-7b-arch", "n_layers": n, "global_batch": world,
+                   "seq_len": S, "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "working set (GB of activations) >> 126 MB L2; no flush needed",
+                   "alpha": swap.alpha, "swap_tokens": info0["split"][0],
+                   "recompute_tokens": info0["split"][1], "t_layer_measured_s": t_layer,
+                   "host_link_d2h_GBps": link["d2h"] / 1e9, "host_link_h2d_GBps": link["h2d"] / 1e9,
+                   "cpu_mem_budget": cpu_mem},
+        "tokens_per_s_per_gpu": value / world,
+        "mfu": mfu, "mfu_vs_measured_peak": flops / (ms * 1e-3) / (burst * 1e12),
+        "e2e": {"value": world * S / (e2e * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(info["h2d_bytes"]), "d2h_bytes_per_step": int(info["d2h_bytes"])},
+        "roofline": {"kernel": "attn_bwd_dkdv (causal FlashAttention dK/dV, tcgen05)",
+                     "bound": "tensor", "achieved": achieved, "peak": sustained,
+                     "unit": "TFLOP/s", "frac": (achieved / sustained) if achieved else None,
+                     "traffic": traffic, "peak_source": f"{peak_src} bf16_tflops_sustained",
+                     "algorithmic_flops_per_launch": dk["flops"] / dk["count"] if dk["count"] else None},
+        "kernels": kernels,
+        "memo": {"schedule_violations": violations, "sim": sim,
+                 "exposed_swap_s": sim["compute_blocked"],
+                 "exposed_swap_frac": sim["compute_blocked"] / sim["iteration_time"] if sim["iteration_time"] else None,
+                 "forward_blocked_s": sim["forward_blocked"],
+                 "offload_GBps": info["offload_bytes"] / off_s / 1e9 if off_s else None,
+                 "prefetch_GBps": info["prefetch_bytes"] / pre_s / 1e9 if pre_s else None,
+                 "planned_device_bytes": info0["device_bytes"], "arena_bytes": info0["arena_bytes"],
+                 "rounding_buffer_bytes": info0["rb_bytes"], "state_bytes": info0["state_bytes"],
+                 "measured_device_bytes": free0 - free1, "pinned_bytes": info0["pinned_bytes"],
+                 "cpu_footprint_planned": swap.cpu_footprint},
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(CONFIGS[args.config])
+        rp = reference_planner_ms(args.config)
+        if rp is not None:
+            line["cpu_baseline"]["reference_planner_ms"] = rp
+    ex.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

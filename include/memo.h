@@ -201,6 +201,77 @@ int memo_attn_bwd(const void* q, const void* k, const void* v, const void* o, co
                   const void* rope, int64_t pos0, int32_t S, int32_t H, int32_t D,
                   float softmax_scale, void* stream);
 
+/* ---------------------------------------------------------------- executor
+ * The real training step that replaces the reference's simulated executor
+ * (schedule.hpp:186 build_schedule / :260 simulate): Llama layers on sm_100a
+ * kernels, one preallocated HBM allocation laid out by the bi-level plan,
+ * token-wise swap to pinned host memory + suffix recompute on copy streams.
+ * The caller (cmd_report's analogue, actmem.cpp:227-273) owns token arrays;
+ * the context owns all device/pinned memory, streams and events.  A context
+ * is not thread-safe. */
+typedef struct memo_exec memo_exec;
+
+typedef struct memo_exec_options {
+  uint64_t seed;              /* weight init seed (counter hash, see oracle/llama_cpu.c) */
+  double alpha;               /* < 0: solve_alpha (swap.hpp:105); else forced (schedule.hpp:409) */
+  uint64_t token_granularity; /* swap.hpp:177 (128) */
+  int32_t swap_enabled;       /* 0: all layers resident, no swap/recompute (parity baseline) */
+  int32_t ce_chunk;           /* classifier tokens per chunk */
+  float eps, rope_theta;
+  int32_t optimizer;          /* 1: AdamW step at the end of memo_exec_step */
+  float lr, beta1, beta2, adam_eps, weight_decay;
+  double t_layer;             /* measured fwd-layer seconds for solve_alpha (0 = analytic) */
+  double plan_time_budget;
+  uint64_t alignment;         /* planner alignment (512) */
+  int32_t op_timing;          /* 1: CUDA events around every GEMM/attention launch */
+  int32_t dry_run;            /* 1: plan only (trace, arena plan, alpha, sizes) — no CUDA */
+} memo_exec_options;
+
+typedef struct memo_exec_info {
+  int32_t S, h, H, D, F, V, n_layers;
+  memo_swap_plan swap;
+  memo_token_split split;
+  memo_skeletal_sizes skeletal;
+  uint64_t arena_bytes, rb_bytes, device_bytes, pinned_bytes, state_bytes;
+  int64_t param_count;
+  int32_t swap_enabled;
+  double last_step_ms, h2d_bytes, d2h_bytes, offload_bytes, prefetch_bytes;
+  int32_t kernel_launches;
+  /* per kernel class of the last step (op_timing=1): 0 attn_fwd, 1 attn_bwd_prep,
+   * 2 attn_bwd_dkdv, 3 attn_bwd_dq, 4 gemm — device ms, algorithmic FLOPs, launches */
+  double op_ms[5], op_flops[5];
+  int32_t op_count[5];
+} memo_exec_info;
+
+int memo_exec_options_default(memo_exec_options* opt);
+/* status 2 bad config, 3 arena+RBs+states exceed HBM or plan not optimal,
+ * 4 pinned host allocation failed / CpuInfeasible. */
+int memo_exec_create(const memo_model_config* cfg, const memo_hardware_config* hw,
+                     const memo_exec_options* opt, memo_exec** out);
+void memo_exec_destroy(memo_exec* ctx);
+/* End to end: host tokens/labels (int32 [S], label < 0 = ignore) -> H2D ->
+ * step -> D2H of the mean loss. */
+int memo_exec_step(memo_exec* ctx, const int32_t* tokens, const int32_t* labels, float* loss);
+/* Split form for device-resident benchmarking: upload once, then run steps. */
+int memo_exec_load_batch(memo_exec* ctx, const int32_t* tokens, const int32_t* labels);
+int memo_exec_step_resident(memo_exec* ctx); /* asynchronous on the compute stream */
+int memo_exec_loss(memo_exec* ctx, float* loss); /* synchronises */
+void* memo_exec_stream(memo_exec* ctx);          /* compute cudaStream_t */
+/* Measured schedule of the last step (schedule.hpp:162-175 ScheduleEvent,
+ * seconds from step start); events may be NULL to query *n. */
+int memo_exec_timeline(memo_exec* ctx, memo_schedule_event* events, size_t capacity, size_t* n);
+int memo_exec_get_info(memo_exec* ctx, memo_exec_info* info);
+/* The executor's own request trace (trace.hpp text format) and the bound plan
+ * (json_io.hpp:189 to_json(GlobalPlan).dump()). */
+int memo_exec_trace(memo_exec* ctx, char** text);
+int memo_exec_plan(memo_exec* ctx, char** json);
+/* Device pointer of a named tensor: "<param>", "grad/<param>", "master/<param>"
+ * with param in {embedding, g1, wqkv, wo, g2, wgu, wd, gf, wcls, all}
+ * (layer = -1 for non-layer params), or "act/<skeletal component>". */
+int memo_exec_tensor(memo_exec* ctx, const char* name, int32_t layer, void** ptr, size_t* bytes);
+/* Synchronous copy of a named tensor (as memo_exec_tensor) into host memory. */
+int memo_exec_read(memo_exec* ctx, const char* name, int32_t layer, void* host, size_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -693,17 +693,21 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   float* delta = a.delta;
   float* lse2 = a.delta + static_cast<long long>(a.H) * a.S;
   const int rows = a.S * a.H;
+  if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
   attn_bwd_prep_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S,
                                                             a.H, D);
   const float scale_log2 = a.softmax_scale * kLog2e;
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   dim3 grid(a.S / TILE, a.H);
+  if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
   attn_bwd_dkdv_kernel<D><<<grid, 256, BwdSmem<D>::BYTES, stream>>>(
       mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
       scale_log2);
+  if (a.ev[2]) cudaEventRecord(a.ev[2], stream);
   attn_bwd_dq_kernel<D><<<grid, 256, BwdSmem<D>::BYTES, stream>>>(
       mq, mk, mv, mdo, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
       scale_log2);
+  if (a.ev[3]) cudaEventRecord(a.ev[3], stream);
   return cudaGetLastError();
 }
 
@@ -719,6 +723,7 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   const float scale_log2 = a.softmax_scale * kLog2e;
   dim3 grid(a.S / TILE, a.H);
+  if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
   if (a.D == 128) {
     static std::once_flag f;
     std::call_once(f, [] {
@@ -736,6 +741,7 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
     attn_fwd_kernel<64><<<grid, 256, FwdSmem<64>::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
                                                                     a.H, scale_log2);
   }
+  if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
   return cudaGetLastError();
 }
 

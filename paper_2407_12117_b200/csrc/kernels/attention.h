@@ -13,6 +13,7 @@ struct AttnFwdArgs {
   float* lse;              // [H, S], natural log
   int S, H, D;
   float softmax_scale;
+  cudaEvent_t ev[2] = {nullptr, nullptr};  // optional: recorded around the kernel
 };
 cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream);
 
@@ -32,6 +33,7 @@ struct AttnBwdArgs {
   long long pos0;
   int S, H, D;
   float softmax_scale;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional: before prep, after prep, after dkdv, after dq
 };
 cudaError_t attn_bwd(const AttnBwdArgs& a, cudaStream_t stream);
 

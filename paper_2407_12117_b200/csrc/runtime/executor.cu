@@ -1,0 +1,836 @@
+// executor.cu — real execution of MEMO's training step on one B200.
+//
+// Memory: ONE cudaMalloc holds [params bf16 | master f32 | adam m | adam v |
+// grads f32 | RB0 | RB1 | transient arena | misc]; every activation pointer is
+// base + a static offset.  Skeletal activations of layer i live in rounding
+// buffer RB[i % 2]; the transient arena is laid out by the
+// bi-level planner (plan_iteration == reference plan_model, bit-exact) over
+// the executor's own request trace, emitted below in the reference trace
+// format (trace.hpp:262).  No allocation happens inside a step.
+//
+// Streams: compute, offload (D2H), prefetch (H2D).  Dependencies, all by
+// cudaEvents, never host syncs:
+//   F1  layers run in order on the compute stream
+//   F2  offload(i) waits fwd(i) done; offloads are FIFO on their stream
+//   F3  fwd(i+2) waits offload(i) (RB[i%2] drained); additionally the last
+//       GEMM of fwd(i+1) — which writes layer i+2's input into RB[i%2] —
+//       waits offload(i), which F3 implies
+//   B2  prefetch(i) waits bwd(i+2) done (RB[i%2] free again)
+//   B3  recompute(i) waits the mandatory part of prefetch(i) (layer input and
+//       attention output; SURVEY discovery 9), bwd(i) waits all of prefetch(i)
+// Token-wise split (swap.hpp:177): rows [0, swap) of the non-mandatory
+// components are offloaded, rows [swap, S) are recomputed from the restored
+// layer input and attention output (attention itself is not recomputed).
+#include "runtime/executor.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "kernels/attention.h"
+#include "kernels/elementwise.h"
+#include "kernels/gemm_tc.h"
+
+namespace memo {
+namespace {
+
+struct CudaError : PlanError {
+  explicit CudaError(const std::string& w) : PlanError(1, w) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr Bytes kAlign = 2ull << 20;
+Bytes up(Bytes v, Bytes a = kAlign) { return (v + a - 1) / a * a; }
+
+enum Comp { C_X = 0, C_XN, C_Q, C_K, C_V, C_O, C_A, C_XN2, C_GU, C_ACT, C_N };
+
+// Request-trace builder: names are resolved to ids per segment; skeletal
+// tensors are keyed by layer so their free in the backward segment matches.
+class TraceBuilder {
+ public:
+  std::size_t begin(Phase p, int layer) {
+    Segment s;
+    s.phase = p;
+    s.layer = layer;
+    t_.segs.push_back(s);
+    return t_.segs.size() - 1;
+  }
+  void malloc(const std::string& key, Bytes bytes, const std::string& name) {
+    const TensorId id = next_++;
+    ids_[key] = {id, bytes};
+    names_[id] = {t_.segs.size() - 1, name};
+    t_.segs.back().reqs.push_back({true, id, bytes});
+  }
+  void free(const std::string& key) {
+    auto it = ids_.at(key);
+    t_.segs.back().reqs.push_back({false, it.first, it.second});
+  }
+  Trace& trace() { return t_; }
+  const std::map<TensorId, std::pair<std::size_t, std::string>>& names() const { return names_; }
+
+ private:
+  Trace t_;
+  TensorId next_ = 1;
+  std::map<std::string, std::pair<TensorId, Bytes>> ids_;
+  std::map<TensorId, std::pair<std::size_t, std::string>> names_;
+};
+
+std::string lkey(int layer, const char* n) { return "L" + std::to_string(layer) + "/" + n; }
+
+}  // namespace
+
+Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const ExecOptions& opt)
+    : cfg_(cfg_in), hw_(hw), opt_(opt) {
+  cfg_.validate();
+  hw_.validate();
+  if (cfg_.batch != 1) throw ConfigError("executor supports batch == 1 (MEMO's long-context setting)");
+  if (cfg_.tp_degree != 1 || cfg_.sp_or_cp_degree != 1)
+    throw ConfigError("single-GPU executor: tp_degree and sp_or_cp_degree must be 1");
+  if (cfg_.dtype_bytes != 2) throw ConfigError("executor computes in bf16 (dtype_bytes = 2)");
+  if ((cfg_.ffn_hidden * 2) % 3) throw ConfigError("ffn_hidden must be 1.5 x the SwiGLU width");
+  d_.S = static_cast<int>(cfg_.seq_len);
+  d_.h = static_cast<int>(cfg_.hidden);
+  d_.H = static_cast<int>(cfg_.n_heads);
+  d_.D = d_.h / d_.H;
+  d_.F = static_cast<int>(cfg_.ffn_hidden * 2 / 3);
+  d_.V = static_cast<int>(cfg_.vocab);
+  d_.n = static_cast<int>(cfg_.n_layers);
+  if (d_.h % d_.H || (d_.D != 64 && d_.D != 128)) throw ConfigError("head_dim must be 64 or 128");
+  if (d_.S % 128 || d_.h % 256 || d_.F % 256 || d_.V % 256)
+    throw ConfigError("seq_len % 128, hidden % 256, intermediate % 256 and vocab % 256 must be 0");
+  if (opt_.ce_chunk <= 0 || opt_.ce_chunk % 128) throw ConfigError("ce_chunk must be a positive multiple of 128");
+
+  // The executor's saved tensors define the skeletal weights (multiples of
+  // b*s*h*dtype bytes); LSE (f32 [H,S]) rides in attn_out.
+  const double h = d_.h, F = d_.F;
+  row_bytes_ = {4ull * d_.h, 2ull * d_.h, 2ull * d_.h, 2ull * d_.h, 2ull * d_.h, 2ull * d_.h,
+                2ull * d_.h, 2ull * d_.h, 4ull * d_.F, 2ull * d_.F};
+  const double w[C_N] = {2.0, 1.0, 1.0, 1.0, 1.0, 1.0 + 2.0 / d_.D, 1.0, 1.0, 2.0 * F / h, F / h};
+  cfg_.skeletal_weight_overrides.clear();
+  for (int c = 0; c < C_N; ++c) cfg_.skeletal_weight_overrides[kSkeletalNames[c]] = w[c];
+  sk_ = skeletal_of(cfg_);
+  rb_bytes_ = 0;
+  rb_off_.resize(C_N);
+  for (int c = 0; c < C_N; ++c) {
+    rb_off_[c] = rb_bytes_;
+    rb_bytes_ += sk_.components[c].second;
+  }
+  {
+    const Bytes want = static_cast<Bytes>(d_.S) * (4ull * d_.h + 2ull * d_.h * 7 + 6ull * d_.F) +
+                       4ull * d_.H * d_.S;
+    if (want != rb_bytes_) throw PlanError(1, "internal: skeletal model does not match executor layout");
+  }
+
+  // alpha and the token split (swap.hpp:105, schedule.hpp:409, swap.hpp:177)
+  Timing tm = timing_of(cfg_, hw_, params_of(cfg_));
+  const double t_layer = opt_.t_layer > 0 ? opt_.t_layer : tm.t_fwd_layer;
+  swap_ = opt_.alpha >= 0 ? swap_with_alpha(sk_, hw_, opt_.alpha, cfg_.n_layers)
+                          : solve_alpha_for(sk_, hw_, t_layer, cfg_.n_layers);
+  split_ = split_tokens(swap_.alpha, cfg_.seq_local(), opt_.token_granularity);
+  can_swap_ = swap_on_ = opt_.swap_enabled;
+
+  build_trace_and_plan();
+  compute_layout();
+  if (opt_.dry_run) return;  // host-only: trace, plan, alpha and sizes (no CUDA)
+  allocate();
+  init_weights();
+}
+
+void Executor::build_trace_and_plan() {
+  const Bytes S = d_.S, h = d_.h, F = d_.F, V = d_.V, H = d_.H;
+  const Bytes T = std::min<Bytes>(static_cast<Bytes>(opt_.ce_chunk), S);
+  const Bytes P = static_cast<Bytes>(rmsnorm_bwd_partials(d_.S));
+  const Bytes R = split_.recompute_tokens;
+  TraceBuilder tb;
+  seg_emb_fwd_ = tb.begin(Phase::EmbFwd, -1);
+  tb.malloc("x_final", S * h * 4, "x_final");
+  tb.malloc("dx_carry", S * h * 4, "dx_carry");
+  tb.malloc("dxb_carry", S * h * 2, "dxb_carry");
+  for (int i = 0; i < d_.n; ++i) {
+    seg_fwd_.push_back(tb.begin(Phase::LayerFwd, i));
+    for (int c = 0; c <= C_A; ++c)
+      tb.malloc(lkey(i, kSkeletalNames[c]), sk_.components[c].second, kSkeletalNames[c]);
+    tb.malloc(lkey(i, "x1"), S * h * 4, "x1");
+    for (int c = C_XN2; c < C_N; ++c)
+      tb.malloc(lkey(i, kSkeletalNames[c]), sk_.components[c].second, kSkeletalNames[c]);
+    tb.free(lkey(i, "x1"));
+  }
+  seg_cls_fwd_ = tb.begin(Phase::ClsFwd, -1);
+  tb.malloc("xf", S * h * 2, "xf");
+  seg_cls_bwd_ = tb.begin(Phase::ClsBwd, -1);
+  tb.malloc("dxf", S * h * 4, "dxf");
+  tb.malloc("loss_rows", S * 4, "loss_rows");
+  tb.malloc("logits", T * V * 4, "logits");
+  tb.malloc("dlogits", T * V * 2, "dlogits");
+  tb.free("logits");
+  tb.free("dlogits");
+  tb.free("loss_rows");
+  tb.malloc("cls_part", P * h * 4, "cls_part");
+  tb.free("cls_part");
+  tb.free("dxf");
+  tb.free("xf");
+  seg_bwd_.assign(d_.n, 0);
+  for (int i = d_.n - 1; i >= 0; --i) {
+    seg_bwd_[i] = tb.begin(Phase::LayerBwd, i);
+    auto m = [&](const char* n, Bytes b) { tb.malloc(lkey(i, n), b, n); };
+    auto f = [&](const char* n) { tb.free(lkey(i, n)); };
+    if (R > 0) {  // every layer carries the recompute buffer so segments stay identical
+      m("x1_rec", R * h * 4);
+      f("x1_rec");
+    }
+    m("dact", S * F * 2);
+    m("dgu", S * 2 * F * 2);
+    f("dact");
+    m("dxn2", S * h * 4);
+    f("dgu");
+    m("da", S * h * 2);
+    m("part2", P * h * 4);
+    f("part2");
+    f("dxn2");
+    m("dout", S * h * 2);
+    f("da");
+    m("attn_ws", 2 * H * S * 4);
+    m("dqkv", S * 3 * h * 2);
+    f("attn_ws");
+    f("dout");
+    m("dxn", S * h * 4);
+    f("dqkv");
+    m("part1", P * h * 4);
+    f("part1");
+    f("dxn");
+    for (int c = C_N - 1; c >= 0; --c) tb.free(lkey(i, kSkeletalNames[c]));
+  }
+  seg_emb_bwd_ = tb.begin(Phase::EmbBwd, -1);
+  tb.free("dxb_carry");
+  tb.free("dx_carry");
+  tb.free("x_final");
+  Trace& t = tb.trace();
+  t.n_layers = d_.n;
+  trace_text_ = trace_to_text(t);
+  ModelPlan mp = plan_iteration(t, 0, opt_.plan_time_budget, opt_.alignment);
+  plan_json_ = plan_to_json(mp);
+  if (!mp.optimal) throw PlanningError("bi-level plan not proven optimal within the time budget");
+  arena_bytes_ = mp.total_peak;
+  for (const AbsAddr& a : mp.absolute) {
+    const auto& nm = tb.names().at(a.id);
+    arena_off_[{a.segment, nm.second}] = a.offset;
+  }
+}
+
+void* Executor::arena_ptr(std::size_t seg, const char* name) const {
+  auto it = arena_off_.find({seg, name});
+  if (it == arena_off_.end()) throw PlanError(1, std::string("internal: no arena slot for ") + name);
+  return arena_ + it->second;
+}
+
+void Executor::compute_layout() {
+  const long long h = d_.h, F = d_.F, V = d_.V;
+  long long off = 0;
+  auto add = [&](const std::string& n, int layer, long long cnt) {
+    ptab_[{n, layer}] = {off, cnt};
+    off += cnt;
+  };
+  add("embedding", -1, V * h);
+  for (int l = 0; l < d_.n; ++l) {
+    add("g1", l, h);
+    add("wqkv", l, 3 * h * h);
+    add("wo", l, h * h);
+    add("g2", l, h);
+    add("wgu", l, 2 * F * h);
+    add("wd", l, h * F);
+  }
+  add("gf", -1, h);
+  add("wcls", -1, V * h);
+  n_params_ = off;
+  const Bytes Pn = static_cast<Bytes>(n_params_);
+  const Bytes sz_params = up(Pn * 2), sz_f32 = up(Pn * 4);
+  state_bytes_ = sz_params + 4 * sz_f32;
+  const Bytes S = d_.S;
+  const Bytes misc = up(S * (d_.D / 2) * 8 + S * 4 * 3 + (V + 1) * 4 + 1024);
+  const int n_rb = swap_on_ ? 2 : d_.n;
+  dev_bytes_ = state_bytes_ + n_rb * up(rb_bytes_) + up(arena_bytes_) + misc;
+  // pinned host slots for the n-2 swapped layers
+  host_slot_.assign(d_.n, 0);
+  per_layer_host_ = sk_.components[C_X].second + sk_.components[C_O].second;
+  for (int c = 0; c < C_N; ++c)
+    if (c != C_X && c != C_O) per_layer_host_ += split_.swap_tokens * row_bytes_[c];
+  const int swapped = d_.n >= 3 ? d_.n - 2 : 0;
+  pinned_bytes_ = can_swap_ ? per_layer_host_ * swapped : 0;
+  for (int i = 0; i < swapped; ++i) host_slot_[i] = per_layer_host_ * i;
+}
+
+void Executor::allocate() {
+  const Bytes Pn = static_cast<Bytes>(n_params_);
+  const Bytes sz_params = up(Pn * 2), sz_f32 = up(Pn * 4);
+  const Bytes S = d_.S;
+  const long long V = d_.V;
+  const int n_rb = swap_on_ ? 2 : d_.n;
+  size_t free_b = 0, total_b = 0;
+  ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+  const Bytes reserve = 1ull << 30;  // cuBLAS-free, but leave room for the CUDA context / TMA maps
+  if (dev_bytes_ + reserve > free_b)
+    throw InfeasibleError("arena " + std::to_string(arena_bytes_) + " + rounding buffers " +
+                          std::to_string(n_rb * rb_bytes_) + " + states " + std::to_string(state_bytes_) +
+                          " exceed free HBM " + std::to_string(free_b));
+  void* p = nullptr;
+  ck(cudaMalloc(&p, dev_bytes_), "cudaMalloc(arena)");
+  dev_ = static_cast<char*>(p);
+  char* q = dev_;
+  params_ = reinterpret_cast<__nv_bfloat16*>(q); q += sz_params;
+  master_ = reinterpret_cast<float*>(q); q += sz_f32;
+  adam_m_ = reinterpret_cast<float*>(q); q += sz_f32;
+  adam_v_ = reinterpret_cast<float*>(q); q += sz_f32;
+  grads_ = reinterpret_cast<float*>(q); q += sz_f32;
+  rb_base_.assign(n_rb, nullptr);
+  for (int r = 0; r < n_rb; ++r) {
+    rb_base_[r] = q;
+    q += up(rb_bytes_);
+  }
+  arena_ = q; q += up(arena_bytes_);
+  rope_ = reinterpret_cast<float2*>(q); q += S * (d_.D / 2) * 8;
+  tok_ = reinterpret_cast<int*>(q); q += S * 4;
+  lab_ = reinterpret_cast<int*>(q); q += S * 4;
+  csr_pos_ = reinterpret_cast<int*>(q); q += S * 4;
+  csr_off_ = reinterpret_cast<int*>(q); q += (V + 1) * 4;
+  loss_dev_ = reinterpret_cast<float*>(up(reinterpret_cast<uintptr_t>(q), 256));
+
+  if (pinned_bytes_ > 0) {
+    void* hp = nullptr;
+    if (cudaHostAlloc(&hp, pinned_bytes_, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      throw CpuInfeasibleError("cannot pin " + std::to_string(pinned_bytes_) +
+                               " bytes of host memory for the swap slots");
+    }
+    pinned_ = static_cast<char*>(hp);
+  }
+  void* sp = nullptr;
+  ck(cudaHostAlloc(&sp, S * 4 * 3 + (V + 1) * 4 + 64, cudaHostAllocDefault), "cudaHostAlloc(staging)");
+  staging_ = static_cast<char*>(sp);
+  loss_host_ = reinterpret_cast<float*>(staging_ + S * 4 * 3 + (V + 1) * 4);
+
+  ck(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&os_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&ps_, cudaStreamNonBlocking), "stream");
+  auto mk = [&](std::vector<cudaEvent_t>& v) {
+    v.resize(d_.n);
+    for (auto& e : v) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  };
+  mk(ev_fwd_done_);
+  mk(ev_bwd_done_);
+  mk(ev_off_done_);
+  mk(ev_pre_mand_);
+  mk(ev_pre_done_);
+  ck(cudaEventCreate(&ev_start_), "event");
+
+  // RoPE table (cos, sin) in double -> f32, identical to the CPU oracle.
+  std::vector<float2> cs(static_cast<size_t>(S) * (d_.D / 2));
+  for (Bytes t = 0; t < S; ++t)
+    for (int p2 = 0; p2 < d_.D / 2; ++p2) {
+      const double inv = std::pow(static_cast<double>(opt_.rope_theta), -2.0 * p2 / d_.D);
+      const double ang = static_cast<double>(t) * inv;
+      cs[t * (d_.D / 2) + p2] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    }
+  ck(cudaMemcpy(rope_, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice), "rope upload");
+}
+
+void Executor::init_weights() {
+  for (const auto& [key, v] : ptab_) {
+    const auto& [name, layer] = key;
+    const auto [o, n] = v;
+    uint64_t tid;
+    if (name == "embedding") tid = 0;
+    else if (name == "gf") tid = 1 + 6ull * d_.n;
+    else if (name == "wcls") tid = 2 + 6ull * d_.n;
+    else {
+      static const char* order[] = {"g1", "wqkv", "wo", "g2", "wgu", "wd"};
+      int k = 0;
+      while (name != order[k]) ++k;
+      tid = 1 + 6ull * layer + k;
+    }
+    const bool is_norm = name == "g1" || name == "g2" || name == "gf";
+    ck(init_uniform(params_ + o, master_ + o, n, opt_.seed, tid, is_norm, cs_), "init_uniform");
+  }
+  ck(cudaMemsetAsync(adam_m_, 0, n_params_ * 4, cs_), "memset");
+  ck(cudaMemsetAsync(adam_v_, 0, n_params_ * 4, cs_), "memset");
+  ck(cudaStreamSynchronize(cs_), "init sync");
+}
+
+Executor::~Executor() {
+  if (opt_.dry_run) return;
+  if (cs_) cudaStreamSynchronize(cs_);
+  if (os_) cudaStreamSynchronize(os_);
+  if (ps_) cudaStreamSynchronize(ps_);
+  for (auto* v : {&ev_fwd_done_, &ev_bwd_done_, &ev_off_done_, &ev_pre_mand_, &ev_pre_done_, &ev_pool_})
+    for (auto e : *v) cudaEventDestroy(e);
+  if (ev_start_) cudaEventDestroy(ev_start_);
+  if (cs_) cudaStreamDestroy(cs_);
+  if (os_) cudaStreamDestroy(os_);
+  if (ps_) cudaStreamDestroy(ps_);
+  if (dev_) cudaFree(dev_);
+  if (pinned_) cudaFreeHost(pinned_);
+  if (staging_) cudaFreeHost(staging_);
+}
+
+cudaEvent_t Executor::take_event() {
+  if (ev_used_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event");
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_used_++];
+}
+
+void Executor::gemm(const GemmDesc& g) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (opt_.op_timing) {
+    a = take_event();
+    b = take_event();
+    ck(cudaEventRecord(a, cs_), "record");
+  }
+  ck(gemm_tc(g, cs_), "gemm_tc");
+  stats_.kernel_launches += 1;
+  if (opt_.op_timing) {
+    ck(cudaEventRecord(b, cs_), "record");
+    ops_.push_back({OP_GEMM, a, b, 2.0 * g.M * static_cast<double>(g.N) * g.K});
+  }
+}
+
+void Executor::attention_fwd(AttnFwdArgs a) {
+  if (opt_.op_timing) {
+    a.ev[0] = take_event();
+    a.ev[1] = take_event();
+  }
+  ck(attn_fwd(a, cs_), "attn_fwd");
+  stats_.kernel_launches += 1;
+  if (opt_.op_timing) {
+    const double s = a.S, hh = static_cast<double>(a.H) * a.D;
+    ops_.push_back({OP_ATTN_FWD, a.ev[0], a.ev[1], 2.0 * s * s * hh});  // causal 2*s^2*h
+  }
+}
+
+void Executor::attention_bwd(AttnBwdArgs a) {
+  if (opt_.op_timing)
+    for (auto& e : a.ev) e = take_event();
+  ck(attn_bwd(a, cs_), "attn_bwd");
+  stats_.kernel_launches += 3;
+  if (opt_.op_timing) {
+    const double s = a.S, hh = static_cast<double>(a.H) * a.D;
+    ops_.push_back({OP_ATTN_PREP, a.ev[0], a.ev[1], 0.0});
+    ops_.push_back({OP_ATTN_DKDV, a.ev[1], a.ev[2], 4.0 * s * s * hh});  // S^T, dP^T, dV, dK
+    ops_.push_back({OP_ATTN_DQ, a.ev[2], a.ev[3], 3.0 * s * s * hh});    // S, dP, dQ
+  }
+}
+
+void Executor::mark(int stream, int kind, int layer, bool begin) {
+  cudaStream_t s = stream == 0 ? cs_ : (stream == 1 ? os_ : ps_);
+  cudaEvent_t e = take_event();
+  ck(cudaEventRecord(e, s), "eventRecord");
+  if (begin) {
+    marks_.push_back({stream, kind, layer, e, nullptr});
+  } else {
+    for (auto it = marks_.rbegin(); it != marks_.rend(); ++it)
+      if (it->stream == stream && it->kind == kind && it->layer == layer && !it->e) {
+        it->e = e;
+        break;
+      }
+  }
+}
+
+bool Executor::tensor(const std::string& name, int layer, void** ptr, size_t* bytes) const {
+  std::string base = name;
+  char* arr = reinterpret_cast<char*>(params_);
+  size_t esz = 2;
+  if (name.rfind("grad/", 0) == 0) {
+    base = name.substr(5);
+    arr = reinterpret_cast<char*>(grads_);
+    esz = 4;
+  } else if (name.rfind("master/", 0) == 0) {
+    base = name.substr(7);
+    arr = reinterpret_cast<char*>(master_);
+    esz = 4;
+  }
+  if (base == "all") {
+    *ptr = arr;
+    *bytes = static_cast<size_t>(n_params_) * esz;
+    return true;
+  }
+  if (name.rfind("act/", 0) == 0) {  // skeletal activation component of a layer's RB
+    for (int c = 0; c < C_N; ++c)
+      if (name.substr(4) == kSkeletalNames[c] && layer >= 0 && layer < d_.n) {
+        *ptr = comp(layer, c);
+        *bytes = sk_.components[c].second;
+        return true;
+      }
+    return false;
+  }
+  auto it = ptab_.find({base, layer});
+  if (it == ptab_.end()) return false;
+  *ptr = arr + it->second.first * esz;
+  *bytes = static_cast<size_t>(it->second.second) * esz;
+  return true;
+}
+
+// ------------------------------------------------------------------ step
+namespace {
+GemmDesc gd(int M, int N, int K, const void* a, long long lda, int amn, const void* b,
+            long long ldb, int bmn, int epi, void* c, long long ldc) {
+  GemmDesc g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.a = a;
+  g.lda = lda;
+  g.a_mn_major = amn;
+  g.b = b;
+  g.ldb = ldb;
+  g.b_mn_major = bmn;
+  g.epi = epi;
+  g.c = c;
+  g.ldc = ldc;
+  return g;
+}
+}  // namespace
+
+void Executor::load_batch(const int* tokens, const int* labels) {
+  const int S = d_.S, V = d_.V;
+  int* st = reinterpret_cast<int*>(staging_);
+  std::memcpy(st, tokens, S * 4);
+  std::memcpy(st + S, labels, S * 4);
+  // counting sort of positions by token id -> CSR for the deterministic embedding gradient
+  int* pos = st + 2 * S;
+  int* offs = st + 3 * S;
+  std::fill(offs, offs + V + 1, 0);
+  for (int t = 0; t < S; ++t) {
+    if (tokens[t] < 0 || tokens[t] >= V) throw ConfigError("token id out of range");
+    ++offs[tokens[t] + 1];
+  }
+  for (int v = 0; v < V; ++v) offs[v + 1] += offs[v];
+  std::vector<int> fillp(offs, offs + V);
+  for (int t = 0; t < S; ++t) pos[fillp[tokens[t]]++] = t;
+  n_labeled_ = 0;
+  for (int t = 0; t < S; ++t) n_labeled_ += labels[t] >= 0;
+  if (n_labeled_ == 0) throw ConfigError("batch has no labeled tokens");
+  // tok | lab | csr_pos | csr_off are contiguous on both sides
+  ck(cudaMemcpyAsync(tok_, staging_, static_cast<size_t>(3 * S + V + 1) * 4, cudaMemcpyHostToDevice, cs_),
+     "H2D batch");
+  stats_.h2d_bytes = static_cast<double>(3 * S + V + 1) * 4;
+}
+
+void Executor::offload(int i) {
+  ck(cudaStreamWaitEvent(os_, ev_fwd_done_[i], 0), "wait");
+  mark(1, static_cast<int>(Kind::Offload), i, true);
+  // Host slot layout (shared with prefetch): [layer_input | attn_out(+LSE) |
+  // prefix rows of the other components in emission order].
+  char* host = pinned_ + host_slot_[i];
+  Bytes moved = 0;
+  auto put = [&](int c, Bytes b) {
+    if (b == 0) return;
+    ck(cudaMemcpyAsync(host, comp(i, c), b, cudaMemcpyDeviceToHost, os_), "D2H offload");
+    host += b;
+    moved += b;
+  };
+  put(C_X, sk_.components[C_X].second);
+  put(C_O, sk_.components[C_O].second);
+  for (int c = 0; c < C_N; ++c)
+    if (c != C_X && c != C_O) put(c, split_.swap_tokens * row_bytes_[c]);
+  stats_.offload_bytes += static_cast<double>(moved);
+  mark(1, static_cast<int>(Kind::Offload), i, false);
+  ck(cudaEventRecord(ev_off_done_[i], os_), "record");
+}
+
+void Executor::prefetch(int i) {
+  ck(cudaStreamWaitEvent(ps_, ev_bwd_done_[i + 2], 0), "wait");
+  mark(2, static_cast<int>(Kind::Prefetch), i, true);
+  const char* host = pinned_ + host_slot_[i];
+  Bytes moved = 0;
+  // mandatory first (layer input, attention output + LSE): recompute needs them
+  const Bytes bx = sk_.components[C_X].second, bo = sk_.components[C_O].second;
+  ck(cudaMemcpyAsync(comp(i, C_X), host, bx, cudaMemcpyHostToDevice, ps_), "H2D");
+  ck(cudaMemcpyAsync(comp(i, C_O), host + bx, bo, cudaMemcpyHostToDevice, ps_), "H2D");
+  ck(cudaEventRecord(ev_pre_mand_[i], ps_), "record");
+  moved += bx + bo;
+  const char* hp = host + bx + bo;
+  for (int c = 0; c < C_N; ++c) {
+    if (c == C_X || c == C_O) continue;
+    const Bytes b = split_.swap_tokens * row_bytes_[c];
+    if (b == 0) continue;
+    ck(cudaMemcpyAsync(comp(i, c), hp, b, cudaMemcpyHostToDevice, ps_), "H2D");
+    hp += b;
+    moved += b;
+  }
+  stats_.prefetch_bytes += static_cast<double>(moved);
+  mark(2, static_cast<int>(Kind::Prefetch), i, false);
+  ck(cudaEventRecord(ev_pre_done_[i], ps_), "record");
+}
+
+#define G(expr) ck(expr, #expr)
+
+void Executor::layer_fwd(int i) {
+  const int S = d_.S, h = d_.h, F = d_.F, H = d_.H, D = d_.D;
+  if (i >= 2 && swaps(i - 2)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 2], 0));  // F3
+  mark(0, static_cast<int>(Kind::LayerFwd), i, true);
+  const std::size_t seg = seg_fwd_[i];
+  auto P = [&](const char* n) { return params_ + ptab_.at({n, i}).first; };
+  float* X = reinterpret_cast<float*>(comp(i, C_X));
+  auto* XN = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN));
+  auto* Q = reinterpret_cast<__nv_bfloat16*>(comp(i, C_Q));
+  auto* K = reinterpret_cast<__nv_bfloat16*>(comp(i, C_K));
+  auto* Vv = reinterpret_cast<__nv_bfloat16*>(comp(i, C_V));
+  auto* O = reinterpret_cast<__nv_bfloat16*>(comp(i, C_O));
+  float* LSE = reinterpret_cast<float*>(comp(i, C_O) + static_cast<Bytes>(S) * h * 2);
+  auto* A = reinterpret_cast<__nv_bfloat16*>(comp(i, C_A));
+  auto* XN2 = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN2));
+  auto* GU = reinterpret_cast<__nv_bfloat16*>(comp(i, C_GU));
+  auto* ACT = reinterpret_cast<__nv_bfloat16*>(comp(i, C_ACT));
+  float* x1 = static_cast<float*>(arena_ptr(seg, "x1"));
+
+  G(rmsnorm_fwd(X, nullptr, P("g1"), XN, S, h, opt_.eps, cs_));
+  GemmDesc g = gd(S, 3 * h, h, XN, h, 0, P("wqkv"), h, 0, GEMM_EPI_QKV_ROPE, nullptr, 0);
+  g.q = Q; g.k = K; g.v = Vv; g.hidden = h; g.head_dim = D; g.rope = rope_; g.pos0 = 0;
+  gemm(g);
+  AttnFwdArgs fa{Q, K, Vv, O, LSE, S, H, D, 1.0f / std::sqrt(static_cast<float>(D))};
+  attention_fwd(fa);
+  g = gd(S, h, h, O, h, 0, P("wo"), h, 0, GEMM_EPI_RESID, A, h);
+  g.out_f32 = x1; g.resid = X; g.ld_f32 = h;
+  gemm(g);
+  G(rmsnorm_fwd(x1, nullptr, P("g2"), XN2, S, h, opt_.eps, cs_));
+  gemm(gd(S, 2 * F, h, XN2, h, 0, P("wgu"), h, 0, GEMM_EPI_BF16, GU, 2 * F));
+  G(swiglu_fwd(GU, ACT, S, F, cs_));
+  float* out = i + 1 < d_.n ? reinterpret_cast<float*>(comp(i + 1, C_X))
+                            : static_cast<float*>(arena_ptr(seg_emb_fwd_, "x_final"));
+  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 1], 0));  // RB drained
+  g = gd(S, h, F, ACT, F, 0, P("wd"), F, 0, GEMM_EPI_RESID, nullptr, 0);
+  g.out_f32 = out; g.resid = x1; g.ld_f32 = h;
+  gemm(g);
+  stats_.kernel_launches += 3;  // 2 rmsnorm_fwd + swiglu (GEMM/attention counted in wrappers)
+  mark(0, static_cast<int>(Kind::LayerFwd), i, false);
+  G(cudaEventRecord(ev_fwd_done_[i], cs_));
+  if (swaps(i)) offload(i);
+}
+
+void Executor::layer_recompute(int i) {
+  const int h = d_.h, F = d_.F, D = d_.D;
+  const int s0 = static_cast<int>(split_.swap_tokens), R = static_cast<int>(split_.recompute_tokens);
+  G(cudaStreamWaitEvent(cs_, ev_pre_mand_[i], 0));  // B3 (+ prefetch-before-recompute)
+  mark(0, static_cast<int>(Kind::Recompute), i, true);
+  if (R > 0) {
+    const std::size_t seg = seg_bwd_[i];
+    auto P = [&](const char* n) { return params_ + ptab_.at({n, i}).first; };
+    const Bytes r0 = static_cast<Bytes>(s0);
+    float* X = reinterpret_cast<float*>(comp(i, C_X)) + r0 * h;
+    auto* XN = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN)) + r0 * h;
+    auto* Q = reinterpret_cast<__nv_bfloat16*>(comp(i, C_Q)) + r0 * h;
+    auto* K = reinterpret_cast<__nv_bfloat16*>(comp(i, C_K)) + r0 * h;
+    auto* Vv = reinterpret_cast<__nv_bfloat16*>(comp(i, C_V)) + r0 * h;
+    auto* O = reinterpret_cast<__nv_bfloat16*>(comp(i, C_O)) + r0 * h;
+    auto* A = reinterpret_cast<__nv_bfloat16*>(comp(i, C_A)) + r0 * h;
+    auto* XN2 = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN2)) + r0 * h;
+    auto* GU = reinterpret_cast<__nv_bfloat16*>(comp(i, C_GU)) + r0 * 2 * F;
+    auto* ACT = reinterpret_cast<__nv_bfloat16*>(comp(i, C_ACT)) + r0 * F;
+    float* x1 = static_cast<float*>(arena_ptr(seg, "x1_rec"));
+    G(rmsnorm_fwd(X, nullptr, P("g1"), XN, R, h, opt_.eps, cs_));
+    GemmDesc g = gd(R, 3 * h, h, XN, h, 0, P("wqkv"), h, 0, GEMM_EPI_QKV_ROPE, nullptr, 0);
+    g.q = Q; g.k = K; g.v = Vv; g.hidden = h; g.head_dim = D; g.rope = rope_; g.pos0 = s0;
+    gemm(g);
+    g = gd(R, h, h, O, h, 0, P("wo"), h, 0, GEMM_EPI_RESID, A, h);
+    g.out_f32 = x1; g.resid = X; g.ld_f32 = h;
+    gemm(g);
+    G(rmsnorm_fwd(x1, nullptr, P("g2"), XN2, R, h, opt_.eps, cs_));
+    gemm(gd(R, 2 * F, h, XN2, h, 0, P("wgu"), h, 0, GEMM_EPI_BF16, GU, 2 * F));
+    G(swiglu_fwd(GU, ACT, R, F, cs_));
+    stats_.kernel_launches += 3;
+  }
+  mark(0, static_cast<int>(Kind::Recompute), i, false);
+}
+
+void Executor::layer_bwd(int i) {
+  const int S = d_.S, h = d_.h, F = d_.F, H = d_.H, D = d_.D;
+  if (swaps(i)) G(cudaStreamWaitEvent(cs_, ev_pre_done_[i], 0));  // B3
+  mark(0, static_cast<int>(Kind::LayerBwd), i, true);
+  const std::size_t seg = seg_bwd_[i];
+  auto P = [&](const char* n) { return params_ + ptab_.at({n, i}).first; };
+  auto Gr = [&](const char* n) { return grads_ + ptab_.at({n, i}).first; };
+  float* X = reinterpret_cast<float*>(comp(i, C_X));
+  auto* XN = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN));
+  auto* Q = reinterpret_cast<__nv_bfloat16*>(comp(i, C_Q));
+  auto* K = reinterpret_cast<__nv_bfloat16*>(comp(i, C_K));
+  auto* Vv = reinterpret_cast<__nv_bfloat16*>(comp(i, C_V));
+  auto* O = reinterpret_cast<__nv_bfloat16*>(comp(i, C_O));
+  float* LSE = reinterpret_cast<float*>(comp(i, C_O) + static_cast<Bytes>(S) * h * 2);
+  auto* A = reinterpret_cast<__nv_bfloat16*>(comp(i, C_A));
+  auto* XN2 = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN2));
+  auto* GU = reinterpret_cast<__nv_bfloat16*>(comp(i, C_GU));
+  auto* ACT = reinterpret_cast<__nv_bfloat16*>(comp(i, C_ACT));
+  float* dxc = static_cast<float*>(arena_ptr(seg_emb_fwd_, "dx_carry"));
+  auto* dxb = static_cast<__nv_bfloat16*>(arena_ptr(seg_emb_fwd_, "dxb_carry"));
+  auto* dact = static_cast<__nv_bfloat16*>(arena_ptr(seg, "dact"));
+  auto* dgu = static_cast<__nv_bfloat16*>(arena_ptr(seg, "dgu"));
+  float* dxn2 = static_cast<float*>(arena_ptr(seg, "dxn2"));
+  auto* da = static_cast<__nv_bfloat16*>(arena_ptr(seg, "da"));
+  float* part2 = static_cast<float*>(arena_ptr(seg, "part2"));
+  auto* dout = static_cast<__nv_bfloat16*>(arena_ptr(seg, "dout"));
+  float* ws = static_cast<float*>(arena_ptr(seg, "attn_ws"));
+  auto* dqkv = static_cast<__nv_bfloat16*>(arena_ptr(seg, "dqkv"));
+  float* dxn = static_cast<float*>(arena_ptr(seg, "dxn"));
+  float* part1 = static_cast<float*>(arena_ptr(seg, "part1"));
+
+  // MLP: dact = dY Wd ; dWd = dY^T act ; SwiGLU bwd ; dxn2 = dGU Wgu ; dWgu = dGU^T xn2
+  gemm(gd(S, F, h, dxb, h, 0, P("wd"), F, 1, GEMM_EPI_BF16, dact, F));
+  gemm(gd(h, F, S, dxb, h, 1, ACT, F, 1, GEMM_EPI_F32, Gr("wd"), F));
+  G(swiglu_bwd(GU, dact, dgu, S, F, cs_));
+  gemm(gd(S, h, 2 * F, dgu, 2 * F, 0, P("wgu"), h, 1, GEMM_EPI_F32, dxn2, h));
+  gemm(gd(2 * F, h, S, dgu, 2 * F, 1, XN2, h, 1, GEMM_EPI_F32, Gr("wgu"), h));
+  // post-attention norm: x1 = x + a recomputed inside the kernel
+  G(rmsnorm_bwd(X, A, P("g2"), dxn2, dxc, dxc, da, part2, Gr("g2"), S, h, opt_.eps, false, cs_));
+  // attention output projection
+  gemm(gd(S, h, h, da, h, 0, P("wo"), h, 1, GEMM_EPI_BF16, dout, h));
+  gemm(gd(h, h, S, da, h, 1, O, h, 1, GEMM_EPI_F32, Gr("wo"), h));
+  AttnBwdArgs ba;
+  ba.q = Q; ba.k = K; ba.v = Vv; ba.o = O; ba.lse = LSE; ba.dout = dout; ba.delta = ws;
+  ba.dq = dqkv; ba.dk = dqkv + h; ba.dv = dqkv + 2 * h; ba.ld_dqkv = 3 * h;
+  ba.rope = rope_; ba.pos0 = 0; ba.S = S; ba.H = H; ba.D = D;
+  ba.softmax_scale = 1.0f / std::sqrt(static_cast<float>(D));
+  attention_bwd(ba);
+  // QKV projection
+  gemm(gd(S, h, 3 * h, dqkv, 3 * h, 0, P("wqkv"), h, 1, GEMM_EPI_F32, dxn, h));
+  gemm(gd(3 * h, h, S, dqkv, 3 * h, 1, XN, h, 1, GEMM_EPI_F32, Gr("wqkv"), h));
+  G(rmsnorm_bwd(X, nullptr, P("g1"), dxn, dxc, dxc, dxb, part1, Gr("g1"), S, h, opt_.eps, false, cs_));
+  stats_.kernel_launches += 5;  // swiglu_bwd + 2 x (rmsnorm_bwd + dg_reduce)
+  mark(0, static_cast<int>(Kind::LayerBwd), i, false);
+  G(cudaEventRecord(ev_bwd_done_[i], cs_));
+  if (i >= 2 && swaps(i - 2)) prefetch(i - 2);  // B2
+}
+
+void Executor::classifier() {
+  const int S = d_.S, h = d_.h, V = d_.V;
+  const int T = std::min(opt_.ce_chunk, S);
+  float* xfin = static_cast<float*>(arena_ptr(seg_emb_fwd_, "x_final"));
+  auto* xf = static_cast<__nv_bfloat16*>(arena_ptr(seg_cls_fwd_, "xf"));
+  const __nv_bfloat16* gf = params_ + ptab_.at({"gf", -1}).first;
+  const __nv_bfloat16* W = params_ + ptab_.at({"wcls", -1}).first;
+  float* gW = grads_ + ptab_.at({"wcls", -1}).first;
+  mark(0, static_cast<int>(Kind::ClsFwd), -1, true);
+  G(rmsnorm_fwd(xfin, nullptr, gf, xf, S, h, opt_.eps, cs_));
+  mark(0, static_cast<int>(Kind::ClsFwd), -1, false);
+  mark(0, static_cast<int>(Kind::ClsBwd), -1, true);
+  float* dxf = static_cast<float*>(arena_ptr(seg_cls_bwd_, "dxf"));
+  float* loss_rows = static_cast<float*>(arena_ptr(seg_cls_bwd_, "loss_rows"));
+  float* logits = static_cast<float*>(arena_ptr(seg_cls_bwd_, "logits"));
+  auto* dlog = static_cast<__nv_bfloat16*>(arena_ptr(seg_cls_bwd_, "dlogits"));
+  float* part = static_cast<float*>(arena_ptr(seg_cls_bwd_, "cls_part"));
+  const float inv_n = 1.0f / static_cast<float>(n_labeled_);
+  for (int c0 = 0; c0 < S; c0 += T) {
+    const int t = std::min(T, S - c0);
+    const __nv_bfloat16* xc = xf + static_cast<Bytes>(c0) * h;
+    gemm(gd(t, V, h, xc, h, 0, W, h, 0, GEMM_EPI_F32, logits, V));
+    G(cross_entropy(logits, lab_ + c0, dlog, loss_rows + c0, t, V, inv_n, cs_));
+    gemm(gd(t, h, V, dlog, V, 0, W, h, 1, GEMM_EPI_F32, dxf + static_cast<Bytes>(c0) * h, h));
+    gemm(gd(V, h, t, dlog, V, 1, xc, h, 1, c0 == 0 ? GEMM_EPI_F32 : GEMM_EPI_F32_ACC, gW, h));
+    stats_.kernel_launches += 1;  // cross-entropy
+  }
+  G(sum_scaled(loss_rows, S, inv_n, loss_dev_, cs_));
+  float* dxc = static_cast<float*>(arena_ptr(seg_emb_fwd_, "dx_carry"));
+  auto* dxb = static_cast<__nv_bfloat16*>(arena_ptr(seg_emb_fwd_, "dxb_carry"));
+  G(rmsnorm_bwd(xfin, nullptr, gf, dxf, nullptr, dxc, dxb, part, grads_ + ptab_.at({"gf", -1}).first,
+                S, h, opt_.eps, false, cs_));
+  stats_.kernel_launches += 4;  // rmsnorm_fwd, sum, rmsnorm_bwd + dg_reduce
+  mark(0, static_cast<int>(Kind::ClsBwd), -1, false);
+}
+
+void Executor::step_resident() {
+  const int n = d_.n;
+  marks_.clear();
+  ops_.clear();
+  ev_used_ = 0;
+  stats_.offload_bytes = stats_.prefetch_bytes = 0;
+  stats_.kernel_launches = 0;
+  G(cudaEventRecord(ev_start_, cs_));
+  // copy streams must not run ahead of this step's start
+  G(cudaStreamWaitEvent(os_, ev_start_, 0));
+  G(cudaStreamWaitEvent(ps_, ev_start_, 0));
+  mark(0, static_cast<int>(Kind::EmbFwd), -1, true);
+  G(embed_fwd(tok_, params_ + ptab_.at({"embedding", -1}).first,
+              reinterpret_cast<float*>(comp(0, C_X)), d_.S, d_.h, cs_));
+  mark(0, static_cast<int>(Kind::EmbFwd), -1, false);
+  for (int i = 0; i < n; ++i) layer_fwd(i);
+  classifier();
+  for (int i = n - 1; i >= 0; --i) {
+    if (swaps(i)) layer_recompute(i);
+    layer_bwd(i);
+  }
+  mark(0, static_cast<int>(Kind::EmbBwd), -1, true);
+  G(embed_bwd(csr_off_, csr_pos_, static_cast<float*>(arena_ptr(seg_emb_fwd_, "dx_carry")),
+              grads_ + ptab_.at({"embedding", -1}).first, d_.V, d_.h, cs_));
+  mark(0, static_cast<int>(Kind::EmbBwd), -1, false);
+  stats_.kernel_launches += 2;
+  if (opt_.optimizer) {
+    ++adam_step_;
+    G(adamw(master_, params_, grads_, adam_m_, adam_v_, n_params_, opt_.lr, opt_.beta1, opt_.beta2,
+            opt_.adam_eps, opt_.weight_decay, adam_step_, cs_));
+    stats_.kernel_launches += 1;
+  }
+  mark(0, 99, -1, true);  // step end marker
+}
+
+float Executor::last_loss() {
+  G(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, cs_));
+  G(cudaStreamSynchronize(cs_));
+  return *loss_host_;
+}
+
+float Executor::step(const int* tokens, const int* labels) {
+  load_batch(tokens, labels);
+  step_resident();
+  G(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, cs_));
+  stats_.d2h_bytes = 4;
+  G(cudaStreamSynchronize(cs_));
+  G(cudaStreamSynchronize(os_));
+  G(cudaStreamSynchronize(ps_));
+  return *loss_host_;
+}
+
+Timeline Executor::timeline() const {
+  ck(cudaStreamSynchronize(cs_), "sync");
+  ck(cudaStreamSynchronize(os_), "sync");
+  ck(cudaStreamSynchronize(ps_), "sync");
+  Timeline t;
+  t.n_layers = d_.n;
+  t.rounding_buffer_bytes = sk_.total;
+  t.swapped_layers = d_.n >= 2 ? d_.n - 2 : 0;
+  for (const Mark& m : marks_) {
+    if (m.kind == 99) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, ev_start_, m.b), "elapsed");
+      const_cast<Executor*>(this)->stats_.step_ms = ms;
+      continue;
+    }
+    if (!m.e) continue;
+    float a = 0, b = 0;
+    ck(cudaEventElapsedTime(&a, ev_start_, m.b), "elapsed");
+    ck(cudaEventElapsedTime(&b, ev_start_, m.e), "elapsed");
+    t.events.push_back({static_cast<Stream>(m.stream), static_cast<Kind>(m.kind), m.layer,
+                        a * 1e-3, b * 1e-3});
+  }
+  StepStats& st = const_cast<Executor*>(this)->stats_;
+  for (int c = 0; c < OP_NCLASS; ++c) {
+    st.op_ms[c] = 0;
+    st.op_flops[c] = 0;
+    st.op_count[c] = 0;
+  }
+  for (const OpMark& o : ops_) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, o.a, o.b), "elapsed");
+    st.op_ms[o.cls] += ms;
+    st.op_flops[o.cls] += o.flops;
+    st.op_count[o.cls] += 1;
+  }
+  return t;
+}
+
+}  // namespace memo

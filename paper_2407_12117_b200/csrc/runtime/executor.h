@@ -1,0 +1,181 @@
+// executor.h — the B200 training-step executor that replaces the reference's
+// simulated schedule (proj/include/actmem/schedule.hpp:186 build_schedule)
+// with real execution: one preallocated HBM allocation (planned transient
+// arena + two rounding buffers + parameter/optimizer state), token-wise
+// offload of each layer's skeletal activations to pinned host memory on a
+// dedicated copy stream, prefetch one layer ahead in backward on a second
+// copy stream, and suffix recompute — all ordered by CUDA events (rules
+// F1-F3, B1-B3 of schedule.hpp:177-185 plus prefetch-before-recompute).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host/planner.hpp"
+#include "kernels/attention.h"
+#include "kernels/gemm_tc.h"
+
+namespace memo {
+
+struct ExecOptions {
+  uint64_t seed = 1234;
+  double alpha = -1.0;  // < 0: solve_alpha with t_layer; else forced (make_swap_plan_with_alpha)
+  uint64_t token_granularity = 128;
+  bool swap_enabled = true;  // false: every layer keeps its activations resident (no swap/recompute)
+  int ce_chunk = 8192;
+  float eps = 1e-5f;
+  float rope_theta = 10000.f;
+  bool optimizer = true;
+  float lr = 1e-4f, beta1 = 0.9f, beta2 = 0.95f, adam_eps = 1e-8f, weight_decay = 0.0f;
+  double t_layer = 0.0;  // measured forward-layer seconds for solve_alpha (0 = analytic)
+  double plan_time_budget = 60.0;
+  Bytes alignment = 512;
+  bool op_timing = false;  // record per-kernel-class CUDA events inside the step
+  bool dry_run = false;  // plan only (trace, arena plan, alpha, sizes); no CUDA calls
+};
+
+// Llama dimensions derived from the reference ModelConfig: intermediate size
+// f = 2/3 * ffn_hidden (SwiGLU mapping, SURVEY discovery 5), D = h / n_heads.
+struct Dims {
+  int S, h, H, D, F, V, n;
+};
+
+// Per-kernel-class device time of the last step (CUDA events on the compute
+// stream, recorded only when ExecOptions::op_timing is set).
+enum OpClass { OP_ATTN_FWD = 0, OP_ATTN_PREP, OP_ATTN_DKDV, OP_ATTN_DQ, OP_GEMM, OP_NCLASS };
+
+struct StepStats {
+  double step_ms = 0;
+  double h2d_bytes = 0, d2h_bytes = 0;
+  double offload_bytes = 0, prefetch_bytes = 0;
+  int kernel_launches = 0;
+  double op_ms[OP_NCLASS] = {0, 0, 0, 0, 0};
+  double op_flops[OP_NCLASS] = {0, 0, 0, 0, 0};
+  int op_count[OP_NCLASS] = {0, 0, 0, 0, 0};
+};
+
+class Executor {
+ public:
+  Executor(const ModelConfig& cfg, const HardwareConfig& hw, const ExecOptions& opt);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  // Host batch -> device (tokens, labels, embedding-gradient CSR).
+  void load_batch(const int* tokens, const int* labels);
+  // One training step on the resident batch; loss stays on device.
+  void step_resident();
+  // End to end: load_batch + step + D2H of the loss.
+  float step(const int* tokens, const int* labels);
+  float last_loss();  // synchronises
+
+  const std::string& trace_text() const { return trace_text_; }
+  const std::string& plan_json() const { return plan_json_; }
+  const ModelConfig& model() const { return cfg_; }
+  const Dims& dims() const { return d_; }
+  const SwapDecision& swap() const { return swap_; }
+  const TokenRange& split() const { return split_; }
+  const Skeletal& skeletal() const { return sk_; }
+  Bytes arena_bytes() const { return arena_bytes_; }
+  Bytes rb_bytes() const { return rb_bytes_; }
+  Bytes device_bytes() const { return dev_bytes_; }
+  Bytes pinned_bytes() const { return pinned_bytes_; }
+  Bytes state_bytes() const { return state_bytes_; }
+  long long param_count() const { return n_params_; }
+  const StepStats& stats() const { return stats_; }
+  // Measured timeline of the last step (seconds from step start), validated
+  // form of schedule.hpp's Schedule.
+  Timeline timeline() const;
+  // Named device tensor lookup for tests: params/grads/master by name+layer.
+  bool tensor(const std::string& name, int layer, void** ptr, size_t* bytes) const;
+  bool swap_enabled() const { return swap_on_; }
+  void* stream() const { return cs_; }
+
+ private:
+  struct Buf {
+    Bytes off = 0;
+    Bytes bytes = 0;
+  };
+  void build_trace_and_plan();
+  void compute_layout();
+  void allocate();
+  void init_weights();
+  void* arena_ptr(std::size_t seg, const char* name) const;
+  char* rb(int layer) const { return swap_on_ ? rb_base_[layer & 1] : rb_base_[layer]; }
+  char* comp(int layer, int c) const { return rb(layer) + rb_off_[c]; }
+  bool swaps(int i) const { return swap_on_ && d_.n >= 3 && i + 2 < d_.n && swap_.swapped_bytes_per_layer > 0; }
+  void layer_fwd(int i);
+  void layer_recompute(int i);
+  void layer_bwd(int i);
+  void classifier();
+  void offload(int i);
+  void prefetch(int i);
+  void mark(int stream, int kind, int layer, bool begin);
+  void gemm(const GemmDesc& g);
+  void attention_fwd(AttnFwdArgs a);
+  void attention_bwd(AttnBwdArgs a);
+  struct OpMark {
+    int cls;
+    cudaEvent_t a, b;
+    double flops;
+  };
+  std::vector<OpMark> ops_;
+
+  ModelConfig cfg_;
+  HardwareConfig hw_;
+  ExecOptions opt_;
+  Dims d_{};
+  Skeletal sk_;
+  SwapDecision swap_;
+  TokenRange split_;
+  bool can_swap_ = true, swap_on_ = true;
+
+  std::string trace_text_, plan_json_;
+  std::map<std::pair<std::size_t, std::string>, Bytes> arena_off_;
+  std::size_t seg_emb_fwd_ = 0, seg_cls_fwd_ = 0, seg_cls_bwd_ = 0, seg_emb_bwd_ = 0;
+  std::vector<std::size_t> seg_fwd_, seg_bwd_;
+
+  // device memory (one cudaMalloc)
+  char* dev_ = nullptr;
+  Bytes dev_bytes_ = 0, arena_bytes_ = 0, rb_bytes_ = 0, state_bytes_ = 0;
+  char* arena_ = nullptr;
+  std::vector<char*> rb_base_;  // 2 rounding buffers (swap on) or one per layer (swap off)
+  std::vector<Bytes> rb_off_;   // component offsets inside a rounding buffer
+  std::vector<Bytes> row_bytes_;  // bytes per token row of each component
+  __nv_bfloat16* params_ = nullptr;
+  float *master_ = nullptr, *grads_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
+  long long n_params_ = 0;
+  std::map<std::pair<std::string, int>, std::pair<long long, long long>> ptab_;  // (off, n)
+  float2* rope_ = nullptr;
+  int *tok_ = nullptr, *lab_ = nullptr, *csr_off_ = nullptr, *csr_pos_ = nullptr;
+  float* loss_dev_ = nullptr;
+  int n_labeled_ = 0;
+  int adam_step_ = 0;
+
+  // host
+  char* pinned_ = nullptr;
+  Bytes pinned_bytes_ = 0, per_layer_host_ = 0;
+  std::vector<Bytes> host_slot_;  // per swapped layer offset in pinned_
+  char* staging_ = nullptr;       // pinned batch staging
+  float* loss_host_ = nullptr;
+
+  // streams / events
+  cudaStream_t cs_ = nullptr, os_ = nullptr, ps_ = nullptr;
+  cudaEvent_t ev_start_ = nullptr;
+  std::vector<cudaEvent_t> ev_fwd_done_, ev_bwd_done_, ev_off_done_, ev_pre_mand_, ev_pre_done_;
+  struct Mark {
+    int stream, kind, layer;
+    cudaEvent_t b, e;
+  };
+  std::vector<Mark> marks_;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::size_t ev_used_ = 0;
+  cudaEvent_t take_event();
+  StepStats stats_;
+};
+
+}  // namespace memo

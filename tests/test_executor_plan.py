@@ -1,0 +1,85 @@
+"""Executor planning path without a GPU (dry_run): the executor's own request
+trace, its bi-level arena plan (bit-exact with the reference planner run on the
+same trace), alpha / token split, and the HBM budget at the BASELINE configs."""
+import json
+import os
+import subprocess
+import tempfile
+
+import pytest
+
+from paper_2407_12117_b200 import planner as P
+from paper_2407_12117_b200._abi import MemoError
+from paper_2407_12117_b200.executor import Executor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROBE = os.path.join(ROOT, "oracle", "_ref", "ref_probe")
+HW = P.HardwareConfig(pcie_bandwidth=50e9, cpu_mem=96 * P.GiB, gpu_mem=180 * 10 ** 9,
+                      peak_flops=2.25e15, efficiency=0.5)
+
+
+def llama(n, h, H, inter, V, S):
+    return P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
+                         batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True)
+
+
+CONFIGS = {
+    "cfg1p": (llama(4, 256, 4, 768, 512, 4096), 0.5),
+    "cfg2": (llama(4, 4096, 32, 11008, 32000, 131072), -1.0),
+    "cfg5": (llama(32, 4096, 32, 11008, 32000, 262144), 0.5),
+    "13b_512k": (llama(40, 5120, 40, 13824, 32000, 524288), 0.25),
+}
+
+
+def _ref_plan(trace):
+    with tempfile.NamedTemporaryFile("w", suffix=".trace", delete=False) as f:
+        f.write(trace)
+    try:
+        return subprocess.check_output([PROBE, "plan", f.name, "0", "60", "512"], text=True).strip()
+    finally:
+        os.unlink(f.name)
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_executor_trace_plan_bit_exact(name):
+    cfg, alpha = CONFIGS[name]
+    hw = P.HardwareConfig(**{**HW.__dict__, "cpu_mem": 2048 * P.GiB})
+    ex = Executor(cfg, hw, alpha=alpha, dry_run=1)
+    trace, plan = ex.trace_text(), ex.plan_json()
+    info = ex.info()
+    assert P.plan_model_json(trace, 0, 60.0, 512) == plan
+    if os.path.exists(PROBE):
+        assert _ref_plan(trace) == plan
+    jp = json.loads(plan)
+    assert jp["optimal"] is True and info["arena_bytes"] == jp["total_peak"]
+    # rounding buffers hold exactly the skeletal model's bytes (swap.hpp:75)
+    assert info["rb_bytes"] == info["skeletal_total"]
+    # token split follows swap.hpp:177 at the executor's alpha
+    st, rc = P.token_split(info["swap"].alpha, cfg.seq_len, 128)
+    assert info["split"] == (st, rc)
+
+
+def test_cfg2_fits_one_b200():
+    cfg, _ = CONFIGS["cfg2"]
+    ex = Executor(cfg, HW, dry_run=1)
+    info = ex.info()
+    assert info["device_bytes"] < 170 * 10 ** 9, info["device_bytes"]
+    sw = info["swap"]
+    assert 0.0 <= sw.alpha <= 1.0 and sw.swapped_layers == 2
+    assert info["pinned_bytes"] <= sw.cpu_footprint
+
+
+def test_executor_rejects_bad_configs():
+    bad = llama(4, 256, 3, 768, 512, 512)  # head_dim not 64/128
+    with pytest.raises(MemoError) as ei:
+        Executor(bad, HW, dry_run=1)
+    assert ei.value.code == 2
+    tp = llama(4, 256, 4, 768, 512, 512)
+    tp.tp_degree = 2
+    with pytest.raises(MemoError):
+        Executor(tp, HW, dry_run=1)
+    # host memory too small for the mandatory offload -> CpuInfeasible (4)
+    tiny = P.HardwareConfig(pcie_bandwidth=50e9, cpu_mem=1024, gpu_mem=1 << 40, peak_flops=2.25e15)
+    with pytest.raises(MemoError) as ei:
+        Executor(CONFIGS["cfg1p"][0], tiny, dry_run=1)
+    assert ei.value.code == 4

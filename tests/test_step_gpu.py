@@ -1,0 +1,120 @@
+"""End-to-end training step on the GPU (executor + all sm_100a kernels) vs the
+CPU numeric oracle, plus the MEMO invariants:
+  * weights initialise bit-identically on CPU and GPU,
+  * loss within 5e-3 relative, every gradient tensor within 2e-2 relative L2,
+  * swap+recompute gradients are BITWISE equal to the no-swap GPU path,
+  * the measured timeline passes the reference validator (F1-F3, B1-B3),
+  * the arena is the bi-level plan of the executor's own trace, and that plan is
+    byte-identical to the reference planner's (oracle/_ref/ref_probe).
+"""
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_12117_b200 import planner as P
+from paper_2407_12117_b200.executor import Executor
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROBE = os.path.join(ROOT, "oracle", "_ref", "ref_probe")
+
+HW = P.HardwareConfig(pcie_bandwidth=50e9, cpu_mem=64 * P.GiB, gpu_mem=180 * 10 ** 9,
+                      peak_flops=2.25e15, efficiency=0.5)
+
+
+def model(n, h, H, F, V, S):
+    return P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=F * 3 // 2, n_heads=H, vocab=V,
+                         batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+CASES = [
+    # n, h, H, F, V, S, alpha
+    (4, 256, 2, 768, 512, 512, 0.5),    # D=128, two swapped layers
+    (4, 256, 4, 768, 512, 1024, 0.25),  # D=64 (cfg1' shape family)
+    (2, 256, 4, 768, 512, 512, 0.5),    # n=2: nothing swaps (reference rule)
+]
+
+
+@pytest.fixture(scope="module")
+def oracle_runs():
+    return {}
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_step_matches_cpu_oracle(case, oracle_runs):
+    n, h, H, F, V, S, alpha = case
+    cfg = model(n, h, H, F, V, S)
+    ocfg = O.make_cfg(n, h, H, F, V, S)
+    params = O.init_params(ocfg, 1234)
+    toks, labels = O.tokens(1234, V, S)
+    with Executor(cfg, HW, seed=1234, alpha=alpha, optimizer=0, ce_chunk=256) as ex:
+        gpu_params = ex.read("all", -1, dtype="bf16")
+        assert np.array_equal(gpu_params, params), "weight init differs from the oracle"
+        loss = ex.step(toks, labels)
+        grads = ex.read("grad/all")
+        tl = ex.timeline()
+        info = ex.info()
+    ref_loss, ref_grads = O.step(ocfg, params, toks, labels)
+    assert abs(loss - ref_loss) <= 5e-3 * abs(ref_loss), (loss, ref_loss)
+    for name, layer, off, cnt in O.layout(ocfg):
+        r = _rel(grads[off:off + cnt], ref_grads[off:off + cnt])
+        assert r < 2e-2, (name, layer, r)
+    # measured timeline obeys the reference executor rules
+    assert P.validate_schedule(tl, n, info["swap"]) == []
+    kinds = [e.kind for e in tl]
+    swapped = max(n - 2, 0)
+    assert kinds.count("offload") == swapped and kinds.count("prefetch") == swapped
+    assert kinds.count("recompute") == swapped
+    assert kinds.count("layer_fwd") == n and kinds.count("layer_bwd") == n
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.5, 1.0])
+def test_swap_recompute_bitwise_equals_no_swap(alpha):
+    n, h, H, F, V, S = 4, 256, 2, 768, 512, 1024
+    cfg = model(n, h, H, F, V, S)
+    toks, labels = O.tokens(99, V, S)
+    with Executor(cfg, HW, seed=5, alpha=alpha, optimizer=0, swap_enabled=1, ce_chunk=512) as ex:
+        l1 = ex.step(toks, labels)
+        g1 = ex.read("grad/all")
+        split = ex.info()["split"]
+    with Executor(cfg, HW, seed=5, alpha=alpha, optimizer=0, swap_enabled=0, ce_chunk=512) as ex:
+        l0 = ex.step(toks, labels)
+        g0 = ex.read("grad/all")
+    assert split[0] + split[1] == S
+    assert l1 == l0
+    assert np.array_equal(g1, g0)
+
+
+def test_arena_plan_matches_reference_planner():
+    cfg = model(4, 256, 2, 768, 512, 512)
+    with Executor(cfg, HW, seed=1, alpha=0.5, optimizer=0, ce_chunk=256) as ex:
+        trace, plan, info = ex.trace_text(), ex.plan_json(), ex.info()
+    assert P.plan_model_json(trace, 0, 60.0, 512) == plan
+    assert info["arena_bytes"] == __import__("json").loads(plan)["total_peak"]
+    if os.path.exists(PROBE):
+        with tempfile.NamedTemporaryFile("w", suffix=".trace", delete=False) as f:
+            f.write(trace)
+        ref = subprocess.check_output([PROBE, "plan", f.name, "0", "60", "512"], text=True).strip()
+        os.unlink(f.name)
+        assert ref == plan
+
+
+def test_optimizer_step_changes_weights_and_loss_decreases():
+    n, h, H, F, V, S = 2, 256, 2, 768, 512, 512
+    cfg = model(n, h, H, F, V, S)
+    toks, labels = O.tokens(3, V, S)
+    with Executor(cfg, HW, seed=3, alpha=1.0, optimizer=1, lr=3e-3, ce_chunk=512) as ex:
+        w0 = ex.read("master/all")
+        losses = [ex.step(toks, labels) for _ in range(6)]
+        w1 = ex.read("master/all")
+    assert not np.array_equal(w0, w1)
+    assert losses[-1] < losses[0], losses
