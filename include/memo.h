@@ -200,6 +200,12 @@ int memo_attn_bwd(const void* q, const void* k, const void* v, const void* o, co
                   const void* dout, float* delta, void* dq, void* dk, void* dv, int64_t ld_dqkv,
                   const void* rope, int64_t pos0, int32_t S, int32_t H, int32_t D,
                   float softmax_scale, void* stream);
+/* As memo_attn_bwd; synchronises and writes the device ms of its three kernels
+ * (delta prep, dK/dV, dQ) to ms3 when ms3 != NULL. */
+int memo_attn_bwd_timed(const void* q, const void* k, const void* v, const void* o,
+                        const float* lse, const void* dout, float* delta, void* dq, void* dk,
+                        void* dv, int64_t ld_dqkv, const void* rope, int64_t pos0, int32_t S,
+                        int32_t H, int32_t D, float softmax_scale, void* stream, float* ms3);
 
 /* ---------------------------------------------------------------- executor
  * The real training step that replaces the reference's simulated executor

@@ -2,32 +2,37 @@
 //
 // Layout: Q, K, V, O are token-major [S, H*D] bf16 (head hh occupies columns
 // [hh*D, hh*D+D)); LSE is [H, S] f32 (natural log).  Tiles are 128 tokens.
+// Every kernel is warp-specialised: warp 0 issues TMA, one thread of warp 1
+// issues tcgen05.mma, warps 4-7 (one thread per TMEM lane / tile row) do the
+// elementwise math between MMAs.  Operands that stay fixed for a CTA's whole
+// loop (Q in the forward and in dQ, dO in dQ) are written once into TMEM and
+// used as the A operand of .kind::f16 MMAs, which halves shared-memory operand
+// traffic (the SS form of M128xN128 sits right at 128 B/clk).
 //
-// Forward (one CTA per (query tile, head)), warp roles:
-//   warp 0  TMA producer: Q once, K/V tiles into two 2-stage rings
-//   warp 1  single-thread tcgen05.mma issuer: S = Q K^T into a double-buffered
-//           TMEM S, then O += P V with P read straight from TMEM (it
-//           overwrites the S buffer it came from)
-//   warps 4-7  softmax: one thread per query row (TMEM lane); online softmax
-//           in the exp2 domain with lazy rescaling (O is only touched when a
-//           row max grows by more than 2^8), then the normalising epilogue.
-// S(j+1) is issued before P(j)V(j), so QK^T of the next tile overlaps the
-// softmax of the current one; tcgen05 ops of one thread execute in order,
-// which is what makes reusing S's buffer for P safe.
-//
+// Forward (CTA per (query tile, head)):  S_j = Q K_j^T into a double-buffered
+//   TMEM S; the softmax warps overwrite S_j with P_j (bf16) which feeds
+//   O += P_j V_j as the TMEM A operand.  S_{j+1} is issued before P_j V_j so QK^T
+//   of the next tile overlaps the softmax of this one (tcgen05 ops of a thread
+//   execute in order, which makes reusing S's columns for P safe).  O is only
+//   rescaled when a row max grows by > 2^8, and a quarter of the exponentials
+//   run as a cubic on the FMA pipe to take load off MUFU.
 // Backward is deterministic (no atomics), so swap+recompute and no-swap
-// gradients are bit-identical:
-//   attn_bwd_dkdv  one CTA per (key tile, head), loops over query tiles:
-//                  S^T = K Q^T, dP^T = V dO^T, dV += P^T dO, dK += dS^T Q
-//   attn_bwd_dq    one CTA per (query tile, head), loops over key tiles:
-//                  S = Q K^T, dP = dO V^T, dQ += dS K
-// with P^T/dS^T kept in TMEM as the A operand.  RoPE's inverse rotation is
-// fused into the dQ/dK epilogues.
+// gradients are bit-identical.  Both kernels walk their partner tiles in
+// 64-row halves with double-buffered TMEM so the P/dS math of half g overlaps
+// the MMAs of half g+1:
+//   attn_bwd_dkdv  CTA per (key tile, head):   S^T = K Q^T, dP^T = V dO^T,
+//                  dV += P^T dO, dK += dS^T Q   (P^T, dS^T from TMEM)
+//   attn_bwd_dq    CTA per (query tile, head): S = Q K^T, dP = dO V^T,
+//                  dQ += dS K                    (Q, dO, dS from TMEM)
+// RoPE's inverse rotation and the softmax scale are fused into the dQ/dK
+// epilogues.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "attention.h"
 #include "sm100.cuh"
@@ -42,16 +47,6 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int D>
-struct FwdSmem {
-  static constexpr int NC = D / 64;  // 64-col chunks per tile
-  static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;
-  static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
-  static constexpr int BYTES = BAR_OFF + 256 + 1024;
-};
 
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
   // K-major tile split in 64-col chunks of 16 KiB; k-step of 16 elements.
@@ -62,27 +57,75 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
   return dev::umma_desc_sw128(base + kk * 2048, CHUNK_BYTES, 1024);
 }
 
+// 2^x for x <= 0 on the FMA pipe: cubic on the fraction + exponent insert.
+// Max relative error 1.0e-4 (bf16 P needs 3.9e-3).
+__device__ __forceinline__ float exp2_fma(float x) {
+  const float fl = floorf(x);
+  const float f = x - fl;
+  float p = fmaf(f, 0.07826793330191018f, 0.22630764718276575f);
+  p = fmaf(p, f, 0.6954244195153241f);
+  p = fmaf(p, f, 1.0f);
+  const float r = __int_as_float(__float_as_int(p) + (static_cast<int>(fl) << 23));
+  return x < -126.f ? 0.f : r;
+}
+
+// Each softmax/compute thread writes its own row (D bf16 from global) into
+// TMEM columns [t_col, t_col + D/2) of its lane: the A-operand layout.
 template <int D>
+__device__ __forceinline__ void row_to_tmem(const __nv_bfloat16* src, uint32_t taddr) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int c = 0; c < D / 64; ++c) {
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = s4[c * 8 + i];
+      r[4 * i + 0] = v.x;
+      r[4 * i + 1] = v.y;
+      r[4 * i + 2] = v.z;
+      r[4 * i + 3] = v.w;
+    }
+    dev::tmem_st32(taddr + c * 32, r);
+  }
+}
+
+constexpr int FWD_STAGES = 3;
+
+template <int D, bool QT>
+struct FwdSmem {
+  static constexpr int NC = D / 64;  // 64-col chunks per tile
+  static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = QT ? 0 : TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + FWD_STAGES * TILE_BYTES;
+  static constexpr int BAR_OFF = V_OFF + FWD_STAGES * TILE_BYTES;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+// QT: Q lives in TMEM (A operand of S = QK^T) instead of shared memory.
+// EMU: a quarter of the softmax exponentials run as a cubic on the FMA pipe.
+template <int D, bool QT, bool EMU>
 __global__ void __launch_bounds__(256, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap map_q,
+    attn_fwd_kernel(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
                     float* __restrict__ lse, int S, int H, float scale_log2) {
-  using L = FwdSmem<D>;
+  using L = FwdSmem<D, QT>;
   constexpr int NC = L::NC;
+  constexpr int NS = FWD_STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;   // [2]
-  uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2]
-  uint64_t* p_full = bars + 11;  // [2]
-  uint64_t* o_done = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* q_ready = bars + 0;
+  uint64_t* k_full = bars + 1;        // [NS]
+  uint64_t* k_empty = k_full + NS;    // [NS]
+  uint64_t* v_full = k_empty + NS;    // [NS]
+  uint64_t* v_empty = v_full + NS;    // [NS]
+  uint64_t* s_full = v_empty + NS;    // [2]
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* o_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int n_tiles = S / TILE;
   const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
@@ -92,15 +135,17 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t lane = dev::lane_id();
 
   if (warp == 0 && lane == 0) {
-    dev::tma_prefetch_desc(&map_q);
     dev::tma_prefetch_desc(&map_k);
     dev::tma_prefetch_desc(&map_v);
-    dev::mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::mbar_init(q_ready, QT ? 128 : 1);
+    for (int s = 0; s < NS; ++s) {
       dev::mbar_init(&k_full[s], 1);
       dev::mbar_init(&k_empty[s], 1);
       dev::mbar_init(&v_full[s], 1);
       dev::mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       dev::mbar_init(&s_full[s], 1);
       dev::mbar_init(&p_full[s], 128);
     }
@@ -114,16 +159,18 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_s[2] = {tmem, tmem + 128};
   const uint32_t t_o = tmem + 256;
+  const uint32_t t_q = tmem + 256 + D;
 
   if (warp == 0) {
     if (lane == 0) {
-      uint8_t* sq = smem + L::Q_OFF;
-      dev::mbar_expect_tx(q_full, L::TILE_BYTES);
-      for (int c = 0; c < NC; ++c)
-        dev::tma_load_2d(sq + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, qt * TILE);
+      if (!QT) {
+        dev::mbar_expect_tx(q_ready, L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c)
+          dev::tma_load_2d(smem + L::Q_OFF + c * CHUNK_BYTES, &map_q, q_ready, hh * D + c * 64, qt * TILE);
+      }
       for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
+        const int st = j % NS;
+        const uint32_t ph = (j / NS) & 1;
         uint8_t* sk = smem + L::K_OFF + st * L::TILE_BYTES;
         uint8_t* sv = smem + L::V_OFF + st * L::TILE_BYTES;
         dev::mbar_wait(&k_empty[st], ph ^ 1);
@@ -140,39 +187,49 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
-      const uint32_t sq = dev::smem_u32(smem + L::Q_OFF);
-      dev::mbar_wait(q_full, 0);
+      dev::mbar_wait(q_ready, 0);
       auto issue_s = [&](int j) {
-        const int st = j & 1;
-        dev::mbar_wait(&k_full[st], (j >> 1) & 1);
+        const int st = j % NS;
+        dev::mbar_wait(&k_full[st], (j / NS) & 1);
         dev::tc_fence_after();
         const uint32_t sk = dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(t_s[st], kmajor_desc(sq, kk), kmajor_desc(sk, kk), idesc_s, kk > 0);
-        dev::mma_commit(&s_full[st]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          if (QT)
+            dev::mma_bf16_ts(t_s[j & 1], t_q + kk * 8, kmajor_desc(sk, kk), idesc_s, kk > 0);
+          else
+            dev::mma_bf16_ss(t_s[j & 1], kmajor_desc(dev::smem_u32(smem + L::Q_OFF), kk),
+                             kmajor_desc(sk, kk), idesc_s, kk > 0);
+        }
+        dev::mma_commit(&s_full[j & 1]);
         dev::mma_commit(&k_empty[st]);
       };
       issue_s(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) issue_s(j + 1);
-        const int st = j & 1;
-        dev::mbar_wait(&p_full[st], (j >> 1) & 1);
-        dev::mbar_wait(&v_full[st], (j >> 1) & 1);
+        const int st = j % NS;
+        dev::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        dev::mbar_wait(&v_full[st], (j / NS) & 1);
         dev::tc_fence_after();
         const uint32_t sv = dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts(t_o, t_s[st] + kk * 8, mnmajor_desc(sv, kk), idesc_o, (j | kk) != 0);
+          dev::mma_bf16_ts(t_o, t_s[j & 1] + kk * 8, mnmajor_desc(sv, kk), idesc_o, (j | kk) != 0);
         dev::mma_commit(o_done);
         dev::mma_commit(&v_empty[st]);
       }
     }
   } else if (warp >= 4) {
     const uint32_t q4 = warp & 3;
-    const int row = q4 * 32 + lane;                 // TMEM lane == query row in tile
+    const int row = q4 * 32 + lane;  // TMEM lane == query row in tile
     const int qidx = qt * TILE + row;
     const uint32_t lane_off = (q4 * 32) << 16;
+    if (QT) {
+      row_to_tmem<D>(q + static_cast<long long>(qidx) * H * D + hh * D, t_q + lane_off);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(q_ready);
+    }
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
       const int st = j & 1;
@@ -202,14 +259,20 @@ __global__ void __launch_bounds__(256, 1)
       float m_new = m;
       if (any) {
         m_new = cand;
-        factor = j == 0 ? 0.f : exp2f(m - m_new);
+        factor = j == 0 ? 0.f : dev::ex2(m - m_new);
       }
       float sum = 0.f;
       uint32_t p[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        const float a = exp2f(s[2 * i] - m_new);
-        const float b = exp2f(s[2 * i + 1] - m_new);
+        float a, b;
+        if (EMU && (i & 3) == 3) {  // a quarter of the exponentials on the FMA pipe
+          a = exp2_fma(s[2 * i] - m_new);
+          b = exp2_fma(s[2 * i + 1] - m_new);
+        } else {
+          a = dev::ex2(s[2 * i] - m_new);
+          b = dev::ex2(s[2 * i + 1] - m_new);
+        }
         sum += a + b;
         p[i] = dev::pack_bf16(a, b);
       }
@@ -270,7 +333,6 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-
 // ============================================================== backward
 // delta[h][t] = sum_d dO*O ; lse2[h][t] = lse * log2(e)
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
@@ -302,14 +364,16 @@ template <int D>
 struct BwdSmem {
   static constexpr int NC = D / 64;
   static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
-  static constexpr int A0_OFF = 0;                      // K (dkdv) | Q (dq)
-  static constexpr int A1_OFF = A0_OFF + TILE_BYTES;    // V (dkdv) | dO (dq)
-  static constexpr int R0_OFF = A1_OFF + TILE_BYTES;    // ring: Q (dkdv) | K (dq)  [2]
+  static constexpr int A0_OFF = 0;                        // K (dkdv)
+  static constexpr int A1_OFF = A0_OFF + TILE_BYTES;      // V (dkdv)
+  static constexpr int R0_OFF = A1_OFF + TILE_BYTES;      // ring: Q (dkdv) | K (dq)  [2]
   static constexpr int R1_OFF = R0_OFF + 2 * TILE_BYTES;  // ring: dO (dkdv) | V (dq) [2]
   static constexpr int VEC_OFF = R1_OFF + 2 * TILE_BYTES;  // [2][2][128] f32 (lse2, delta)
   static constexpr int BAR_OFF = VEC_OFF + 2 * 2 * 128 * 4;
   static constexpr int BYTES = BAR_OFF + 256 + 1024;
 };
+constexpr int HALF = 64;             // rows of the partner tile per pipeline step
+constexpr int HALF_BYTES = HALF * 128;  // byte offset of the second half inside a 64-col chunk
 
 // Writes 32 consecutive columns of a dq/dk row: scale, inverse RoPE, bf16.
 __device__ __forceinline__ void store_grad32(__nv_bfloat16* dst, float (&x)[32], float scale,
@@ -355,16 +419,17 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* kv_full = bars + 0;
   uint64_t* in_full = bars + 1;   // [2]
   uint64_t* in_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_ready = bars + 6;
-  uint64_t* fin = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* s_full = bars + 5;    // [2] per TMEM buffer
+  uint64_t* p_ready = bars + 7;   // [2]
+  uint64_t* fin = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
   float* vec = reinterpret_cast<float*>(smem + L::VEC_OFF);  // [stage][lse2|delta][128]
 
   const int n_tiles = S / TILE;
   const int kt = blockIdx.x;  // key tile
   const int hh = blockIdx.y;
   const int n_q = n_tiles - kt;  // query tiles kt..n_tiles-1
+  const int n_g = 2 * n_q;       // 64-query halves
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
 
@@ -377,9 +442,9 @@ __global__ void __launch_bounds__(256, 1)
     for (int s2 = 0; s2 < 2; ++s2) {
       dev::mbar_init(&in_full[s2], 1);
       dev::mbar_init(&in_empty[s2], 1);
+      dev::mbar_init(&s_full[s2], 1);
+      dev::mbar_init(&p_ready[s2], 128);
     }
-    dev::mbar_init(s_full, 1);
-    dev::mbar_init(p_ready, 128);
     dev::mbar_init(fin, 1);
     dev::fence_barrier_init();
   }
@@ -388,7 +453,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   dev::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_st = tmem, t_dpt = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + D;
+  // buffer b: S^T half at b*128, dP^T half at b*128 + 64
+  const uint32_t t_dv = tmem + 256, t_dk = tmem + 256 + D;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -414,33 +480,45 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, HALF, false, false);
       constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
       const uint32_t sk = dev::smem_u32(smem + L::A0_OFF);
       const uint32_t sv = dev::smem_u32(smem + L::A1_OFF);
       dev::mbar_wait(kv_full, 0);
-      for (int i = 0; i < n_q; ++i) {
-        const int st = i & 1;
-        dev::mbar_wait(&in_full[st], (i >> 1) & 1);
-        dev::tc_fence_after();
-        const uint32_t sq = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES);
-        const uint32_t sdo = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES);
+      auto issue_sd = [&](int g) {
+        const int i = g >> 1, half = g & 1, st = i & 1, b = g & 1;
+        if (half == 0) {
+          dev::mbar_wait(&in_full[st], (i >> 1) & 1);
+          dev::tc_fence_after();
+        }
+        const uint32_t sq = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
+        const uint32_t sdo = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(t_st, kmajor_desc(sk, kk), kmajor_desc(sq, kk), idesc_s, kk > 0);
+          dev::mma_bf16_ss(tmem + b * 128, kmajor_desc(sk, kk), kmajor_desc(sq, kk), idesc_s, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(t_dpt, kmajor_desc(sv, kk), kmajor_desc(sdo, kk), idesc_s, kk > 0);
-        dev::mma_commit(s_full);
-        dev::mbar_wait(p_ready, i & 1);
+          dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_desc(sv, kk), kmajor_desc(sdo, kk), idesc_s,
+                           kk > 0);
+        dev::mma_commit(&s_full[b]);
+      };
+      issue_sd(0);
+      for (int g = 0; g < n_g; ++g) {
+        if (g + 1 < n_g) issue_sd(g + 1);
+        const int i = g >> 1, half = g & 1, st = i & 1, b = g & 1;
+        dev::mbar_wait(&p_ready[b], (g >> 1) & 1);
         dev::tc_fence_after();
+        const uint32_t sq = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
+        const uint32_t sdo = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts(t_dv, t_st + kk * 8, mnmajor_desc(sdo, kk), idesc_g, (i | kk) != 0);
+        for (int kk = 0; kk < HALF / 16; ++kk)
+          dev::mma_bf16_ts(t_dv, tmem + b * 128 + kk * 8, mnmajor_desc(sdo, kk), idesc_g,
+                           (g | kk) != 0);
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts(t_dk, t_dpt + kk * 8, mnmajor_desc(sq, kk), idesc_g, (i | kk) != 0);
-        dev::mma_commit(&in_empty[st]);
+        for (int kk = 0; kk < HALF / 16; ++kk)
+          dev::mma_bf16_ts(t_dk, tmem + b * 128 + 64 + kk * 8, mnmajor_desc(sq, kk), idesc_g,
+                           (g | kk) != 0);
+        if (half == 1) dev::mma_commit(&in_empty[st]);
       }
       dev::mma_commit(fin);
     }
@@ -449,41 +527,56 @@ __global__ void __launch_bounds__(256, 1)
     const int r = q4 * 32 + lane;  // key row in tile
     const int kidx = kt * TILE + r;
     const uint32_t lane_off = (q4 * 32) << 16;
-    for (int i = 0; i < n_q; ++i) {
-      const int st = i & 1;
+    for (int g = 0; g < n_g; ++g) {
+      const int i = g >> 1, half = g & 1, st = i & 1, b = g & 1;
       const bool diag = i == 0;
-      dev::mbar_wait(&in_full[st], (i >> 1) & 1);
-      dev::mbar_wait(s_full, i & 1);
+      if (half == 0) dev::mbar_wait(&in_full[st], (i >> 1) & 1);
+      dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       dev::tc_fence_after();
-      const float* l2 = vec + st * 256;
+      const float* l2 = vec + st * 256 + half * HALF;
       const float* dl = l2 + 128;
+      const uint32_t t_st = tmem + b * 128 + lane_off, t_dpt = t_st + 64;
+      // The causal mask only touches the diagonal tile; keep it out of the hot loop.
+      auto body = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sr[32], dr[32];
-        dev::tmem_ld32(t_st + lane_off + c * 32, sr);
-        dev::tmem_ld32(t_dpt + lane_off + c * 32, dr);
-        dev::tmem_ld_wait();
-        uint32_t pp[16], dd[16];
+        for (int c = 0; c < 2; ++c) {
+          uint32_t sr[32], dr[32];
+          dev::tmem_ld32(t_st + c * 32, sr);
+          dev::tmem_ld32(t_dpt + c * 32, dr);
+          dev::tmem_ld_wait();
+          uint32_t pp[16], dd[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float p2[2], d2[2];
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 lv = *reinterpret_cast<const float4*>(l2 + c * 32 + 4 * j4);
+            const float4 dv4 = *reinterpret_cast<const float4*>(dl + c * 32 + 4 * j4);
+            const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
+            const float dq[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+            float p4[4], d4[4];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int qc = c * 32 + 2 * j + e;
-            float p = exp2f(__uint_as_float(sr[2 * j + e]) * scale_log2 - l2[qc]);
-            if (diag && qc < r) p = 0.f;
-            p2[e] = p;
-            d2[e] = p * (__uint_as_float(dr[2 * j + e]) - dl[qc]);
+            for (int e = 0; e < 4; ++e) {
+              const int qc = c * 32 + 4 * j4 + e;
+              float p = dev::ex2(__uint_as_float(sr[4 * j4 + e]) * scale_log2 - lq[e]);
+              if (DIAG && half * HALF + qc < r) p = 0.f;
+              p4[e] = p;
+              d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) - dq[e]);
+            }
+            pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
+            pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
+            dd[2 * j4] = dev::pack_bf16(d4[0], d4[1]);
+            dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
           }
-          pp[j] = dev::pack_bf16(p2[0], p2[1]);
-          dd[j] = dev::pack_bf16(d2[0], d2[1]);
+          dev::tmem_st16(t_st + c * 16, pp);
+          dev::tmem_st16(t_dpt + c * 16, dd);
         }
-        dev::tmem_st16(t_st + lane_off + c * 16, pp);
-        dev::tmem_st16(t_dpt + lane_off + c * 16, dd);
-      }
+      };
+      if (diag)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
       dev::tmem_st_wait();
       dev::tc_fence_before();
-      dev::mbar_arrive(p_ready);
+      dev::mbar_arrive(&p_ready[b]);
     }
     dev::mbar_wait(fin, 0);
     dev::tc_fence_after();
@@ -514,14 +607,16 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-template <int D>
+// AT: Q and dO live in TMEM (A operands) instead of shared memory.
+template <int D, bool AT>
 __global__ void __launch_bounds__(256, 1)
-    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap map_q,
+    attn_bwd_dq_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dout,
+                       const __grid_constant__ CUtensorMap map_q,
+                       const __grid_constant__ CUtensorMap map_do,
                        const __grid_constant__ CUtensorMap map_k,
-                       const __grid_constant__ CUtensorMap map_v,
-                       const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                       const __grid_constant__ CUtensorMap map_v, const float* __restrict__ lse2,
                        const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq, long long ld,
-                       const float2* __restrict__ rope, long long pos0, int S, float scale,
+                       const float2* __restrict__ rope, long long pos0, int S, int H, float scale,
                        float scale_log2) {
   using L = BwdSmem<D>;
   constexpr int NC = L::NC;
@@ -529,33 +624,32 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* qd_full = bars + 0;
+  uint64_t* qd_ready = bars + 0;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* ds_ready = bars + 6;
-  uint64_t* fin = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* ds_ready = bars + 7;  // [2]
+  uint64_t* fin = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int n_tiles = S / TILE;
   const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
   const int hh = blockIdx.y;
   const int n_kv = qt + 1;
+  const int n_g = 2 * n_kv;
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
 
   if (warp == 0 && lane == 0) {
-    dev::tma_prefetch_desc(&map_q);
     dev::tma_prefetch_desc(&map_k);
     dev::tma_prefetch_desc(&map_v);
-    dev::tma_prefetch_desc(&map_do);
-    dev::mbar_init(qd_full, 1);
+    dev::mbar_init(qd_ready, AT ? 128 : 1);
     for (int s2 = 0; s2 < 2; ++s2) {
       dev::mbar_init(&kv_full[s2], 1);
       dev::mbar_init(&kv_empty[s2], 1);
+      dev::mbar_init(&s_full[s2], 1);
+      dev::mbar_init(&ds_ready[s2], 128);
     }
-    dev::mbar_init(s_full, 1);
-    dev::mbar_init(ds_ready, 128);
     dev::mbar_init(fin, 1);
     dev::fence_barrier_init();
   }
@@ -564,14 +658,17 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   dev::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256;
+  // buffer b: S half at b*128, dP half at b*128 + 64; dQ at 256; Q, dO as A operands after it
+  const uint32_t t_dq = tmem + 256, t_q = tmem + 256 + D, t_do = t_q + D / 2;
 
   if (warp == 0) {
     if (lane == 0) {
-      dev::mbar_expect_tx(qd_full, 2 * L::TILE_BYTES);
-      for (int c = 0; c < NC; ++c) {
-        dev::tma_load_2d(smem + L::A0_OFF + c * CHUNK_BYTES, &map_q, qd_full, hh * D + c * 64, qt * TILE);
-        dev::tma_load_2d(smem + L::A1_OFF + c * CHUNK_BYTES, &map_do, qd_full, hh * D + c * 64, qt * TILE);
+      if (!AT) {
+        dev::mbar_expect_tx(qd_ready, 2 * L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::A0_OFF + c * CHUNK_BYTES, &map_q, qd_ready, hh * D + c * 64, qt * TILE);
+          dev::tma_load_2d(smem + L::A1_OFF + c * CHUNK_BYTES, &map_do, qd_ready, hh * D + c * 64, qt * TILE);
+        }
       }
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
@@ -587,30 +684,47 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, HALF, false, false);
       constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
-      const uint32_t sq = dev::smem_u32(smem + L::A0_OFF);
-      const uint32_t sdo = dev::smem_u32(smem + L::A1_OFF);
-      dev::mbar_wait(qd_full, 0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        dev::mbar_wait(&kv_full[st], (j >> 1) & 1);
+      dev::mbar_wait(qd_ready, 0);
+      auto issue_s = [&](int g) {
+        const int j = g >> 1, half = g & 1, st = j & 1, b = g & 1;
+        if (half == 0) {
+          dev::mbar_wait(&kv_full[st], (j >> 1) & 1);
+          dev::tc_fence_after();
+        }
+        const uint32_t sk = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
+        const uint32_t sv = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
+        const uint32_t sqa = dev::smem_u32(smem + L::A0_OFF), sdoa = dev::smem_u32(smem + L::A1_OFF);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          if (AT)
+            dev::mma_bf16_ts(tmem + b * 128, t_q + kk * 8, kmajor_desc(sk, kk), idesc_s, kk > 0);
+          else
+            dev::mma_bf16_ss(tmem + b * 128, kmajor_desc(sqa, kk), kmajor_desc(sk, kk), idesc_s, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          if (AT)
+            dev::mma_bf16_ts(tmem + b * 128 + 64, t_do + kk * 8, kmajor_desc(sv, kk), idesc_s, kk > 0);
+          else
+            dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_desc(sdoa, kk), kmajor_desc(sv, kk), idesc_s,
+                             kk > 0);
+        }
+        dev::mma_commit(&s_full[b]);
+      };
+      issue_s(0);
+      for (int g = 0; g < n_g; ++g) {
+        if (g + 1 < n_g) issue_s(g + 1);
+        const int j = g >> 1, half = g & 1, st = j & 1, b = g & 1;
+        dev::mbar_wait(&ds_ready[b], (g >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t sk = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES);
-        const uint32_t sv = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES);
+        const uint32_t sk = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(t_s, kmajor_desc(sq, kk), kmajor_desc(sk, kk), idesc_s, kk > 0);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(t_dp, kmajor_desc(sdo, kk), kmajor_desc(sv, kk), idesc_s, kk > 0);
-        dev::mma_commit(s_full);
-        dev::mbar_wait(ds_ready, j & 1);
-        dev::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts(t_dq, t_s + kk * 8, mnmajor_desc(sk, kk), idesc_g, (j | kk) != 0);
-        dev::mma_commit(&kv_empty[st]);
+        for (int kk = 0; kk < HALF / 16; ++kk)
+          dev::mma_bf16_ts(t_dq, tmem + b * 128 + kk * 8, mnmajor_desc(sk, kk), idesc_g,
+                           (g | kk) != 0);
+        if (half == 1) dev::mma_commit(&kv_empty[st]);
       }
       dev::mma_commit(fin);
     }
@@ -619,37 +733,54 @@ __global__ void __launch_bounds__(256, 1)
     const int r = q4 * 32 + lane;
     const int qidx = qt * TILE + r;
     const uint32_t lane_off = (q4 * 32) << 16;
+    const long long rowoff = static_cast<long long>(qidx) * H * D + hh * D;
+    if (AT) {
+      row_to_tmem<D>(q + rowoff, t_q + lane_off);
+      row_to_tmem<D>(dout + rowoff, t_do + lane_off);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(qd_ready);
+    }
     const long long vi = static_cast<long long>(hh) * S + qidx;
     const float my_lse2 = lse2[vi];
     const float my_delta = delta[vi];
-    for (int j = 0; j < n_kv; ++j) {
+    for (int g = 0; g < n_g; ++g) {
+      const int j = g >> 1, half = g & 1, b = g & 1;
       const bool diag = j == qt;
-      dev::mbar_wait(s_full, j & 1);
+      dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       dev::tc_fence_after();
+      const uint32_t t_s = tmem + b * 128 + lane_off, t_dp = t_s + 64;
+      auto body = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sr[32], dr[32];
-        dev::tmem_ld32(t_s + lane_off + c * 32, sr);
-        dev::tmem_ld32(t_dp + lane_off + c * 32, dr);
-        dev::tmem_ld_wait();
-        uint32_t dd[16];
+        for (int c = 0; c < 2; ++c) {
+          uint32_t sr[32], dr[32];
+          dev::tmem_ld32(t_s + c * 32, sr);
+          dev::tmem_ld32(t_dp + c * 32, dr);
+          dev::tmem_ld_wait();
+          uint32_t dd[16];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          float d2[2];
+          for (int jj = 0; jj < 16; ++jj) {
+            float d2[2];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int kc = c * 32 + 2 * jj + e;
-            float p = exp2f(__uint_as_float(sr[2 * jj + e]) * scale_log2 - my_lse2);
-            if (diag && kc > r) p = 0.f;
-            d2[e] = p * (__uint_as_float(dr[2 * jj + e]) - my_delta);
+            for (int e = 0; e < 2; ++e) {
+              const int kc = half * HALF + c * 32 + 2 * jj + e;
+              float p = dev::ex2(__uint_as_float(sr[2 * jj + e]) * scale_log2 - my_lse2);
+              if (DIAG && kc > r) p = 0.f;
+              d2[e] = p * (__uint_as_float(dr[2 * jj + e]) - my_delta);
+            }
+            dd[jj] = dev::pack_bf16(d2[0], d2[1]);
           }
-          dd[jj] = dev::pack_bf16(d2[0], d2[1]);
+          dev::tmem_st16(t_s + c * 16, dd);
         }
-        dev::tmem_st16(t_s + lane_off + c * 16, dd);
-      }
+      };
+      if (diag)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
       dev::tmem_st_wait();
       dev::tc_fence_before();
-      dev::mbar_arrive(ds_ready);
+      dev::mbar_arrive(&ds_ready[b]);
     }
     dev::mbar_wait(fin, 0);
     dev::tc_fence_after();
@@ -687,7 +818,9 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   std::call_once(f, [] {
     cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
-    cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         BwdSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dq_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
   });
   float* delta = a.delta;
@@ -704,14 +837,45 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
       mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
       scale_log2);
   if (a.ev[2]) cudaEventRecord(a.ev[2], stream);
-  attn_bwd_dq_kernel<D><<<grid, 256, BwdSmem<D>::BYTES, stream>>>(
-      mq, mk, mv, mdo, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
-      scale_log2);
+  static const bool dq_at = [] {
+    const char* e = getenv("MEMO_ATTN_DQ_TMEM_A");
+    return e ? atoi(e) != 0 : false;
+  }();
+  if (dq_at)
+    attn_bwd_dq_kernel<D, true><<<grid, 256, BwdSmem<D>::BYTES, stream>>>(
+        a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
+        a.softmax_scale, scale_log2);
+  else
+    attn_bwd_dq_kernel<D, false><<<grid, 256, BwdSmem<D>::BYTES, stream>>>(
+        a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
+        a.softmax_scale, scale_log2);
   if (a.ev[3]) cudaEventRecord(a.ev[3], stream);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+template <int D, bool QT, bool EMU>
+void launch_fwd(const AttnFwdArgs& a, const CUtensorMap& mq, const CUtensorMap& mk,
+                const CUtensorMap& mv, float scale_log2, cudaStream_t stream) {
+  using L = FwdSmem<D, QT>;
+  static std::once_flag f;
+  std::call_once(f, [] {
+    cudaFuncSetAttribute(attn_fwd_kernel<D, QT, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         L::BYTES);
+  });
+  dim3 grid(a.S / TILE, a.H);
+  attn_fwd_kernel<D, QT, EMU><<<grid, 256, L::BYTES, stream>>>(a.q, mq, mk, mv, a.o, a.lse, a.S,
+                                                               a.H, scale_log2);
+}
+
+int fwd_variant() {
+  static int v = [] {
+    const char* e = getenv("MEMO_ATTN_FWD_VARIANT");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
 
 cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   if (a.S % TILE != 0 || (a.D != 64 && a.D != 128)) return cudaErrorInvalidValue;
@@ -722,24 +886,17 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
             make_tma_2d_bf16(&mv, a.v, h, a.S, h, 64, TILE);
   if (!ok) return cudaErrorInvalidValue;
   const float scale_log2 = a.softmax_scale * kLog2e;
-  dim3 grid(a.S / TILE, a.H);
   if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
+  const int v = fwd_variant();  // bit0: Q in TMEM, bit1: FMA exp2 share
   if (a.D == 128) {
-    static std::once_flag f;
-    std::call_once(f, [] {
-      cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           FwdSmem<128>::BYTES);
-    });
-    attn_fwd_kernel<128><<<grid, 256, FwdSmem<128>::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
-                                                                      a.H, scale_log2);
+    switch (v) {
+      case 0: launch_fwd<128, false, false>(a, mq, mk, mv, scale_log2, stream); break;
+      case 1: launch_fwd<128, true, false>(a, mq, mk, mv, scale_log2, stream); break;
+      case 2: launch_fwd<128, false, true>(a, mq, mk, mv, scale_log2, stream); break;
+      default: launch_fwd<128, true, true>(a, mq, mk, mv, scale_log2, stream); break;
+    }
   } else {
-    static std::once_flag f;
-    std::call_once(f, [] {
-      cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           FwdSmem<64>::BYTES);
-    });
-    attn_fwd_kernel<64><<<grid, 256, FwdSmem<64>::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
-                                                                    a.H, scale_log2);
+    launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
   }
   if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
   return cudaGetLastError();

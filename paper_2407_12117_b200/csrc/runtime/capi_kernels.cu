@@ -63,6 +63,15 @@ extern "C" int memo_attn_bwd(const void* q, const void* k, const void* v, const 
                              const float* lse, const void* dout, float* delta, void* dq, void* dk,
                              void* dv, int64_t ld, const void* rope, int64_t pos0, int32_t S,
                              int32_t H, int32_t D, float scale, void* stream) {
+  return memo_attn_bwd_timed(q, k, v, o, lse, dout, delta, dq, dk, dv, ld, rope, pos0, S, H, D,
+                             scale, stream, nullptr);
+}
+
+extern "C" int memo_attn_bwd_timed(const void* q, const void* k, const void* v, const void* o,
+                                   const float* lse, const void* dout, float* delta, void* dq,
+                                   void* dk, void* dv, int64_t ld, const void* rope, int64_t pos0,
+                                   int32_t S, int32_t H, int32_t D, float scale, void* stream,
+                                   float* ms3) {
   memo::AttnBwdArgs a;
   a.q = static_cast<const __nv_bfloat16*>(q);
   a.k = static_cast<const __nv_bfloat16*>(k);
@@ -81,7 +90,18 @@ extern "C" int memo_attn_bwd(const void* q, const void* k, const void* v, const 
   a.H = H;
   a.D = D;
   a.softmax_scale = scale;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (ms3) {
+    for (auto& x : ev) cudaEventCreate(&x);
+    for (int i = 0; i < 4; ++i) a.ev[i] = ev[i];
+  }
   cudaError_t e = memo::attn_bwd(a, static_cast<cudaStream_t>(stream));
+  if (ms3 && e == cudaSuccess) {
+    cudaEventSynchronize(ev[3]);
+    for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms3[i], ev[i], ev[i + 1]);
+  }
+  if (ms3)
+    for (auto& x : ev) cudaEventDestroy(x);
   if (e != cudaSuccess)
     return set_error(MEMO_ERR_INTERNAL, std::string("memo_attn_bwd: ") + cudaGetErrorString(e));
   return MEMO_OK;

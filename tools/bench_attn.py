@@ -63,9 +63,34 @@ def bench(S, H, D, iters=5, bwd=False):
         ms = e0.elapsed_time(e1) / iters
         out["bwd_ms"] = ms
         out["bwd_tflops_algo"] = 2.5 * flops / ms / 1e9
+        ms3 = (C.c_float * 3)()
+        _abi.check(_abi.lib.memo_attn_bwd_timed(
+            C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()), C.c_void_p(o.data_ptr()),
+            C.c_void_p(lse.data_ptr()), C.c_void_p(do.data_ptr()), C.c_void_p(delta.data_ptr()),
+            C.c_void_p(dqkv.data_ptr()), C.c_void_p(dqkv.data_ptr() + 2 * H * D),
+            C.c_void_p(dqkv.data_ptr() + 4 * H * D), C.c_int64(3 * H * D), None, C.c_int64(0), S, H, D, sc, None, ms3))
+        out["prep_ms"], out["dkdv_ms"], out["dq_ms"] = list(ms3)
+        out["dkdv_tflops"] = 2 * flops / ms3[1] / 1e9
+        out["dq_tflops"] = 1.5 * flops / ms3[2] / 1e9
     return out
 
 
 if __name__ == "__main__":
     for S in [int(x) for x in (sys.argv[1:] or ["8192", "32768"])]:
         print(json.dumps(bench(S, 32, 128, bwd=True)), flush=True)
+    if os.environ.get("MEMO_FWD_SWEEP"):
+        import subprocess
+        for v in range(4):
+            env = dict(os.environ, MEMO_ATTN_FWD_VARIANT=str(v))
+            env.pop("MEMO_FWD_SWEEP")
+            out = subprocess.check_output([sys.executable, __file__, sys.argv[-1]], env=env, text=True)
+            r = json.loads(out.strip().splitlines()[0])
+            print(json.dumps({"variant": v, "S": r["S"], "fwd_tflops": r["fwd_tflops"]}), flush=True)
+    if os.environ.get("MEMO_DQ_SWEEP"):
+        import subprocess
+        for v in range(2):
+            env = dict(os.environ, MEMO_ATTN_DQ_TMEM_A=str(v))
+            env.pop("MEMO_DQ_SWEEP")
+            out = subprocess.check_output([sys.executable, __file__, sys.argv[-1]], env=env, text=True)
+            r = json.loads(out.strip().splitlines()[0])
+            print(json.dumps({"dq_tmem_a": v, "S": r["S"], "dq_ms": r["dq_ms"], "dq_tflops": r["dq_tflops"]}), flush=True)
