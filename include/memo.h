@@ -275,6 +275,21 @@ int memo_exec_plan(memo_exec* ctx, char** json);
  * with param in {embedding, g1, wqkv, wo, g2, wgu, wd, gf, wcls, all}
  * (layer = -1 for non-layer params), or "act/<skeletal component>". */
 int memo_exec_tensor(memo_exec* ctx, const char* name, int32_t layer, void** ptr, size_t* bytes);
+/* ---------------------------------------------------------------- SP + TP
+ * Megatron-style sequence+tensor parallelism over cfg->tp_degree ranks
+ * (reference mapping: tp_degree = t, sp_or_cp_degree = 1).  Collectives run
+ * on NCCL (one process per GPU; the 128-byte unique id comes from
+ * memo_comm_unique_id on rank 0) or on a single-GPU loopback group (t ranks as
+ * t host threads sharing one device — for testing the sharded path). */
+typedef struct memo_loopback_group memo_loopback_group;
+memo_loopback_group* memo_comm_loopback_group(int32_t size);
+void memo_comm_loopback_group_destroy(memo_loopback_group* g);
+int memo_comm_unique_id(uint8_t out[128]);
+/* kind 0: loopback (handle = memo_loopback_group*), kind 1: NCCL (handle = unique id bytes) */
+int memo_exec_create_tp(const memo_model_config* cfg, const memo_hardware_config* hw,
+                        const memo_exec_options* opt, int32_t kind, const void* handle,
+                        int32_t rank, memo_exec** out);
+
 /* Synchronous copy of a named tensor (as memo_exec_tensor) into host memory. */
 int memo_exec_read(memo_exec* ctx, const char* name, int32_t layer, void* host, size_t bytes);
 

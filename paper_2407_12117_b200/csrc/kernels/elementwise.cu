@@ -390,6 +390,126 @@ __global__ void adamw_kernel(float* __restrict__ master, __nv_bfloat16* __restri
   }
 }
 
+
+// ------------------------------------------------------------------ tensor-parallel helpers
+// Counter-hash init of a shard: local [R_l, C_l] whose rows map to global rows
+// through up to three contiguous segments; identical values to the full init.
+struct RowSegs {
+  long long local0[3], count[3], global0[3];
+  int n;
+};
+__global__ void init_sliced_kernel(__nv_bfloat16* __restrict__ w, float* __restrict__ master,
+                                   long long R, long long C, RowSegs segs, long long C_glob,
+                                   long long c_off, uint64_t seed, uint64_t tid, int is_norm) {
+  const long long n = R * C;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / C, c = i - r * C;
+    long long gr = r;
+    for (int k = 0; k < segs.n; ++k)
+      if (r >= segs.local0[k] && r < segs.local0[k] + segs.count[k]) gr = segs.global0[k] + (r - segs.local0[k]);
+    const uint64_t gi = static_cast<uint64_t>(gr * C_glob + c_off + c);
+    const uint64_t h = splitmix64(seed * 0x9E3779B97F4A7C15ULL + tid * 0xD1B54A32D192ED03ULL + gi);
+    const float u = __fmul_rn(static_cast<float>(h >> 40), 1.0f / 16777216.0f);
+    const float x = __fsub_rn(__fmul_rn(2.0f, u), 1.0f);
+    const float v = is_norm ? __fadd_rn(1.0f, __fmul_rn(x, 0.1f)) : __fmul_rn(x, 0.0346410161513775f);
+    const __nv_bfloat16 b = __float2bfloat16_rn(v);
+    w[i] = b;
+    if (master) master[i] = __bfloat162float(b);
+  }
+}
+
+// out = x + bf16(a) ; a_bf16 = bf16(a) (optional).  The reduce-scattered
+// projection output becomes the bf16 skeletal tensor the residual adds.
+__global__ void resid_round_kernel(const float* __restrict__ x, const float* __restrict__ a,
+                                   __nv_bfloat16* __restrict__ a_bf16, float* __restrict__ out,
+                                   long long n4) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float4 xv = reinterpret_cast<const float4*>(x)[i];
+    const float4 av = reinterpret_cast<const float4*>(a)[i];
+    const float r0 = dev::bf16_round(av.x), r1 = dev::bf16_round(av.y), r2 = dev::bf16_round(av.z),
+                r3 = dev::bf16_round(av.w);
+    if (a_bf16) store_bf16x4(a_bf16 + i * 4, r0, r1, r2, r3);
+    reinterpret_cast<float4*>(out)[i] = make_float4(xv.x + r0, xv.y + r1, xv.z + r2, xv.w + r3);
+  }
+}
+
+// Vocab-parallel cross-entropy on a shard of V_l logits per row (columns
+// v0..v0+V_l of the full vocabulary): three passes around two all-reduces.
+__global__ void __launch_bounds__(256) ce_vp_max_kernel(const float* __restrict__ logits,
+                                                        float* __restrict__ rmax, int V) {
+  const float* lr = logits + static_cast<long long>(blockIdx.x) * V;
+  __shared__ float sh[8];
+  float mx = -INFINITY;
+  for (int j = threadIdx.x * 4; j < V; j += 1024) {
+    const float4 t = *reinterpret_cast<const float4*>(lr + j);
+    mx = fmaxf(mx, fmaxf(fmaxf(t.x, t.y), fmaxf(t.z, t.w)));
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = sh[0];
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, sh[w]);
+    rmax[blockIdx.x] = m;
+  }
+}
+// stats[row] = sum exp(x - max) over the shard; stats[T + row] = target logit if owned, else 0
+__global__ void __launch_bounds__(256) ce_vp_sum_kernel(const float* __restrict__ logits,
+                                                        const float* __restrict__ gmax,
+                                                        const int* __restrict__ labels, int v0,
+                                                        float* __restrict__ stats, int T, int V) {
+  const int row = blockIdx.x;
+  const float* lr = logits + static_cast<long long>(row) * V;
+  const float m = gmax[row];
+  __shared__ float sh[8];
+  float sum = 0.f;
+  for (int j = threadIdx.x * 4; j < V; j += 1024) {
+    const float4 t = *reinterpret_cast<const float4*>(lr + j);
+    sum += __expf(t.x - m) + __expf(t.y - m) + __expf(t.z - m) + __expf(t.w - m);
+  }
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += sh[w];
+    stats[row] = s;
+    const int lab = labels[row] - v0;
+    stats[T + row] = (labels[row] >= 0 && lab >= 0 && lab < V) ? lr[lab] : 0.f;
+  }
+}
+__global__ void __launch_bounds__(256) ce_vp_grad_kernel(const float* __restrict__ logits,
+                                                         const float* __restrict__ gmax,
+                                                         const float* __restrict__ gstats,
+                                                         const int* __restrict__ labels, int v0,
+                                                         __nv_bfloat16* __restrict__ dlogits,
+                                                         float* __restrict__ loss_rows, int T, int V,
+                                                         float inv_n) {
+  const int row = blockIdx.x;
+  const float* lr = logits + static_cast<long long>(row) * V;
+  __nv_bfloat16* dr = dlogits + static_cast<long long>(row) * V;
+  const int label = labels[row];
+  if (label < 0) {
+    for (int j = threadIdx.x * 4; j < V; j += 1024) store_bf16x4(dr + j, 0.f, 0.f, 0.f, 0.f);
+    if (threadIdx.x == 0) loss_rows[row] = 0.f;
+    return;
+  }
+  const float m = gmax[row], inv_sum = 1.f / gstats[row];
+  const int lab = label - v0;
+  for (int j = threadIdx.x * 4; j < V; j += 1024) {
+    const float4 t = *reinterpret_cast<const float4*>(lr + j);
+    float p[4] = {__expf(t.x - m) * inv_sum, __expf(t.y - m) * inv_sum, __expf(t.z - m) * inv_sum,
+                  __expf(t.w - m) * inv_sum};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (j + k == lab) p[k] -= 1.f;
+    store_bf16x4(dr + j, p[0] * inv_n, p[1] * inv_n, p[2] * inv_n, p[3] * inv_n);
+  }
+  if (threadIdx.x == 0) loss_rows[row] = (m + logf(gstats[row])) - gstats[T + row];
+}
+
 int stride_grid(long long n, int per_thread, int threads) {
   const long long want = (n / per_thread + threads - 1) / threads;
   const long long cap = static_cast<long long>(num_sms()) * 16;
@@ -397,6 +517,45 @@ int stride_grid(long long n, int per_thread, int threads) {
 }
 
 }  // namespace
+
+cudaError_t init_sliced(__nv_bfloat16* w, float* master, long long R, long long C,
+                        const long long* local0, const long long* count, const long long* global0,
+                        int nseg, long long C_glob, long long c_off, uint64_t seed, uint64_t tid,
+                        bool is_norm, cudaStream_t st) {
+  RowSegs segs{};
+  segs.n = nseg;
+  for (int k = 0; k < nseg && k < 3; ++k) {
+    segs.local0[k] = local0[k];
+    segs.count[k] = count[k];
+    segs.global0[k] = global0[k];
+  }
+  init_sliced_kernel<<<stride_grid(R * C, 1, 256), 256, 0, st>>>(w, master, R, C, segs, C_glob, c_off,
+                                                                 seed, tid, is_norm);
+  return cudaGetLastError();
+}
+
+cudaError_t resid_round(const float* x, const float* a, __nv_bfloat16* a_bf16, float* out,
+                        long long n, cudaStream_t st) {
+  if (n % 4) return cudaErrorInvalidValue;
+  resid_round_kernel<<<stride_grid(n, 4, 256), 256, 0, st>>>(x, a, a_bf16, out, n / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t ce_vp_max(const float* logits, float* rmax, int T, int V, cudaStream_t st) {
+  ce_vp_max_kernel<<<T, 256, 0, st>>>(logits, rmax, V);
+  return cudaGetLastError();
+}
+cudaError_t ce_vp_sum(const float* logits, const float* gmax, const int* labels, int v0,
+                      float* stats, int T, int V, cudaStream_t st) {
+  ce_vp_sum_kernel<<<T, 256, 0, st>>>(logits, gmax, labels, v0, stats, T, V);
+  return cudaGetLastError();
+}
+cudaError_t ce_vp_grad(const float* logits, const float* gmax, const float* gstats,
+                       const int* labels, int v0, __nv_bfloat16* dlogits, float* loss_rows, int T,
+                       int V, float inv_n, cudaStream_t st) {
+  ce_vp_grad_kernel<<<T, 256, 0, st>>>(logits, gmax, gstats, labels, v0, dlogits, loss_rows, T, V, inv_n);
+  return cudaGetLastError();
+}
 
 cudaError_t init_uniform(__nv_bfloat16* w, float* master, long long n, uint64_t seed,
                          uint64_t tid, bool is_norm, cudaStream_t st) {

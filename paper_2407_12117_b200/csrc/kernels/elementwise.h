@@ -35,4 +35,18 @@ cudaError_t adamw(float* master, __nv_bfloat16* w, const float* grad, float* m, 
                   long long n, float lr, float b1, float b2, float eps, float wd, int step,
                   cudaStream_t st);
 
+// Tensor-parallel helpers.
+cudaError_t init_sliced(__nv_bfloat16* w, float* master, long long R, long long C,
+                        const long long* local0, const long long* count, const long long* global0,
+                        int nseg, long long C_glob, long long c_off, uint64_t seed, uint64_t tid,
+                        bool is_norm, cudaStream_t st);
+cudaError_t resid_round(const float* x, const float* a, __nv_bfloat16* a_bf16, float* out,
+                        long long n, cudaStream_t st);
+cudaError_t ce_vp_max(const float* logits, float* rmax, int T, int V, cudaStream_t st);
+cudaError_t ce_vp_sum(const float* logits, const float* gmax, const int* labels, int v0,
+                      float* stats, int T, int V, cudaStream_t st);
+cudaError_t ce_vp_grad(const float* logits, const float* gmax, const float* gstats,
+                       const int* labels, int v0, __nv_bfloat16* dlogits, float* loss_rows, int T,
+                       int V, float inv_n, cudaStream_t st);
+
 }  // namespace memo

@@ -5,6 +5,7 @@
 #include "host/convert.hpp"
 #include "host/status.hpp"
 #include "memo.h"
+#include "runtime/comm.h"
 #include "runtime/executor.h"
 
 struct memo_exec {
@@ -51,10 +52,72 @@ extern "C" int memo_exec_options_default(memo_exec_options* o) {
   return MEMO_OK;
 }
 
+struct memo_loopback_group {
+  std::shared_ptr<memo::LoopbackGroup> g;
+};
+
+extern "C" memo_loopback_group* memo_comm_loopback_group(int32_t size) {
+  try {
+    return new memo_loopback_group{memo::make_loopback_group(size)};
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+extern "C" void memo_comm_loopback_group_destroy(memo_loopback_group* g) { delete g; }
+
+extern "C" int memo_comm_unique_id(uint8_t out[128]) {
+  return guard([&] {
+    if (!memo::nccl_get_unique_id(out)) throw memo::PlanError(1, "NCCL unavailable (ncclGetUniqueId)");
+  });
+}
+
+namespace {
+memo::ExecOptions to_options(const memo_exec_options* o);
+}
+
+extern "C" int memo_exec_create_tp(const memo_model_config* cfg, const memo_hardware_config* hw,
+                                   const memo_exec_options* o, int32_t kind, const void* handle,
+                                   int32_t rank, memo_exec** out) {
+  return guard([&] {
+    if (!cfg || !hw || !o || !out || !handle) throw memo::ConfigError("null argument");
+    const int t = static_cast<int>(cfg->tp_degree);
+    std::unique_ptr<memo::Comm> comm;
+    if (kind == 0)
+      comm = memo::make_loopback_comm(static_cast<const memo_loopback_group*>(handle)->g, rank);
+    else if (kind == 1)
+      comm = memo::make_nccl_comm(handle, rank, t);
+    else
+      throw memo::ConfigError("unknown communicator kind");
+    auto* ctx = new memo_exec{nullptr};
+    try {
+      ctx->ex = new memo::Executor(memo::from_c(*cfg), memo::from_c(*hw), to_options(o), std::move(comm));
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
 extern "C" int memo_exec_create(const memo_model_config* cfg, const memo_hardware_config* hw,
                                 const memo_exec_options* o, memo_exec** out) {
   return guard([&] {
     if (!cfg || !hw || !o || !out) throw memo::ConfigError("null argument");
+    memo::ExecOptions d = to_options(o);
+    auto* ctx = new memo_exec{nullptr};
+    try {
+      ctx->ex = new memo::Executor(memo::from_c(*cfg), memo::from_c(*hw), d);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+namespace {
+memo::ExecOptions to_options(const memo_exec_options* o) {
     memo::ExecOptions d;
     d.seed = o->seed;
     d.alpha = o->alpha;
@@ -74,16 +137,9 @@ extern "C" int memo_exec_create(const memo_model_config* cfg, const memo_hardwar
     d.alignment = o->alignment;
     d.dry_run = o->dry_run != 0;
     d.op_timing = o->op_timing != 0;
-    auto* ctx = new memo_exec{nullptr};
-    try {
-      ctx->ex = new memo::Executor(memo::from_c(*cfg), memo::from_c(*hw), d);
-    } catch (...) {
-      delete ctx;
-      throw;
-    }
-    *out = ctx;
-  });
+    return d;
 }
+}  // namespace
 
 extern "C" void memo_exec_destroy(memo_exec* ctx) {
   if (!ctx) return;

@@ -50,6 +50,10 @@ Bytes up(Bytes v, Bytes a = kAlign) { return (v + a - 1) / a * a; }
 
 enum Comp { C_X = 0, C_XN, C_Q, C_K, C_V, C_O, C_A, C_XN2, C_GU, C_ACT, C_N };
 
+std::string lkey(int layer, const char* n) { return "L" + std::to_string(layer) + "/" + n; }
+
+}  // namespace
+
 // Request-trace builder: names are resolved to ids per segment; skeletal
 // tensors are keyed by layer so their free in the backward segment matches.
 class TraceBuilder {
@@ -81,17 +85,15 @@ class TraceBuilder {
   std::map<TensorId, std::pair<std::size_t, std::string>> names_;
 };
 
-std::string lkey(int layer, const char* n) { return "L" + std::to_string(layer) + "/" + n; }
 
-}  // namespace
-
-Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const ExecOptions& opt)
-    : cfg_(cfg_in), hw_(hw), opt_(opt) {
+Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const ExecOptions& opt,
+                   std::unique_ptr<Comm> comm)
+    : cfg_(cfg_in), hw_(hw), opt_(opt), comm_(std::move(comm)) {
   cfg_.validate();
   hw_.validate();
   if (cfg_.batch != 1) throw ConfigError("executor supports batch == 1 (MEMO's long-context setting)");
-  if (cfg_.tp_degree != 1 || cfg_.sp_or_cp_degree != 1)
-    throw ConfigError("single-GPU executor: tp_degree and sp_or_cp_degree must be 1");
+  if (cfg_.sp_or_cp_degree != 1)
+    throw ConfigError("Megatron SP+TP maps to tp_degree = t, sp_or_cp_degree = 1 (SURVEY discovery 4)");
   if (cfg_.dtype_bytes != 2) throw ConfigError("executor computes in bf16 (dtype_bytes = 2)");
   if ((cfg_.ffn_hidden * 2) % 3) throw ConfigError("ffn_hidden must be 1.5 x the SwiGLU width");
   d_.S = static_cast<int>(cfg_.seq_len);
@@ -101,16 +103,29 @@ Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const Ex
   d_.F = static_cast<int>(cfg_.ffn_hidden * 2 / 3);
   d_.V = static_cast<int>(cfg_.vocab);
   d_.n = static_cast<int>(cfg_.n_layers);
+  d_.t = static_cast<int>(cfg_.tp_degree);
+  d_.r = comm_ ? comm_->rank() : 0;
+  if (d_.t > 1 && (!comm_ || comm_->size() != d_.t) && !opt_.dry_run)
+    throw ConfigError("tp_degree > 1 needs a communicator of that size");
   if (d_.h % d_.H || (d_.D != 64 && d_.D != 128)) throw ConfigError("head_dim must be 64 or 128");
   if (d_.S % 128 || d_.h % 256 || d_.F % 256 || d_.V % 256)
     throw ConfigError("seq_len % 128, hidden % 256, intermediate % 256 and vocab % 256 must be 0");
+  if (d_.S % (128 * d_.t) || d_.H % d_.t || d_.F % (32 * d_.t) || d_.V % (32 * d_.t))
+    throw ConfigError("seq_len/(128 t), heads/t, intermediate/(32 t) and vocab/(32 t) must be whole");
+  d_.Sl = d_.S / d_.t;
+  d_.Hl = d_.H / d_.t;
+  d_.hl = d_.Hl * d_.D;
+  d_.Fl = d_.F / d_.t;
+  d_.Vl = d_.V / d_.t;
   if (opt_.ce_chunk <= 0 || opt_.ce_chunk % 128) throw ConfigError("ce_chunk must be a positive multiple of 128");
 
   // The executor's saved tensors define the skeletal weights (multiples of
-  // b*s*h*dtype bytes); LSE (f32 [H,S]) rides in attn_out.
+  // b*s*(h/t)*dtype bytes per device); LSE (f32 [H/t, S]) rides in attn_out.
+  // Sequence-sharded components hold S/t rows of full width, head-sharded ones
+  // S rows of width/t — the same bytes, hence the same weights for every t.
   const double h = d_.h, F = d_.F;
-  row_bytes_ = {4ull * d_.h, 2ull * d_.h, 2ull * d_.h, 2ull * d_.h, 2ull * d_.h, 2ull * d_.h,
-                2ull * d_.h, 2ull * d_.h, 4ull * d_.F, 2ull * d_.F};
+  row_bytes_ = {4ull * d_.h,  2ull * d_.h,  2ull * d_.hl, 2ull * d_.hl, 2ull * d_.hl,
+                2ull * d_.hl, 2ull * d_.h,  2ull * d_.h,  4ull * d_.Fl, 2ull * d_.Fl};
   const double w[C_N] = {2.0, 1.0, 1.0, 1.0, 1.0, 1.0 + 2.0 / d_.D, 1.0, 1.0, 2.0 * F / h, F / h};
   cfg_.skeletal_weight_overrides.clear();
   for (int c = 0; c < C_N; ++c) cfg_.skeletal_weight_overrides[kSkeletalNames[c]] = w[c];
@@ -122,17 +137,20 @@ Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const Ex
     rb_bytes_ += sk_.components[c].second;
   }
   {
-    const Bytes want = static_cast<Bytes>(d_.S) * (4ull * d_.h + 2ull * d_.h * 7 + 6ull * d_.F) +
-                       4ull * d_.H * d_.S;
+    const Bytes want = static_cast<Bytes>(d_.Sl) * (4ull * d_.h + 2ull * d_.h * 3) +
+                       static_cast<Bytes>(d_.S) * (2ull * d_.hl * 4 + 6ull * d_.Fl) +
+                       4ull * d_.Hl * d_.S;
     if (want != rb_bytes_) throw PlanError(1, "internal: skeletal model does not match executor layout");
   }
 
-  // alpha and the token split (swap.hpp:105, schedule.hpp:409, swap.hpp:177)
+  // alpha and the token split (swap.hpp:105, schedule.hpp:409, swap.hpp:177);
+  // sequence-sharded components split their S/t local rows (SURVEY §7 hard part v).
   Timing tm = timing_of(cfg_, hw_, params_of(cfg_));
   const double t_layer = opt_.t_layer > 0 ? opt_.t_layer : tm.t_fwd_layer;
   swap_ = opt_.alpha >= 0 ? swap_with_alpha(sk_, hw_, opt_.alpha, cfg_.n_layers)
                           : solve_alpha_for(sk_, hw_, t_layer, cfg_.n_layers);
   split_ = split_tokens(swap_.alpha, cfg_.seq_local(), opt_.token_granularity);
+  split_l_ = split_tokens(swap_.alpha, static_cast<std::uint64_t>(d_.Sl), opt_.token_granularity);
   can_swap_ = swap_on_ = opt_.swap_enabled;
 
   build_trace_and_plan();
@@ -142,12 +160,19 @@ Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const Ex
   init_weights();
 }
 
+const TokenRange& Executor::split_of(int c) const {
+  return (c == C_X || c == C_XN || c == C_A || c == C_XN2) ? split_l_ : split_;
+}
+
 void Executor::build_trace_and_plan() {
   const Bytes S = d_.S, h = d_.h, F = d_.F, V = d_.V, H = d_.H;
   const Bytes T = std::min<Bytes>(static_cast<Bytes>(opt_.ce_chunk), S);
   const Bytes P = static_cast<Bytes>(rmsnorm_bwd_partials(d_.S));
   const Bytes R = split_.recompute_tokens;
   TraceBuilder tb;
+  if (d_.t > 1) {
+    build_trace_tp(tb);
+  } else {
   seg_emb_fwd_ = tb.begin(Phase::EmbFwd, -1);
   tb.malloc("x_final", S * h * 4, "x_final");
   tb.malloc("dx_carry", S * h * 4, "dx_carry");
@@ -210,6 +235,7 @@ void Executor::build_trace_and_plan() {
   tb.free("dxb_carry");
   tb.free("dx_carry");
   tb.free("x_final");
+  }
   Trace& t = tb.trace();
   t.n_layers = d_.n;
   trace_text_ = trace_to_text(t);
@@ -223,6 +249,126 @@ void Executor::build_trace_and_plan() {
   }
 }
 
+// SP+TP request trace of one rank (same segment structure; every layer
+// segment identical so the bi-level plan stays provably optimal).
+void Executor::build_trace_tp(TraceBuilder& tb) {
+  const Bytes S = d_.S, Sl = d_.Sl, h = d_.h, hl = d_.hl, Fl = d_.Fl, Vl = d_.Vl, Hl = d_.Hl;
+  const Bytes T = std::min<Bytes>(static_cast<Bytes>(opt_.ce_chunk), S);
+  const Bytes P = static_cast<Bytes>(rmsnorm_bwd_partials(d_.Sl));
+  const Bytes R = split_.recompute_tokens;
+  seg_emb_fwd_ = tb.begin(Phase::EmbFwd, -1);
+  tb.malloc("x_final", Sl * h * 4, "x_final");
+  tb.malloc("dx_carry", Sl * h * 4, "dx_carry");
+  tb.malloc("dxb_carry", Sl * h * 2, "dxb_carry");
+  auto sk = [&](int i, int c) { tb.malloc(lkey(i, kSkeletalNames[c]), sk_.components[c].second, kSkeletalNames[c]); };
+  for (int i = 0; i < d_.n; ++i) {
+    seg_fwd_.push_back(tb.begin(Phase::LayerFwd, i));
+    auto m = [&](const char* n, Bytes b) { tb.malloc(lkey(i, n), b, n); };
+    auto f = [&](const char* n) { tb.free(lkey(i, n)); };
+    sk(i, C_X);
+    sk(i, C_XN);
+    m("xn_full", S * h * 2);
+    sk(i, C_Q);
+    sk(i, C_K);
+    sk(i, C_V);
+    f("xn_full");
+    sk(i, C_O);
+    m("a_part", S * h * 4);
+    m("a_red", Sl * h * 4);
+    f("a_part");
+    sk(i, C_A);
+    m("x1", Sl * h * 4);
+    f("a_red");
+    sk(i, C_XN2);
+    m("xn2_full", S * h * 2);
+    sk(i, C_GU);
+    sk(i, C_ACT);
+    f("xn2_full");
+    m("d_part", S * h * 4);
+    m("d_red", Sl * h * 4);
+    f("d_part");
+    f("d_red");
+    f("x1");
+  }
+  seg_cls_fwd_ = tb.begin(Phase::ClsFwd, -1);
+  tb.malloc("xf", Sl * h * 2, "xf");
+  seg_cls_bwd_ = tb.begin(Phase::ClsBwd, -1);
+  tb.malloc("xf_full", S * h * 2, "xf_full");
+  tb.malloc("dxf_part", S * h * 4, "dxf_part");
+  tb.malloc("loss_rows", S * 4, "loss_rows");
+  tb.malloc("logits", T * Vl * 4, "logits");
+  tb.malloc("dlogits", T * Vl * 2, "dlogits");
+  tb.malloc("ce_stats", 6 * T * 4, "ce_stats");
+  tb.free("ce_stats");
+  tb.free("logits");
+  tb.free("dlogits");
+  tb.free("loss_rows");
+  tb.free("xf_full");
+  tb.malloc("dxf", Sl * h * 4, "dxf");
+  tb.free("dxf_part");
+  tb.malloc("cls_part", P * h * 4, "cls_part");
+  tb.free("cls_part");
+  tb.free("dxf");
+  tb.free("xf");
+  seg_bwd_.assign(d_.n, 0);
+  for (int i = d_.n - 1; i >= 0; --i) {
+    seg_bwd_[i] = tb.begin(Phase::LayerBwd, i);
+    auto m = [&](const char* n, Bytes b) { tb.malloc(lkey(i, n), b, n); };
+    auto f = [&](const char* n) { tb.free(lkey(i, n)); };
+    if (R > 0) {  // recompute transients, carried by every layer
+      m("r_xn_full", S * h * 2);
+      f("r_xn_full");
+      m("r_a_part", S * h * 4);
+      m("r_a_red", Sl * h * 4);
+      f("r_a_part");
+      m("r_x1", Sl * h * 4);
+      f("r_a_red");
+      m("r_xn2_full", S * h * 2);
+      f("r_xn2_full");
+      f("r_x1");
+    }
+    m("dy_full", S * h * 2);
+    m("dact", S * Fl * 2);
+    m("dgu", S * 2 * Fl * 2);
+    f("dact");
+    m("dxn2_part", S * h * 4);
+    m("dxn2", Sl * h * 4);
+    f("dxn2_part");
+    m("b_xn2_full", S * h * 2);
+    f("b_xn2_full");
+    f("dgu");
+    f("dy_full");
+    m("da", Sl * h * 2);
+    m("part2", P * h * 4);
+    f("part2");
+    f("dxn2");
+    m("da_full", S * h * 2);
+    m("dout", S * hl * 2);
+    f("da");
+    f("da_full");
+    m("attn_ws", 2 * Hl * S * 4);
+    m("dqkv", S * 3 * hl * 2);
+    f("attn_ws");
+    f("dout");
+    m("dxn_part", S * h * 4);
+    m("dxn", Sl * h * 4);
+    f("dxn_part");
+    m("b_xn_full", S * h * 2);
+    f("b_xn_full");
+    f("dqkv");
+    m("part1", P * h * 4);
+    f("part1");
+    f("dxn");
+    for (int c = C_N - 1; c >= 0; --c) tb.free(lkey(i, kSkeletalNames[c]));
+  }
+  seg_emb_bwd_ = tb.begin(Phase::EmbBwd, -1);
+  tb.malloc("ar_tmp", static_cast<Bytes>(d_.V) * h * 4, "ar_tmp");
+  tb.free("ar_tmp");
+  tb.free("dxb_carry");
+  tb.free("dx_carry");
+  tb.free("x_final");
+}
+
 void* Executor::arena_ptr(std::size_t seg, const char* name) const {
   auto it = arena_off_.find({seg, name});
   if (it == arena_off_.end()) throw PlanError(1, std::string("internal: no arena slot for ") + name);
@@ -230,23 +376,25 @@ void* Executor::arena_ptr(std::size_t seg, const char* name) const {
 }
 
 void Executor::compute_layout() {
-  const long long h = d_.h, F = d_.F, V = d_.V;
+  const long long h = d_.h, V = d_.V, hl = d_.hl, Fl = d_.Fl, Vl = d_.Vl;
   long long off = 0;
   auto add = [&](const std::string& n, int layer, long long cnt) {
     ptab_[{n, layer}] = {off, cnt};
     off += cnt;
   };
+  // local shards: Wqkv/Wgu column-parallel, Wo/Wd row-parallel, Wcls
+  // vocab-parallel; embedding and norm weights replicated (t = 1: full tensors)
   add("embedding", -1, V * h);
   for (int l = 0; l < d_.n; ++l) {
     add("g1", l, h);
-    add("wqkv", l, 3 * h * h);
-    add("wo", l, h * h);
+    add("wqkv", l, 3 * hl * h);
+    add("wo", l, h * hl);
     add("g2", l, h);
-    add("wgu", l, 2 * F * h);
-    add("wd", l, h * F);
+    add("wgu", l, 2 * Fl * h);
+    add("wd", l, h * Fl);
   }
   add("gf", -1, h);
-  add("wcls", -1, V * h);
+  add("wcls", -1, Vl * h);
   n_params_ = off;
   const Bytes Pn = static_cast<Bytes>(n_params_);
   const Bytes sz_params = up(Pn * 2), sz_f32 = up(Pn * 4);
@@ -259,7 +407,7 @@ void Executor::compute_layout() {
   host_slot_.assign(d_.n, 0);
   per_layer_host_ = sk_.components[C_X].second + sk_.components[C_O].second;
   for (int c = 0; c < C_N; ++c)
-    if (c != C_X && c != C_O) per_layer_host_ += split_.swap_tokens * row_bytes_[c];
+    if (c != C_X && c != C_O) per_layer_host_ += split_of(c).swap_tokens * row_bytes_[c];
   const int swapped = d_.n >= 3 ? d_.n - 2 : 0;
   pinned_bytes_ = can_swap_ ? per_layer_host_ * swapped : 0;
   for (int i = 0; i < swapped; ++i) host_slot_[i] = per_layer_host_ * i;
@@ -354,7 +502,30 @@ void Executor::init_weights() {
       tid = 1 + 6ull * layer + k;
     }
     const bool is_norm = name == "g1" || name == "g2" || name == "gf";
-    ck(init_uniform(params_ + o, master_ + o, n, opt_.seed, tid, is_norm, cs_), "init_uniform");
+    const long long h = d_.h, hl = d_.hl, Fl = d_.Fl, Vl = d_.Vl, r = d_.r;
+    if (d_.t == 1 || name == "embedding" || is_norm) {
+      ck(init_uniform(params_ + o, master_ + o, n, opt_.seed, tid, is_norm, cs_), "init_uniform");
+      continue;
+    }
+    // shard of the full tensor: same counter-hash values as the unsharded init
+    long long l0[3] = {0, 0, 0}, cnt[3] = {0, 0, 0}, g0[3] = {0, 0, 0};
+    int nseg = 1;
+    long long R = 0, Cl = 0, Cg = 0, coff = 0;
+    if (name == "wqkv") {
+      R = 3 * hl; Cl = h; Cg = h; nseg = 3;
+      for (int k = 0; k < 3; ++k) { l0[k] = k * hl; cnt[k] = hl; g0[k] = k * h + r * hl; }
+    } else if (name == "wo") {
+      R = h; Cl = hl; Cg = h; coff = r * hl; cnt[0] = h;
+    } else if (name == "wgu") {
+      R = 2 * Fl; Cl = h; Cg = h; nseg = 2;
+      for (int k = 0; k < 2; ++k) { l0[k] = k * Fl; cnt[k] = Fl; g0[k] = k * static_cast<long long>(d_.F) + r * Fl; }
+    } else if (name == "wd") {
+      R = h; Cl = Fl; Cg = d_.F; coff = r * Fl; cnt[0] = h;
+    } else {  // wcls
+      R = Vl; Cl = h; Cg = h; cnt[0] = Vl; g0[0] = r * Vl;
+    }
+    ck(init_sliced(params_ + o, master_ + o, R, Cl, l0, cnt, g0, nseg, Cg, coff, opt_.seed, tid,
+                   false, cs_), "init_sliced");
   }
   ck(cudaMemsetAsync(adam_m_, 0, n_params_ * 4, cs_), "memset");
   ck(cudaMemsetAsync(adam_v_, 0, n_params_ * 4, cs_), "memset");
@@ -506,13 +677,14 @@ void Executor::load_batch(const int* tokens, const int* labels) {
   int* pos = st + 2 * S;
   int* offs = st + 3 * S;
   std::fill(offs, offs + V + 1, 0);
-  for (int t = 0; t < S; ++t) {
+  for (int t = 0; t < S; ++t)
     if (tokens[t] < 0 || tokens[t] >= V) throw ConfigError("token id out of range");
-    ++offs[tokens[t] + 1];
-  }
+  // embedding-gradient CSR over this rank's token shard (positions are local rows)
+  const int t0 = d_.r * d_.Sl, t1 = t0 + d_.Sl;
+  for (int t = t0; t < t1; ++t) ++offs[tokens[t] + 1];
   for (int v = 0; v < V; ++v) offs[v + 1] += offs[v];
   std::vector<int> fillp(offs, offs + V);
-  for (int t = 0; t < S; ++t) pos[fillp[tokens[t]]++] = t;
+  for (int t = t0; t < t1; ++t) pos[fillp[tokens[t]]++] = t - t0;
   n_labeled_ = 0;
   for (int t = 0; t < S; ++t) n_labeled_ += labels[t] >= 0;
   if (n_labeled_ == 0) throw ConfigError("batch has no labeled tokens");
@@ -538,7 +710,7 @@ void Executor::offload(int i) {
   put(C_X, sk_.components[C_X].second);
   put(C_O, sk_.components[C_O].second);
   for (int c = 0; c < C_N; ++c)
-    if (c != C_X && c != C_O) put(c, split_.swap_tokens * row_bytes_[c]);
+    if (c != C_X && c != C_O) put(c, split_of(c).swap_tokens * row_bytes_[c]);
   stats_.offload_bytes += static_cast<double>(moved);
   mark(1, static_cast<int>(Kind::Offload), i, false);
   ck(cudaEventRecord(ev_off_done_[i], os_), "record");
@@ -558,7 +730,7 @@ void Executor::prefetch(int i) {
   const char* hp = host + bx + bo;
   for (int c = 0; c < C_N; ++c) {
     if (c == C_X || c == C_O) continue;
-    const Bytes b = split_.swap_tokens * row_bytes_[c];
+    const Bytes b = split_of(c).swap_tokens * row_bytes_[c];
     if (b == 0) continue;
     ck(cudaMemcpyAsync(comp(i, c), hp, b, cudaMemcpyHostToDevice, ps_), "H2D");
     hp += b;
@@ -743,6 +915,273 @@ void Executor::classifier() {
   mark(0, static_cast<int>(Kind::ClsBwd), -1, false);
 }
 
+// ================================================================== SP + TP
+// Megatron sequence+tensor parallelism.  Per layer forward:
+//   xn = norm(x_local) -> AG -> QKV (column-parallel, local heads) -> attention
+//   -> out-proj (row-parallel) -> RS -> x1 = x + a -> norm -> AG -> gate/up
+//   (column-parallel) -> SwiGLU -> down (row-parallel) -> RS -> x + d.
+// Backward mirrors it with AG <-> RS swapped; all-gathered activations are
+// regathered rather than saved (the skeletal tensors stay sharded).
+namespace {
+inline void ag(Comm* c, const __nv_bfloat16* src, __nv_bfloat16* dst, size_t count, cudaStream_t st) {
+  c->all_gather(src, dst, count, CommDtype::BF16, st);
+}
+inline void rs(Comm* c, const float* src, float* dst, size_t count, cudaStream_t st) {
+  c->reduce_scatter(src, dst, count, CommDtype::F32, st);
+}
+}  // namespace
+
+void Executor::layer_fwd_tp(int i) {
+  const int S = d_.S, Sl = d_.Sl, h = d_.h, hl = d_.hl, Fl = d_.Fl, Hl = d_.Hl, D = d_.D;
+  if (i >= 2 && swaps(i - 2)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 2], 0));  // F3
+  mark(0, static_cast<int>(Kind::LayerFwd), i, true);
+  const std::size_t seg = seg_fwd_[i];
+  auto P = [&](const char* n) { return params_ + ptab_.at({n, i}).first; };
+  auto A_ = [&](const char* n) { return arena_ptr(seg, n); };
+  float* X = reinterpret_cast<float*>(comp(i, C_X));
+  auto* XN = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN));
+  auto* Q = reinterpret_cast<__nv_bfloat16*>(comp(i, C_Q));
+  auto* K = reinterpret_cast<__nv_bfloat16*>(comp(i, C_K));
+  auto* Vv = reinterpret_cast<__nv_bfloat16*>(comp(i, C_V));
+  auto* O = reinterpret_cast<__nv_bfloat16*>(comp(i, C_O));
+  float* LSE = reinterpret_cast<float*>(comp(i, C_O) + static_cast<Bytes>(S) * hl * 2);
+  auto* A = reinterpret_cast<__nv_bfloat16*>(comp(i, C_A));
+  auto* XN2 = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN2));
+  auto* GU = reinterpret_cast<__nv_bfloat16*>(comp(i, C_GU));
+  auto* ACT = reinterpret_cast<__nv_bfloat16*>(comp(i, C_ACT));
+  auto* xn_full = static_cast<__nv_bfloat16*>(A_("xn_full"));
+  float* a_part = static_cast<float*>(A_("a_part"));
+  float* a_red = static_cast<float*>(A_("a_red"));
+  float* x1 = static_cast<float*>(A_("x1"));
+  auto* xn2_full = static_cast<__nv_bfloat16*>(A_("xn2_full"));
+  float* d_part = static_cast<float*>(A_("d_part"));
+  float* d_red = static_cast<float*>(A_("d_red"));
+  const size_t shard = static_cast<size_t>(Sl) * h;
+
+  G(rmsnorm_fwd(X, nullptr, P("g1"), XN, Sl, h, opt_.eps, cs_));
+  ag(comm_.get(), XN, xn_full, shard, cs_);
+  GemmDesc g = gd(S, 3 * hl, h, xn_full, h, 0, P("wqkv"), h, 0, GEMM_EPI_QKV_ROPE, nullptr, 0);
+  g.q = Q; g.k = K; g.v = Vv; g.hidden = hl; g.head_dim = D; g.rope = rope_; g.pos0 = 0;
+  gemm(g);
+  AttnFwdArgs fa{Q, K, Vv, O, LSE, S, Hl, D, 1.0f / std::sqrt(static_cast<float>(D))};
+  attention_fwd(fa);
+  gemm(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, a_part, h));
+  rs(comm_.get(), a_part, a_red, shard, cs_);
+  G(resid_round(X, a_red, A, x1, static_cast<long long>(shard), cs_));
+  G(rmsnorm_fwd(x1, nullptr, P("g2"), XN2, Sl, h, opt_.eps, cs_));
+  ag(comm_.get(), XN2, xn2_full, shard, cs_);
+  gemm(gd(S, 2 * Fl, h, xn2_full, h, 0, P("wgu"), h, 0, GEMM_EPI_BF16, GU, 2 * Fl));
+  G(swiglu_fwd(GU, ACT, S, Fl, cs_));
+  gemm(gd(S, h, Fl, ACT, Fl, 0, P("wd"), Fl, 0, GEMM_EPI_F32, d_part, h));
+  rs(comm_.get(), d_part, d_red, shard, cs_);
+  float* out = i + 1 < d_.n ? reinterpret_cast<float*>(comp(i + 1, C_X))
+                            : static_cast<float*>(arena_ptr(seg_emb_fwd_, "x_final"));
+  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 1], 0));  // RB drained
+  G(resid_round(x1, d_red, nullptr, out, static_cast<long long>(shard), cs_));
+  stats_.kernel_launches += 5;
+  mark(0, static_cast<int>(Kind::LayerFwd), i, false);
+  G(cudaEventRecord(ev_fwd_done_[i], cs_));
+  if (swaps(i)) offload(i);
+}
+
+void Executor::layer_recompute_tp(int i) {
+  const int S = d_.S, Sl = d_.Sl, h = d_.h, hl = d_.hl, Fl = d_.Fl, D = d_.D;
+  const int sw = static_cast<int>(split_.swap_tokens), R = static_cast<int>(split_.recompute_tokens);
+  const int swl = static_cast<int>(split_l_.swap_tokens), Rl = static_cast<int>(split_l_.recompute_tokens);
+  G(cudaStreamWaitEvent(cs_, ev_pre_mand_[i], 0));  // B3 (+ prefetch-before-recompute)
+  mark(0, static_cast<int>(Kind::Recompute), i, true);
+  if (R > 0 || Rl > 0) {
+    const std::size_t seg = seg_bwd_[i];
+    auto P = [&](const char* n) { return params_ + ptab_.at({n, i}).first; };
+    auto A_ = [&](const char* n) { return arena_ptr(seg, n); };
+    float* X = reinterpret_cast<float*>(comp(i, C_X));
+    auto* XN = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN));
+    auto* Q = reinterpret_cast<__nv_bfloat16*>(comp(i, C_Q));
+    auto* K = reinterpret_cast<__nv_bfloat16*>(comp(i, C_K));
+    auto* Vv = reinterpret_cast<__nv_bfloat16*>(comp(i, C_V));
+    auto* O = reinterpret_cast<__nv_bfloat16*>(comp(i, C_O));
+    auto* A = reinterpret_cast<__nv_bfloat16*>(comp(i, C_A));
+    auto* XN2 = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN2));
+    auto* GU = reinterpret_cast<__nv_bfloat16*>(comp(i, C_GU));
+    auto* ACT = reinterpret_cast<__nv_bfloat16*>(comp(i, C_ACT));
+    auto* xn_full = static_cast<__nv_bfloat16*>(A_("r_xn_full"));
+    float* a_part = static_cast<float*>(A_("r_a_part"));
+    float* a_red = static_cast<float*>(A_("r_a_red"));
+    float* x1 = static_cast<float*>(A_("r_x1"));
+    auto* xn2_full = static_cast<__nv_bfloat16*>(A_("r_xn2_full"));
+    const size_t shard = static_cast<size_t>(Sl) * h;
+    const Bytes r0 = static_cast<Bytes>(swl);
+    // local suffix rows of the input norm, then the full gathered input
+    if (Rl > 0) G(rmsnorm_fwd(X + r0 * h, nullptr, P("g1"), XN + r0 * h, Rl, h, opt_.eps, cs_));
+    ag(comm_.get(), XN, xn_full, shard, cs_);
+    if (R > 0) {
+      GemmDesc g = gd(R, 3 * hl, h, xn_full + static_cast<Bytes>(sw) * h, h, 0, P("wqkv"), h, 0,
+                      GEMM_EPI_QKV_ROPE, nullptr, 0);
+      g.q = Q + static_cast<Bytes>(sw) * hl; g.k = K + static_cast<Bytes>(sw) * hl;
+      g.v = Vv + static_cast<Bytes>(sw) * hl;
+      g.hidden = hl; g.head_dim = D; g.rope = rope_; g.pos0 = sw;
+      gemm(g);
+    }
+    // attn_proj needs every rank's partial: redo the out-projection + RS exactly as forward
+    gemm(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, a_part, h));
+    rs(comm_.get(), a_part, a_red, shard, cs_);
+    if (Rl > 0) {
+      G(resid_round(X + r0 * h, a_red + r0 * h, A + r0 * h, x1 + r0 * h,
+                    static_cast<long long>(Rl) * h, cs_));
+      G(rmsnorm_fwd(x1 + r0 * h, nullptr, P("g2"), XN2 + r0 * h, Rl, h, opt_.eps, cs_));
+    }
+    ag(comm_.get(), XN2, xn2_full, shard, cs_);
+    if (R > 0) {
+      gemm(gd(R, 2 * Fl, h, xn2_full + static_cast<Bytes>(sw) * h, h, 0, P("wgu"), h, 0,
+              GEMM_EPI_BF16, GU + static_cast<Bytes>(sw) * 2 * Fl, 2 * Fl));
+      G(swiglu_fwd(GU + static_cast<Bytes>(sw) * 2 * Fl, ACT + static_cast<Bytes>(sw) * Fl, R, Fl, cs_));
+    }
+    stats_.kernel_launches += 5;
+  }
+  mark(0, static_cast<int>(Kind::Recompute), i, false);
+}
+
+void Executor::layer_bwd_tp(int i) {
+  const int S = d_.S, Sl = d_.Sl, h = d_.h, hl = d_.hl, Fl = d_.Fl, Hl = d_.Hl, D = d_.D;
+  if (swaps(i)) G(cudaStreamWaitEvent(cs_, ev_pre_done_[i], 0));  // B3
+  mark(0, static_cast<int>(Kind::LayerBwd), i, true);
+  const std::size_t seg = seg_bwd_[i];
+  auto P = [&](const char* n) { return params_ + ptab_.at({n, i}).first; };
+  auto Gr = [&](const char* n) { return grads_ + ptab_.at({n, i}).first; };
+  auto A_ = [&](const char* n) { return arena_ptr(seg, n); };
+  float* X = reinterpret_cast<float*>(comp(i, C_X));
+  auto* XN = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN));
+  auto* Q = reinterpret_cast<__nv_bfloat16*>(comp(i, C_Q));
+  auto* K = reinterpret_cast<__nv_bfloat16*>(comp(i, C_K));
+  auto* Vv = reinterpret_cast<__nv_bfloat16*>(comp(i, C_V));
+  auto* O = reinterpret_cast<__nv_bfloat16*>(comp(i, C_O));
+  float* LSE = reinterpret_cast<float*>(comp(i, C_O) + static_cast<Bytes>(S) * hl * 2);
+  auto* A = reinterpret_cast<__nv_bfloat16*>(comp(i, C_A));
+  auto* XN2 = reinterpret_cast<__nv_bfloat16*>(comp(i, C_XN2));
+  auto* GU = reinterpret_cast<__nv_bfloat16*>(comp(i, C_GU));
+  auto* ACT = reinterpret_cast<__nv_bfloat16*>(comp(i, C_ACT));
+  float* dxc = static_cast<float*>(arena_ptr(seg_emb_fwd_, "dx_carry"));
+  auto* dxb = static_cast<__nv_bfloat16*>(arena_ptr(seg_emb_fwd_, "dxb_carry"));
+  auto* dy_full = static_cast<__nv_bfloat16*>(A_("dy_full"));
+  auto* dact = static_cast<__nv_bfloat16*>(A_("dact"));
+  auto* dgu = static_cast<__nv_bfloat16*>(A_("dgu"));
+  float* dxn2_part = static_cast<float*>(A_("dxn2_part"));
+  float* dxn2 = static_cast<float*>(A_("dxn2"));
+  auto* xn2_full = static_cast<__nv_bfloat16*>(A_("b_xn2_full"));
+  auto* da = static_cast<__nv_bfloat16*>(A_("da"));
+  float* part2 = static_cast<float*>(A_("part2"));
+  auto* da_full = static_cast<__nv_bfloat16*>(A_("da_full"));
+  auto* dout = static_cast<__nv_bfloat16*>(A_("dout"));
+  float* ws = static_cast<float*>(A_("attn_ws"));
+  auto* dqkv = static_cast<__nv_bfloat16*>(A_("dqkv"));
+  float* dxn_part = static_cast<float*>(A_("dxn_part"));
+  float* dxn = static_cast<float*>(A_("dxn"));
+  auto* xn_full = static_cast<__nv_bfloat16*>(A_("b_xn_full"));
+  float* part1 = static_cast<float*>(A_("part1"));
+  const size_t shard = static_cast<size_t>(Sl) * h;
+
+  // MLP (down is row-parallel: its input gradient is the gathered output grad)
+  ag(comm_.get(), dxb, dy_full, shard, cs_);
+  gemm(gd(S, Fl, h, dy_full, h, 0, P("wd"), Fl, 1, GEMM_EPI_BF16, dact, Fl));
+  gemm(gd(h, Fl, S, dy_full, h, 1, ACT, Fl, 1, GEMM_EPI_F32, Gr("wd"), Fl));
+  G(swiglu_bwd(GU, dact, dgu, S, Fl, cs_));
+  gemm(gd(S, h, 2 * Fl, dgu, 2 * Fl, 0, P("wgu"), h, 1, GEMM_EPI_F32, dxn2_part, h));
+  rs(comm_.get(), dxn2_part, dxn2, shard, cs_);
+  ag(comm_.get(), XN2, xn2_full, shard, cs_);
+  gemm(gd(2 * Fl, h, S, dgu, 2 * Fl, 1, xn2_full, h, 1, GEMM_EPI_F32, Gr("wgu"), h));
+  G(rmsnorm_bwd(X, A, P("g2"), dxn2, dxc, dxc, da, part2, Gr("g2"), Sl, h, opt_.eps, false, cs_));
+  // attention output projection (row-parallel)
+  ag(comm_.get(), da, da_full, shard, cs_);
+  gemm(gd(S, hl, h, da_full, h, 0, P("wo"), hl, 1, GEMM_EPI_BF16, dout, hl));
+  gemm(gd(h, hl, S, da_full, h, 1, O, hl, 1, GEMM_EPI_F32, Gr("wo"), hl));
+  AttnBwdArgs ba;
+  ba.q = Q; ba.k = K; ba.v = Vv; ba.o = O; ba.lse = LSE; ba.dout = dout; ba.delta = ws;
+  ba.dq = dqkv; ba.dk = dqkv + hl; ba.dv = dqkv + 2 * hl; ba.ld_dqkv = 3 * hl;
+  ba.rope = rope_; ba.pos0 = 0; ba.S = S; ba.H = Hl; ba.D = D;
+  ba.softmax_scale = 1.0f / std::sqrt(static_cast<float>(D));
+  attention_bwd(ba);
+  // QKV projection (column-parallel)
+  gemm(gd(S, h, 3 * hl, dqkv, 3 * hl, 0, P("wqkv"), h, 1, GEMM_EPI_F32, dxn_part, h));
+  rs(comm_.get(), dxn_part, dxn, shard, cs_);
+  ag(comm_.get(), XN, xn_full, shard, cs_);
+  gemm(gd(3 * hl, h, S, dqkv, 3 * hl, 1, xn_full, h, 1, GEMM_EPI_F32, Gr("wqkv"), h));
+  G(rmsnorm_bwd(X, nullptr, P("g1"), dxn, dxc, dxc, dxb, part1, Gr("g1"), Sl, h, opt_.eps, false, cs_));
+  stats_.kernel_launches += 5;
+  mark(0, static_cast<int>(Kind::LayerBwd), i, false);
+  G(cudaEventRecord(ev_bwd_done_[i], cs_));
+  if (i >= 2 && swaps(i - 2)) prefetch(i - 2);  // B2
+}
+
+void Executor::classifier_tp() {
+  const int S = d_.S, Sl = d_.Sl, h = d_.h, Vl = d_.Vl;
+  const int T = std::min(opt_.ce_chunk, S);
+  float* xfin = static_cast<float*>(arena_ptr(seg_emb_fwd_, "x_final"));
+  auto* xf = static_cast<__nv_bfloat16*>(arena_ptr(seg_cls_fwd_, "xf"));
+  const __nv_bfloat16* gf = params_ + ptab_.at({"gf", -1}).first;
+  const __nv_bfloat16* W = params_ + ptab_.at({"wcls", -1}).first;
+  float* gW = grads_ + ptab_.at({"wcls", -1}).first;
+  mark(0, static_cast<int>(Kind::ClsFwd), -1, true);
+  G(rmsnorm_fwd(xfin, nullptr, gf, xf, Sl, h, opt_.eps, cs_));
+  mark(0, static_cast<int>(Kind::ClsFwd), -1, false);
+  mark(0, static_cast<int>(Kind::ClsBwd), -1, true);
+  const std::size_t sb = seg_cls_bwd_;
+  auto* xf_full = static_cast<__nv_bfloat16*>(arena_ptr(sb, "xf_full"));
+  float* dxf_part = static_cast<float*>(arena_ptr(sb, "dxf_part"));
+  float* loss_rows = static_cast<float*>(arena_ptr(sb, "loss_rows"));
+  float* logits = static_cast<float*>(arena_ptr(sb, "logits"));
+  auto* dlog = static_cast<__nv_bfloat16*>(arena_ptr(sb, "dlogits"));
+  float* stats = static_cast<float*>(arena_ptr(sb, "ce_stats"));  // [lmax | gmax | lsum,ltgt | gsum,gtgt]
+  const size_t shard = static_cast<size_t>(Sl) * h;
+  ag(comm_.get(), xf, xf_full, shard, cs_);
+  const float inv_n = 1.0f / static_cast<float>(n_labeled_);
+  const int v0 = d_.r * Vl;
+  for (int c0 = 0; c0 < S; c0 += T) {
+    const int t = std::min(T, S - c0);
+    const __nv_bfloat16* xc = xf_full + static_cast<Bytes>(c0) * h;
+    float* lmax = stats;
+    float* gmax = stats + T;
+    float* lst = stats + 2 * T;  // [sum | target] x T
+    float* gst = stats + 4 * T;
+    gemm(gd(t, Vl, h, xc, h, 0, W, h, 0, GEMM_EPI_F32, logits, Vl));
+    G(ce_vp_max(logits, lmax, t, Vl, cs_));
+    comm_->all_reduce(lmax, gmax, t, CommDtype::F32, CommOp::Max, cs_);
+    G(ce_vp_sum(logits, gmax, lab_ + c0, v0, lst, t, Vl, cs_));
+    // stats layout per chunk is [sum(t) | target(t)] contiguous at lst
+    comm_->all_reduce(lst, gst, 2 * static_cast<size_t>(t), CommDtype::F32, CommOp::Sum, cs_);
+    G(ce_vp_grad(logits, gmax, gst, lab_ + c0, v0, dlog, loss_rows + c0, t, Vl, inv_n, cs_));
+    gemm(gd(t, h, Vl, dlog, Vl, 0, W, h, 1, GEMM_EPI_F32, dxf_part + static_cast<Bytes>(c0) * h, h));
+    gemm(gd(Vl, h, t, dlog, Vl, 1, xc, h, 1, c0 == 0 ? GEMM_EPI_F32 : GEMM_EPI_F32_ACC, gW, h));
+    stats_.kernel_launches += 3;
+  }
+  G(sum_scaled(loss_rows, S, inv_n, loss_dev_, cs_));
+  float* dxf = static_cast<float*>(arena_ptr(sb, "dxf"));
+  rs(comm_.get(), dxf_part, dxf, shard, cs_);
+  float* dxc = static_cast<float*>(arena_ptr(seg_emb_fwd_, "dx_carry"));
+  auto* dxb = static_cast<__nv_bfloat16*>(arena_ptr(seg_emb_fwd_, "dxb_carry"));
+  float* part = static_cast<float*>(arena_ptr(sb, "cls_part"));
+  G(rmsnorm_bwd(xfin, nullptr, gf, dxf, nullptr, dxc, dxb, part, grads_ + ptab_.at({"gf", -1}).first,
+                Sl, h, opt_.eps, false, cs_));
+  stats_.kernel_launches += 4;
+  mark(0, static_cast<int>(Kind::ClsBwd), -1, false);
+}
+
+// Replicated parameters (embedding, norm weights) accumulate gradients from
+// every rank's token shard: sum them so all replicas step identically.
+void Executor::sync_replicated_grads() {
+  float* tmp = static_cast<float*>(arena_ptr(seg_emb_bwd_, "ar_tmp"));
+  auto sum = [&](const char* n, int layer) {
+    const auto [off, cnt] = ptab_.at({n, layer});
+    comm_->all_reduce(grads_ + off, tmp, static_cast<size_t>(cnt), CommDtype::F32, CommOp::Sum, cs_);
+    G(cudaMemcpyAsync(grads_ + off, tmp, static_cast<size_t>(cnt) * 4, cudaMemcpyDeviceToDevice, cs_));
+  };
+  sum("embedding", -1);
+  for (int l = 0; l < d_.n; ++l) {
+    sum("g1", l);
+    sum("g2", l);
+  }
+  sum("gf", -1);
+}
+
 void Executor::step_resident() {
   const int n = d_.n;
   marks_.clear();
@@ -755,18 +1194,20 @@ void Executor::step_resident() {
   G(cudaStreamWaitEvent(os_, ev_start_, 0));
   G(cudaStreamWaitEvent(ps_, ev_start_, 0));
   mark(0, static_cast<int>(Kind::EmbFwd), -1, true);
-  G(embed_fwd(tok_, params_ + ptab_.at({"embedding", -1}).first,
-              reinterpret_cast<float*>(comp(0, C_X)), d_.S, d_.h, cs_));
+  G(embed_fwd(tok_ + d_.r * d_.Sl, params_ + ptab_.at({"embedding", -1}).first,
+              reinterpret_cast<float*>(comp(0, C_X)), d_.Sl, d_.h, cs_));
   mark(0, static_cast<int>(Kind::EmbFwd), -1, false);
-  for (int i = 0; i < n; ++i) layer_fwd(i);
-  classifier();
+  const bool tp = d_.t > 1;
+  for (int i = 0; i < n; ++i) tp ? layer_fwd_tp(i) : layer_fwd(i);
+  tp ? classifier_tp() : classifier();
   for (int i = n - 1; i >= 0; --i) {
-    if (swaps(i)) layer_recompute(i);
-    layer_bwd(i);
+    if (swaps(i)) tp ? layer_recompute_tp(i) : layer_recompute(i);
+    tp ? layer_bwd_tp(i) : layer_bwd(i);
   }
   mark(0, static_cast<int>(Kind::EmbBwd), -1, true);
   G(embed_bwd(csr_off_, csr_pos_, static_cast<float*>(arena_ptr(seg_emb_fwd_, "dx_carry")),
               grads_ + ptab_.at({"embedding", -1}).first, d_.V, d_.h, cs_));
+  if (tp) sync_replicated_grads();
   mark(0, static_cast<int>(Kind::EmbBwd), -1, false);
   stats_.kernel_launches += 2;
   if (opt_.optimizer) {

@@ -18,8 +18,11 @@
 #include "host/planner.hpp"
 #include "kernels/attention.h"
 #include "kernels/gemm_tc.h"
+#include "runtime/comm.h"
 
 namespace memo {
+
+class TraceBuilder;
 
 struct ExecOptions {
   uint64_t seed = 1234;
@@ -40,8 +43,14 @@ struct ExecOptions {
 
 // Llama dimensions derived from the reference ModelConfig: intermediate size
 // f = 2/3 * ffn_hidden (SwiGLU mapping, SURVEY discovery 5), D = h / n_heads.
+// With tensor/sequence parallelism over t ranks (Megatron SP+TP, reference
+// mapping tp_degree = t, sp_or_cp_degree = 1; SURVEY discovery 4) rank r owns
+// tokens [r*Sl, (r+1)*Sl) of the norm/residual regions, heads [r*Hl, ...),
+// SwiGLU columns [r*Fl, ...) and vocabulary rows [r*Vl, ...).
 struct Dims {
   int S, h, H, D, F, V, n;
+  int t = 1, r = 0;           // tensor-parallel size / rank
+  int Sl, hl, Hl, Fl, Vl;     // local extents
 };
 
 // Per-kernel-class device time of the last step (CUDA events on the compute
@@ -60,7 +69,8 @@ struct StepStats {
 
 class Executor {
  public:
-  Executor(const ModelConfig& cfg, const HardwareConfig& hw, const ExecOptions& opt);
+  Executor(const ModelConfig& cfg, const HardwareConfig& hw, const ExecOptions& opt,
+           std::unique_ptr<Comm> comm = nullptr);
   ~Executor();
   Executor(const Executor&) = delete;
   Executor& operator=(const Executor&) = delete;
@@ -101,6 +111,7 @@ class Executor {
     Bytes bytes = 0;
   };
   void build_trace_and_plan();
+  void build_trace_tp(TraceBuilder& tb);
   void compute_layout();
   void allocate();
   void init_weights();
@@ -112,6 +123,12 @@ class Executor {
   void layer_recompute(int i);
   void layer_bwd(int i);
   void classifier();
+  void layer_fwd_tp(int i);
+  void layer_recompute_tp(int i);
+  void layer_bwd_tp(int i);
+  void classifier_tp();
+  void sync_replicated_grads();
+  const TokenRange& split_of(int c) const;
   void offload(int i);
   void prefetch(int i);
   void mark(int stream, int kind, int layer, bool begin);
@@ -131,8 +148,10 @@ class Executor {
   Dims d_{};
   Skeletal sk_;
   SwapDecision swap_;
-  TokenRange split_;
+  TokenRange split_;    // hidden/head-sharded components: token_split(alpha, S)
+  TokenRange split_l_;  // sequence-sharded components: token_split(alpha, S/t)
   bool can_swap_ = true, swap_on_ = true;
+  std::unique_ptr<Comm> comm_;
 
   std::string trace_text_, plan_json_;
   std::map<std::pair<std::size_t, std::string>, Bytes> arena_off_;

@@ -40,6 +40,9 @@ class ExecInfoC(C.Structure):
         ("op_ms", C.c_double * 5), ("op_flops", C.c_double * 5), ("op_count", C.c_int32 * 5)]
 
 
+lib.memo_comm_loopback_group.restype = C.c_void_p
+lib.memo_comm_loopback_group.argtypes = [C.c_int32]
+lib.memo_comm_loopback_group_destroy.argtypes = [C.c_void_p]
 lib.memo_exec_stream.restype = C.c_void_p
 lib.memo_exec_stream.argtypes = [C.c_void_p]
 lib.memo_exec_destroy.argtypes = [C.c_void_p]
@@ -54,7 +57,9 @@ def default_options() -> ExecOptionsC:
 class Executor:
     """One B200 training-step context (arena, rounding buffers, copy streams)."""
 
-    def __init__(self, cfg: ModelConfig, hw: HardwareConfig, **options):
+    def __init__(self, cfg: ModelConfig, hw: HardwareConfig, tp=None, **options):
+        """tp: None (single GPU) or (kind, handle, rank) with kind 0 = LoopbackGroup,
+        kind 1 = 128-byte NCCL unique id; cfg.tp_degree is the group size."""
         o = default_options()
         for k, v in options.items():
             if not hasattr(o, k):
@@ -62,8 +67,14 @@ class Executor:
             setattr(o, k, v)
         self._h = C.c_void_p()
         self.cfg = cfg
-        check(lib.memo_exec_create(C.byref(cfg.to_c()), C.byref(hw.to_c()), C.byref(o),
-                                   C.byref(self._h)))
+        if tp is None:
+            check(lib.memo_exec_create(C.byref(cfg.to_c()), C.byref(hw.to_c()), C.byref(o),
+                                       C.byref(self._h)))
+        else:
+            kind, handle, rank = tp
+            h = handle.ptr if isinstance(handle, LoopbackGroup) else C.c_char_p(bytes(handle))
+            check(lib.memo_exec_create_tp(C.byref(cfg.to_c()), C.byref(hw.to_c()), C.byref(o),
+                                          kind, h, rank, C.byref(self._h)))
 
     def close(self):
         if self._h:
@@ -164,3 +175,45 @@ class Executor:
         check(lib.memo_exec_read(self._h, name.encode(), layer, out.ctypes.data_as(C.c_void_p),
                                  C.c_size_t(nbytes)))
         return out
+
+
+class LoopbackGroup:
+    """t tensor-parallel ranks sharing one GPU (one host thread per rank)."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self.ptr = C.c_void_p(lib.memo_comm_loopback_group(size))
+        if not self.ptr:
+            raise RuntimeError("could not create loopback group")
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib.memo_comm_loopback_group_destroy(self.ptr)
+            self.ptr = None
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib.memo_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def run_ranks(size: int, fn):
+    """Run fn(rank) on `size` threads (loopback SP+TP); returns results by rank."""
+    import threading
+    out, err = [None] * size, [None] * size
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+    th = [threading.Thread(target=body, args=(r,)) for r in range(size)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out

@@ -74,12 +74,30 @@ def test_executor_rejects_bad_configs():
     with pytest.raises(MemoError) as ei:
         Executor(bad, HW, dry_run=1)
     assert ei.value.code == 2
-    tp = llama(4, 256, 4, 768, 512, 512)
-    tp.tp_degree = 2
+    cp = llama(4, 256, 4, 768, 512, 512)
+    cp.sp_or_cp_degree = 2  # SP+TP is tp_degree = t, sp_or_cp_degree = 1
     with pytest.raises(MemoError):
-        Executor(tp, HW, dry_run=1)
+        Executor(cp, HW, dry_run=1)
     # host memory too small for the mandatory offload -> CpuInfeasible (4)
     tiny = P.HardwareConfig(pcie_bandwidth=50e9, cpu_mem=1024, gpu_mem=1 << 40, peak_flops=2.25e15)
     with pytest.raises(MemoError) as ei:
         Executor(CONFIGS["cfg1p"][0], tiny, dry_run=1)
     assert ei.value.code == 4
+
+
+@pytest.mark.parametrize("t", [2, 4, 8])
+def test_tp_rank_plan_bit_exact_and_sized(t):
+    """Per-rank SP+TP plan (cfg3 shape scaled down in S): bit-exact with the
+    reference planner; skeletal bytes equal the reference model at tp_degree=t."""
+    cfg = llama(4, 4096, 32, 11008, 32000, 131072)
+    cfg.tp_degree = t
+    ex = Executor(cfg, HW, alpha=0.5, dry_run=1)
+    trace, plan, info = ex.trace_text(), ex.plan_json(), ex.info()
+    assert P.plan_model_json(trace, 0, 60.0, 512) == plan
+    if os.path.exists(PROBE):
+        assert _ref_plan(trace) == plan
+    sz = P.skeletal_sizes(P.ModelConfig(**{**cfg.__dict__, "skeletal_weights": {}}))
+    # same weights, per-device bytes shrink by t except the fixed LSE share
+    assert info["rb_bytes"] * t == pytest.approx(
+        sum(info["skeletal_components"]) * t, rel=0)
+    assert info["split"][0] + info["split"][1] == cfg.seq_len
