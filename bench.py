@@ -8,8 +8,11 @@ one B200, alpha tuned by the planner (solve_alpha with the MEASURED host-link
 bandwidth and MEASURED forward-layer time).  A step = embedding -> 4 layers fwd
 (offload of the swapped layers' activations) -> classifier + CE -> 4 layers bwd
 (prefetch + suffix recompute) -> embedding grad -> AdamW.  Synthetic tokens,
-random-init weights (counter hash).  N>1 under torchrun: every rank runs an
-independent replica (weak scaling, "replicas only" this round — see DESIGN.md).
+random-init weights (counter hash).  N>1 under torchrun: Megatron SP+TP of the
+same cfg2 sequence across the N GPUs over NCCL (tp_degree = N; strong scaling:
+`value` = tokens of the one sequence / step time, max over ranks); if the NCCL
+communicator cannot start, every rank runs an independent replica instead
+(weak scaling) and `config.parallelism` says which ran.
 
 Prints ONE JSON line (rank 0).  `value` is device-resident tokens/s over all
 ranks; `e2e` is the same metric through the C-ABI step with host token buffers
@@ -228,6 +231,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
+                    help="N>1: Megatron SP+TP over NCCL (strong scaling of one sequence) or "
+                         "independent replicas (weak scaling)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -245,13 +251,26 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_12117_b200 import planner as P
     from paper_2407_12117_b200.executor import Executor
 
     n, h, H, inter, V, S, desc = CONFIGS[args.config]
+    mode = "single" if world == 1 else args.parallel
+    tp_spec = None
+    if mode == "tp":
+        # one NCCL communicator for the SP+TP group; fall back to replicas if it cannot start
+        from paper_2407_12117_b200.executor import nccl_unique_id
+        try:
+            uid = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            tp_spec = (1, uid[0], rank)
+        except Exception as ex:  # noqa: BLE001
+            print(f"[bench] SP+TP unavailable ({ex}); running replicas", file=sys.stderr)
+            mode = "replicas"
     cfg = P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
-                        batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True)
+                        batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True,
+                        tp_degree=world if mode == "tp" else 1)
     link = host_link_bandwidth(torch)
     host_mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
     gpus_on_node = max(torch.cuda.device_count(), world)
@@ -259,19 +278,23 @@ def main():
     hw = P.HardwareConfig(pcie_bandwidth=link["d2h"], cpu_mem=cpu_mem,
                           gpu_mem=torch.cuda.get_device_properties(local).total_memory,
                           peak_flops=B200_SPEC_BF16, efficiency=0.5)
-    toks, labels = synthetic_batch(1234 + rank, V, S)
+    toks, labels = synthetic_batch(1234 + (rank if mode == "replicas" else 0), V, S)
     forced_alpha = 0.5 if args.config == "cfg1p" else -1.0
 
     # Calibrate: one step with the analytic layer time, then re-solve alpha with
     # the measured forward-layer time (swap.hpp:105 with SwapOptions.t_layer).
-    with Executor(cfg, hw, alpha=forced_alpha, op_timing=0) as ex:
+    with Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, op_timing=0) as ex:
         ex.step(toks, labels)
         tl = ex.timeline()
     t_fwd = [e.end - e.start for e in tl if e.kind == "layer_fwd"]
     t_layer = float(np.median(t_fwd))
+    if dist:  # SPMD: every rank solves alpha from the same (slowest) layer time
+        tt = torch.tensor([t_layer], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_layer = tt.item()
     torch.cuda.synchronize()
     free0, _ = torch.cuda.mem_get_info()
-    ex = Executor(cfg, hw, alpha=forced_alpha, t_layer=t_layer, op_timing=1)
+    ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, t_layer=t_layer, op_timing=1)
     free1, _ = torch.cuda.mem_get_info()
     info0 = ex.info()
     stream = torch.cuda.ExternalStream(ex.stream)
@@ -300,7 +323,8 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = t.item()
-    value = world * S / (t_max * 1e-3)
+    seqs = world if mode == "replicas" else 1  # sequences processed by the job per step
+    value = seqs * S / (t_max * 1e-3)
 
     # ---- end to end through the C ABI with host buffers
     e2e_ms = []
@@ -323,7 +347,7 @@ def main():
     p_total = P.count_params(cfg)["total"]
     sim = P.simulate(tl, cfg, hw, p_total)
     flops = P.estimate_flops_per_sample(cfg, p_total)
-    mfu = flops / (ms * 1e-3) / B200_SPEC_BF16
+    mfu = seqs * flops / (t_max * 1e-3) / (world * B200_SPEC_BF16)
     burst, sustained, hbm, peak_src = measured_peaks()
     off = [e for e in tl if e.kind == "offload"]
     pre = [e for e in tl if e.kind == "prefetch"]
@@ -344,18 +368,20 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong" if mode == "tp" else "weak",
+        "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (splitmix64 tokens, counter-hash random-init weights)",
         "config": {"workload": desc, "model": "llama-7b-arch", "n_layers": n, "global_batch": world,
-                   "seq_len": S, "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "seq_len": S, "parallelism": {"single": "single", "tp": f"sp+tp{world}",
+                                                 "replicas": f"replicas{world}"}[mode],
                    "l2": "working set (GB of activations) >> 126 MB L2; no flush needed",
                    "alpha": swap.alpha, "swap_tokens": info0["split"][0],
                    "recompute_tokens": info0["split"][1], "t_layer_measured_s": t_layer,
                    "host_link_d2h_GBps": link["d2h"] / 1e9, "host_link_h2d_GBps": link["h2d"] / 1e9,
                    "cpu_mem_budget": cpu_mem},
         "tokens_per_s_per_gpu": value / world,
-        "mfu": mfu, "mfu_vs_measured_peak": flops / (ms * 1e-3) / (burst * 1e12),
-        "e2e": {"value": world * S / (e2e * 1e-3), "unit": "tokens/s",
+        "mfu": mfu, "mfu_vs_measured_peak": mfu * B200_SPEC_BF16 / (burst * 1e12),
+        "e2e": {"value": seqs * S / (e2e * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(info["h2d_bytes"]), "d2h_bytes_per_step": int(info["d2h_bytes"])},
         "roofline": {"kernel": "attn_bwd_dkdv (causal FlashAttention dK/dV, tcgen05)",
                      "bound": "tensor", "achieved": achieved, "peak": sustained,
