@@ -48,14 +48,25 @@ constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 
-__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
-  // K-major tile split in 64-col chunks of 16 KiB; k-step of 16 elements.
-  return dev::umma_desc_sw128(base + (kk >> 2) * CHUNK_BYTES + (kk & 3) * 32, 16, 1024);
+// Descriptors are built once per tile base; the k-steps only move the start
+// address (bits [0,14) in 16-byte units), so each MMA issue is one 64-bit add
+// of a compile-time constant.  (The single issuing thread is otherwise the
+// bottleneck for the N=64 halves, whose MMAs take only 32 cycles.)
+__device__ __forceinline__ uint64_t kmajor_base(uint32_t base) {
+  return dev::umma_desc_sw128(base, 16, 1024);
 }
-__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
-  // MN-major tile: 128 K-rows of 128 B per 64-wide MN chunk; k-step of 16 rows.
-  return dev::umma_desc_sw128(base + kk * 2048, CHUNK_BYTES, 1024);
+__device__ __forceinline__ uint64_t mnmajor_base(uint32_t base) {
+  return dev::umma_desc_sw128(base, CHUNK_BYTES, 1024);
 }
+// K-major tile split in 64-col chunks of 16 KiB; k-step of 16 elements.
+__device__ __forceinline__ uint64_t kmajor_step(uint64_t d, int kk) {
+  return d + static_cast<uint64_t>(((kk >> 2) * CHUNK_BYTES + (kk & 3) * 32) >> 4);
+}
+// MN-major tile: 128 K-rows of 128 B per 64-wide MN chunk; k-step of 16 rows.
+__device__ __forceinline__ uint64_t mnmajor_step(uint64_t d, int kk) {
+  return d + static_cast<uint64_t>((kk * 2048) >> 4);
+}
+
 
 // 2^x for x <= 0 on the FMA pipe: cubic on the fraction + exponent insert.
 // Max relative error 1.0e-4 (bf16 P needs 3.9e-3).
@@ -192,14 +203,14 @@ __global__ void __launch_bounds__(256, 1)
         const int st = j % NS;
         dev::mbar_wait(&k_full[st], (j / NS) & 1);
         dev::tc_fence_after();
-        const uint32_t sk = dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES);
+        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
+        const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::Q_OFF));
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           if (QT)
-            dev::mma_bf16_ts(t_s[j & 1], t_q + kk * 8, kmajor_desc(sk, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ts(t_s[j & 1], t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
           else
-            dev::mma_bf16_ss(t_s[j & 1], kmajor_desc(dev::smem_u32(smem + L::Q_OFF), kk),
-                             kmajor_desc(sk, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ss(t_s[j & 1], kmajor_step(qd, kk), kmajor_step(kd, kk), idesc_s, kk > 0);
         }
         dev::mma_commit(&s_full[j & 1]);
         dev::mma_commit(&k_empty[st]);
@@ -211,10 +222,10 @@ __global__ void __launch_bounds__(256, 1)
         dev::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         dev::mbar_wait(&v_full[st], (j / NS) & 1);
         dev::tc_fence_after();
-        const uint32_t sv = dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES);
+        const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts(t_o, t_s[j & 1] + kk * 8, mnmajor_desc(sv, kk), idesc_o, (j | kk) != 0);
+          dev::mma_bf16_ts(t_o, t_s[j & 1] + kk * 8, mnmajor_step(vd, kk), idesc_o, (j | kk) != 0);
         dev::mma_commit(o_done);
         dev::mma_commit(&v_empty[st]);
       }
@@ -242,16 +253,27 @@ __global__ void __launch_bounds__(256, 1)
         dev::tmem_ld32(t_s[st] + lane_off + c * 32, r);
         dev::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * scale_log2;
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);  // raw logits
       }
       if (j == qt) {  // diagonal tile: causal mask
 #pragma unroll
         for (int i = 0; i < 128; ++i)
           if (i > row) s[i] = -INFINITY;
       }
-      float mx = s[0];
+      // One warp per SMSP: reduce with 8 independent chains, not one
+      // 127-deep dependent FMNMX chain.
+      float mx8[8];
 #pragma unroll
-      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      for (int k = 0; k < 8; ++k) mx8[k] = s[k];
+#pragma unroll
+      for (int i = 8; i < 128; i += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], s[i + k]);
+#pragma unroll
+      for (int k = 4; k > 0; k >>= 1)
+#pragma unroll
+        for (int q2 = 0; q2 < k; ++q2) mx8[q2] = fmaxf(mx8[q2], mx8[q2 + k]);
+      const float mx = mx8[0] * scale_log2;  // scale > 0 commutes with max
       const float cand = fmaxf(m, mx);
       const bool need = j == 0 || cand > m + kRescaleThreshold;
       const bool any = __any_sync(0xffffffffu, need);
@@ -261,22 +283,26 @@ __global__ void __launch_bounds__(256, 1)
         m_new = cand;
         factor = j == 0 ? 0.f : dev::ex2(m - m_new);
       }
-      float sum = 0.f;
+      float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint32_t p[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
         float a, b;
         if (EMU && (i & 3) == 3) {  // a quarter of the exponentials on the FMA pipe
-          a = exp2_fma(s[2 * i] - m_new);
-          b = exp2_fma(s[2 * i + 1] - m_new);
+          a = exp2_fma(fmaf(s[2 * i], scale_log2, -m_new));
+          b = exp2_fma(fmaf(s[2 * i + 1], scale_log2, -m_new));
         } else {
-          a = dev::ex2(s[2 * i] - m_new);
-          b = dev::ex2(s[2 * i + 1] - m_new);
+          a = dev::ex2(fmaf(s[2 * i], scale_log2, -m_new));
+          b = dev::ex2(fmaf(s[2 * i + 1], scale_log2, -m_new));
         }
-        sum += a + b;
+        sum8[i & 7] += a + b;
         p[i] = dev::pack_bf16(a, b);
       }
-      l = l * factor + sum;
+#pragma unroll
+      for (int k = 4; k > 0; k >>= 1)
+#pragma unroll
+        for (int q2 = 0; q2 < k; ++q2) sum8[q2] += sum8[q2 + k];
+      l = l * factor + sum8[0];
       m = m_new;
       {
         uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&p[0]);
@@ -482,8 +508,8 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, HALF, false, false);
       constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
-      const uint32_t sk = dev::smem_u32(smem + L::A0_OFF);
-      const uint32_t sv = dev::smem_u32(smem + L::A1_OFF);
+      const uint64_t kd0 = kmajor_base(dev::smem_u32(smem + L::A0_OFF));
+      const uint64_t vd0 = kmajor_base(dev::smem_u32(smem + L::A1_OFF));
       dev::mbar_wait(kv_full, 0);
       auto issue_sd = [&](int g) {
         const int i = g >> 1, half = g & 1, st = i & 1, b = g & 1;
@@ -491,14 +517,14 @@ __global__ void __launch_bounds__(256, 1)
           dev::mbar_wait(&in_full[st], (i >> 1) & 1);
           dev::tc_fence_after();
         }
-        const uint32_t sq = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
-        const uint32_t sdo = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
+        const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
+        const uint64_t dod = kmajor_base(dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(tmem + b * 128, kmajor_desc(sk, kk), kmajor_desc(sq, kk), idesc_s, kk > 0);
+          dev::mma_bf16_ss(tmem + b * 128, kmajor_step(kd0, kk), kmajor_step(qd, kk), idesc_s, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_desc(sv, kk), kmajor_desc(sdo, kk), idesc_s,
+          dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_step(vd0, kk), kmajor_step(dod, kk), idesc_s,
                            kk > 0);
         dev::mma_commit(&s_full[b]);
       };
@@ -508,15 +534,15 @@ __global__ void __launch_bounds__(256, 1)
         const int i = g >> 1, half = g & 1, st = i & 1, b = g & 1;
         dev::mbar_wait(&p_ready[b], (g >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t sq = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
-        const uint32_t sdo = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
+        const uint64_t qm = mnmajor_base(dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
+        const uint64_t dom = mnmajor_base(dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
 #pragma unroll
         for (int kk = 0; kk < HALF / 16; ++kk)
-          dev::mma_bf16_ts(t_dv, tmem + b * 128 + kk * 8, mnmajor_desc(sdo, kk), idesc_g,
+          dev::mma_bf16_ts(t_dv, tmem + b * 128 + kk * 8, mnmajor_step(dom, kk), idesc_g,
                            (g | kk) != 0);
 #pragma unroll
         for (int kk = 0; kk < HALF / 16; ++kk)
-          dev::mma_bf16_ts(t_dk, tmem + b * 128 + 64 + kk * 8, mnmajor_desc(sq, kk), idesc_g,
+          dev::mma_bf16_ts(t_dk, tmem + b * 128 + 64 + kk * 8, mnmajor_step(qm, kk), idesc_g,
                            (g | kk) != 0);
         if (half == 1) dev::mma_commit(&in_empty[st]);
       }
@@ -687,28 +713,29 @@ __global__ void __launch_bounds__(256, 1)
       constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, HALF, false, false);
       constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
       dev::mbar_wait(qd_ready, 0);
+      const uint64_t qa0 = kmajor_base(dev::smem_u32(smem + L::A0_OFF));
+      const uint64_t doa0 = kmajor_base(dev::smem_u32(smem + L::A1_OFF));
       auto issue_s = [&](int g) {
         const int j = g >> 1, half = g & 1, st = j & 1, b = g & 1;
         if (half == 0) {
           dev::mbar_wait(&kv_full[st], (j >> 1) & 1);
           dev::tc_fence_after();
         }
-        const uint32_t sk = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
-        const uint32_t sv = dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
-        const uint32_t sqa = dev::smem_u32(smem + L::A0_OFF), sdoa = dev::smem_u32(smem + L::A1_OFF);
+        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
+        const uint64_t vd = kmajor_base(dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           if (AT)
-            dev::mma_bf16_ts(tmem + b * 128, t_q + kk * 8, kmajor_desc(sk, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ts(tmem + b * 128, t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
           else
-            dev::mma_bf16_ss(tmem + b * 128, kmajor_desc(sqa, kk), kmajor_desc(sk, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ss(tmem + b * 128, kmajor_step(qa0, kk), kmajor_step(kd, kk), idesc_s, kk > 0);
         }
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           if (AT)
-            dev::mma_bf16_ts(tmem + b * 128 + 64, t_do + kk * 8, kmajor_desc(sv, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ts(tmem + b * 128 + 64, t_do + kk * 8, kmajor_step(vd, kk), idesc_s, kk > 0);
           else
-            dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_desc(sdoa, kk), kmajor_desc(sv, kk), idesc_s,
+            dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_step(doa0, kk), kmajor_step(vd, kk), idesc_s,
                              kk > 0);
         }
         dev::mma_commit(&s_full[b]);
@@ -719,10 +746,10 @@ __global__ void __launch_bounds__(256, 1)
         const int j = g >> 1, half = g & 1, st = j & 1, b = g & 1;
         dev::mbar_wait(&ds_ready[b], (g >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t sk = dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES;
+        const uint64_t km = mnmajor_base(dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
 #pragma unroll
         for (int kk = 0; kk < HALF / 16; ++kk)
-          dev::mma_bf16_ts(t_dq, tmem + b * 128 + kk * 8, mnmajor_desc(sk, kk), idesc_g,
+          dev::mma_bf16_ts(t_dq, tmem + b * 128 + kk * 8, mnmajor_step(km, kk), idesc_g,
                            (g | kk) != 0);
         if (half == 1) dev::mma_commit(&kv_empty[st]);
       }

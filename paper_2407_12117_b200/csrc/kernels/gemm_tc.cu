@@ -248,12 +248,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           dev::tc_fence_after();
           const uint32_t sa = dev::smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_TILE_BYTES;
+          const uint64_t ad0 = A_MN ? dev::umma_desc_sw128(sa, 8192, 1024) : dev::umma_desc_sw128(sa, 16, 1024);
+          const uint64_t bd0 = B_MN ? dev::umma_desc_sw128(sb, 8192, 1024) : dev::umma_desc_sw128(sb, 16, 1024);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = A_MN ? dev::umma_desc_sw128(sa + k * 2048, 8192, 1024)
-                                     : dev::umma_desc_sw128(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? dev::umma_desc_sw128(sb + k * 2048, 8192, 1024)
-                                     : dev::umma_desc_sw128(sb + k * 32, 16, 1024);
+            // only the start-address field moves with k (16-byte units)
+            const uint64_t ad = ad0 + static_cast<uint64_t>((A_MN ? k * 2048 : k * 32) >> 4);
+            const uint64_t bd = bd0 + static_cast<uint64_t>((B_MN ? k * 2048 : k * 32) >> 4);
             dev::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
           dev::mma_commit(&empty_bar[stage]);
