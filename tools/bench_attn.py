@@ -86,6 +86,14 @@ if __name__ == "__main__":
             out = subprocess.check_output([sys.executable, __file__, sys.argv[-1]], env=env, text=True)
             r = json.loads(out.strip().splitlines()[0])
             print(json.dumps({"variant": v, "S": r["S"], "fwd_tflops": r["fwd_tflops"]}), flush=True)
+    if os.environ.get("MEMO_DBG_SWEEP"):
+        import subprocess
+        for v in [0, 1, 2, 4, 3, 5, 6, 7]:
+            env = dict(os.environ, MEMO_ATTN_DEBUG=str(v))
+            env.pop("MEMO_DBG_SWEEP")
+            out = subprocess.check_output([sys.executable, __file__, sys.argv[-1]], env=env, text=True)
+            r = json.loads(out.strip().splitlines()[0])
+            print(json.dumps({"dbg": v, "S": r["S"], "dq_ms": r["dq_ms"], "dkdv_ms": r["dkdv_ms"]}), flush=True)
     if os.environ.get("MEMO_DQ_SWEEP"):
         import subprocess
         for v in range(2):
