@@ -323,6 +323,7 @@ Json goldens_schedule() {
                      {"swap", to_json(swap)}, {"params", p},
                      {"events", events_json(sched)},
                      {"violations", validate_schedule(sched, swap)},
+                     {"timeline_csv", schedule_timeline_csv(sched)},
                      {"sim", to_json(simulate(sched, cfg, hw, p))}});
   }
   return cases;

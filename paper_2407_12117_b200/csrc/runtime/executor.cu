@@ -398,7 +398,8 @@ void Executor::compute_layout() {
   n_params_ = off;
   const Bytes Pn = static_cast<Bytes>(n_params_);
   const Bytes sz_params = up(Pn * 2), sz_f32 = up(Pn * 4);
-  state_bytes_ = sz_params + 4 * sz_f32;
+  // optimizer off: no f32 master / Adam moments (bf16 params + f32 grads only)
+  state_bytes_ = sz_params + (opt_.optimizer ? 4 : 1) * sz_f32;
   const Bytes S = d_.S;
   const Bytes misc = up(S * (d_.D / 2) * 8 + S * 4 * 3 + (V + 1) * 4 + 1024);
   const int n_rb = swap_on_ ? 2 : d_.n;
@@ -431,9 +432,11 @@ void Executor::allocate() {
   dev_ = static_cast<char*>(p);
   char* q = dev_;
   params_ = reinterpret_cast<__nv_bfloat16*>(q); q += sz_params;
-  master_ = reinterpret_cast<float*>(q); q += sz_f32;
-  adam_m_ = reinterpret_cast<float*>(q); q += sz_f32;
-  adam_v_ = reinterpret_cast<float*>(q); q += sz_f32;
+  if (opt_.optimizer) {
+    master_ = reinterpret_cast<float*>(q); q += sz_f32;
+    adam_m_ = reinterpret_cast<float*>(q); q += sz_f32;
+    adam_v_ = reinterpret_cast<float*>(q); q += sz_f32;
+  }
   grads_ = reinterpret_cast<float*>(q); q += sz_f32;
   rb_base_.assign(n_rb, nullptr);
   for (int r = 0; r < n_rb; ++r) {
@@ -504,7 +507,7 @@ void Executor::init_weights() {
     const bool is_norm = name == "g1" || name == "g2" || name == "gf";
     const long long h = d_.h, hl = d_.hl, Fl = d_.Fl, Vl = d_.Vl, r = d_.r;
     if (d_.t == 1 || name == "embedding" || is_norm) {
-      ck(init_uniform(params_ + o, master_ + o, n, opt_.seed, tid, is_norm, cs_), "init_uniform");
+      ck(init_uniform(params_ + o, master_ ? master_ + o : nullptr, n, opt_.seed, tid, is_norm, cs_), "init_uniform");
       continue;
     }
     // shard of the full tensor: same counter-hash values as the unsharded init
@@ -524,11 +527,13 @@ void Executor::init_weights() {
     } else {  // wcls
       R = Vl; Cl = h; Cg = h; cnt[0] = Vl; g0[0] = r * Vl;
     }
-    ck(init_sliced(params_ + o, master_ + o, R, Cl, l0, cnt, g0, nseg, Cg, coff, opt_.seed, tid,
+    ck(init_sliced(params_ + o, master_ ? master_ + o : nullptr, R, Cl, l0, cnt, g0, nseg, Cg, coff, opt_.seed, tid,
                    false, cs_), "init_sliced");
   }
-  ck(cudaMemsetAsync(adam_m_, 0, n_params_ * 4, cs_), "memset");
-  ck(cudaMemsetAsync(adam_v_, 0, n_params_ * 4, cs_), "memset");
+  if (opt_.optimizer) {
+    ck(cudaMemsetAsync(adam_m_, 0, n_params_ * 4, cs_), "memset");
+    ck(cudaMemsetAsync(adam_v_, 0, n_params_ * 4, cs_), "memset");
+  }
   ck(cudaStreamSynchronize(cs_), "init sync");
 }
 
@@ -622,6 +627,7 @@ bool Executor::tensor(const std::string& name, int layer, void** ptr, size_t* by
     arr = reinterpret_cast<char*>(grads_);
     esz = 4;
   } else if (name.rfind("master/", 0) == 0) {
+    if (!master_) return false;
     base = name.substr(7);
     arr = reinterpret_cast<char*>(master_);
     esz = 4;

@@ -256,6 +256,14 @@ def simulate(events: List[ScheduleEvent], cfg: ModelConfig, hw: HardwareConfig, 
     return {f: getattr(out, f) for f, _ in SimReportC._fields_}
 
 
+def schedule_timeline_csv(events: List[ScheduleEvent]) -> str:
+    """json_io.hpp:246-254: `stream,kind,layer,start,end` with 17 significant digits."""
+    out = ["stream,kind,layer,start,end"]
+    for e in events:
+        out.append(f"{e.stream},{e.kind},{e.layer},{e.start:.17g},{e.end:.17g}")
+    return "\n".join(out) + "\n"
+
+
 def fnv1a_hex(data: str) -> str:
     b = data.encode()
     out = C.create_string_buffer(19)
@@ -288,4 +296,5 @@ __all__ = ["ModelConfig", "HardwareConfig", "SkeletalSizes", "SwapPlan", "Timing
            "make_swap_plan_with_alpha", "token_split", "count_params", "estimate_flops_per_sample",
            "mfu_from_tgs", "analytic_timing", "plan_model", "plan_model_json", "solve_dsa",
            "trace_roundtrip", "build_schedule", "validate_schedule", "simulate", "fnv1a_hex",
+           "schedule_timeline_csv",
            "load_run_config"]

@@ -26,8 +26,9 @@ def main():
                     for key, ext in (("trace_text", "trace"), ("plan_json", "plan.json")):
                         if key in rec:
                             path = os.path.join(HERE, "traces", f"{cfg}.{ext}.gz")
-                            with gzip.open(path, "wt") as f:
-                                f.write(rec.pop(key))
+                            with open(path, "wb") as raw, gzip.GzipFile(
+                                    fileobj=raw, mode="wb", mtime=0, filename="") as f:
+                                f.write(rec.pop(key).encode())
                             rec[key + "_file"] = os.path.relpath(path, HERE)
             with open(os.path.join(HERE, name), "w") as f:
                 json.dump(data, f, indent=1, sort_keys=True)

@@ -187,6 +187,7 @@ def test_schedule_goldens(i):
     assert [[P.STREAMS.index(e.stream), P.KINDS.index(e.kind), e.layer, e.start, e.end]
             for e in events] == c["events"]
     assert P.validate_schedule(events, cfg.n_layers, swap) == c["violations"]
+    assert P.schedule_timeline_csv(events) == c["timeline_csv"]  # json_io.hpp:246
     sim = P.simulate(events, cfg, hw, c["params"])
     for k, v in c["sim"].items():
         assert sim[k] == v
