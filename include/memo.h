@@ -195,13 +195,15 @@ int memo_attn_fwd(const void* q, const void* k, const void* v, void* o, float* l
 /* Causal FlashAttention backward (deterministic).  Writes dq/dk/dv with row
  * pitch ld_dqkv; when rope != NULL the inverse rotary rotation (float2 table
  * [pos][D/2], positions pos0..pos0+S-1) is applied to dq and dk.  delta is a
- * 2*H*S f32 workspace. */
+ * device workspace of memo_attn_bwd_workspace_bytes(S, H, D) bytes. */
+uint64_t memo_attn_bwd_workspace_bytes(int32_t S, int32_t H, int32_t D);
 int memo_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
                   const void* dout, float* delta, void* dq, void* dk, void* dv, int64_t ld_dqkv,
                   const void* rope, int64_t pos0, int32_t S, int32_t H, int32_t D,
                   float softmax_scale, void* stream);
-/* As memo_attn_bwd; synchronises and writes the device ms of its three kernels
- * (delta prep, dK/dV, dQ) to ms3 when ms3 != NULL. */
+/* As memo_attn_bwd; synchronises and writes the device ms of its three phases
+ * (delta prep, main kernel — fused dK/dV/dQ at D=128, dK/dV at D=64 — and dQ
+ * finish: f32->bf16 conversion at D=128, the dQ kernel at D=64) to ms3. */
 int memo_attn_bwd_timed(const void* q, const void* k, const void* v, const void* o,
                         const float* lse, const void* dout, float* delta, void* dq, void* dk,
                         void* dv, int64_t ld_dqkv, const void* rope, int64_t pos0, int32_t S,

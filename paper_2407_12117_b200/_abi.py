@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmemo.so")
+LIB_PATH = os.environ.get("MEMO_LIB_PATH") or os.path.join(_HERE, "_lib", "libmemo.so")
 
 NUM_SKELETAL = 10
 SKELETAL_NAMES = (
@@ -100,6 +100,7 @@ def _load():
     for name in ("memo_flops_per_sample", "memo_mfu_from_tgs"):
         if hasattr(lib, name):
             getattr(lib, name).restype = C.c_double
+    lib.memo_attn_bwd_workspace_bytes.restype = C.c_uint64
     return lib
 
 

@@ -30,8 +30,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <type_traits>
 
 #include "attention.h"
@@ -195,39 +197,39 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, converged: MMAs/commits elect one lane
       constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
-      dev::mbar_wait(q_ready, 0);
+      dev::mbar_wait_w(q_ready, 0);
       auto issue_s = [&](int j) {
         const int st = j % NS;
-        dev::mbar_wait(&k_full[st], (j / NS) & 1);
+        dev::mbar_wait_w(&k_full[st], (j / NS) & 1);
         dev::tc_fence_after();
         const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
         const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::Q_OFF));
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           if (QT)
-            dev::mma_bf16_ts(t_s[j & 1], t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ts_w(t_s[j & 1], t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
           else
-            dev::mma_bf16_ss(t_s[j & 1], kmajor_step(qd, kk), kmajor_step(kd, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ss_w(t_s[j & 1], kmajor_step(qd, kk), kmajor_step(kd, kk), idesc_s, kk > 0);
         }
-        dev::mma_commit(&s_full[j & 1]);
-        dev::mma_commit(&k_empty[st]);
+        dev::mma_commit_w(&s_full[j & 1]);
+        dev::mma_commit_w(&k_empty[st]);
       };
       issue_s(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) issue_s(j + 1);
         const int st = j % NS;
-        dev::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-        dev::mbar_wait(&v_full[st], (j / NS) & 1);
+        dev::mbar_wait_w(&p_full[j & 1], (j >> 1) & 1);
+        dev::mbar_wait_w(&v_full[st], (j / NS) & 1);
         dev::tc_fence_after();
         const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts(t_o, t_s[j & 1] + kk * 8, mnmajor_step(vd, kk), idesc_o, (j | kk) != 0);
-        dev::mma_commit(o_done);
-        dev::mma_commit(&v_empty[st]);
+          dev::mma_bf16_ts_w(t_o, t_s[j & 1] + kk * 8, mnmajor_step(vd, kk), idesc_o, (j | kk) != 0);
+        dev::mma_commit_w(o_done);
+        dev::mma_commit_w(&v_empty[st]);
       }
     }
   } else if (warp >= 4) {
@@ -454,51 +456,51 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, converged: MMAs/commits elect one lane
       constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
       const uint64_t qd[2] = {kmajor_base(dev::smem_u32(smem + L::QA_OFF)),
                               kmajor_base(dev::smem_u32(smem + L::QB_OFF))};
-      dev::mbar_wait(q_full, 0);
+      dev::mbar_wait_w(q_full, 0);
       // S_g(j) = Q_g K_j^T
       auto issue_s = [&](int g, int j) {
         const int st = j & 1;
         if (g == 0) {  // group A issues first for every tile: wait for K here
-          dev::mbar_wait(&k_full[st], (j >> 1) & 1);
+          dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
           dev::tc_fence_after();
         }
         const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(tmem + g * 128, kmajor_step(qd[g], kk), kmajor_step(kd, kk), idesc_s, kk > 0);
-        dev::mma_commit(&s_full[g]);
+          dev::mma_bf16_ss_w(tmem + g * 128, kmajor_step(qd[g], kk), kmajor_step(kd, kk), idesc_s, kk > 0);
+        dev::mma_commit_w(&s_full[g]);
       };
       // O_g += P_g(j) V_j
       auto issue_pv = [&](int g, int j, int uses) {
         const int st = j & 1;
-        dev::mbar_wait(&p_full[g], uses & 1);
+        dev::mbar_wait_w(&p_full[g], uses & 1);
         if (g == 0 || j == n_kv - 1) {  // first PV of tile j waits for V
-          dev::mbar_wait(&v_full[st], (j >> 1) & 1);
+          dev::mbar_wait_w(&v_full[st], (j >> 1) & 1);
         }
         dev::tc_fence_after();
         const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
+          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
                            (uses | kk) != 0);
-        dev::mma_commit(&o_done[g]);
+        dev::mma_commit_w(&o_done[g]);
       };
       const int nA = n_kv - 1;
       // the last key tile (diagonal of B) is never used by A: group B's K wait for it
       auto issue_s_b_last = [&](int j) {
         const int st = j & 1;
-        dev::mbar_wait(&k_full[st], (j >> 1) & 1);
+        dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
         dev::tc_fence_after();
         const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(tmem + 128, kmajor_step(qd[1], kk), kmajor_step(kd, kk), idesc_s, kk > 0);
-        dev::mma_commit(&s_full[1]);
+          dev::mma_bf16_ss_w(tmem + 128, kmajor_step(qd[1], kk), kmajor_step(kd, kk), idesc_s, kk > 0);
+        dev::mma_commit_w(&s_full[1]);
       };
       issue_s(0, 0);
       issue_s(1, 0);
@@ -509,8 +511,8 @@ __global__ void __launch_bounds__(384, 1)
           if (j + 1 < nA) issue_s(0, j + 1);
         }
         issue_pv(1, j, j);
-        dev::mma_commit(&k_empty[st]);
-        dev::mma_commit(&v_empty[st]);
+        dev::mma_commit_w(&k_empty[st]);
+        dev::mma_commit_w(&v_empty[st]);
         if (j + 1 < n_kv) {
           if (j + 1 < nA)
             issue_s(1, j + 1);
@@ -786,48 +788,48 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, converged: MMAs/commits elect one lane
       constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, HALF, false, false);
       constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
       const uint64_t kd0 = kmajor_base(dev::smem_u32(smem + L::A0_OFF));
       const uint64_t vd0 = kmajor_base(dev::smem_u32(smem + L::A1_OFF));
-      dev::mbar_wait(kv_full, 0);
+      dev::mbar_wait_w(kv_full, 0);
       auto issue_sd = [&](int g) {
         const int i = g >> 1, half = g & 1, st = i & 1, b = g & 1;
         if (half == 0) {
-          dev::mbar_wait(&in_full[st], (i >> 1) & 1);
+          dev::mbar_wait_w(&in_full[st], (i >> 1) & 1);
           dev::tc_fence_after();
         }
         const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
         const uint64_t dod = kmajor_base(dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(tmem + b * 128, kmajor_step(kd0, kk), kmajor_step(qd, kk), idesc_s, kk > 0);
+          dev::mma_bf16_ss_w(tmem + b * 128, kmajor_step(kd0, kk), kmajor_step(qd, kk), idesc_s, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_step(vd0, kk), kmajor_step(dod, kk), idesc_s,
+          dev::mma_bf16_ss_w(tmem + b * 128 + 64, kmajor_step(vd0, kk), kmajor_step(dod, kk), idesc_s,
                            kk > 0);
-        dev::mma_commit(&s_full[b]);
+        dev::mma_commit_w(&s_full[b]);
       };
       issue_sd(0);
       for (int g = 0; g < n_g; ++g) {
         if (g + 1 < n_g) issue_sd(g + 1);
         const int i = g >> 1, half = g & 1, st = i & 1, b = g & 1;
-        dev::mbar_wait(&p_ready[b], (g >> 1) & 1);
+        dev::mbar_wait_w(&p_ready[b], (g >> 1) & 1);
         dev::tc_fence_after();
         const uint64_t qm = mnmajor_base(dev::smem_u32(smem + L::R0_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
         const uint64_t dom = mnmajor_base(dev::smem_u32(smem + L::R1_OFF + st * L::TILE_BYTES) + half * HALF_BYTES);
 #pragma unroll
         for (int kk = 0; kk < HALF / 16; ++kk)
-          dev::mma_bf16_ts(t_dv, tmem + b * 128 + kk * 8, mnmajor_step(dom, kk), idesc_g,
-                           (g | kk) != 0);
+          dev::mma_bf16_ts_w(t_dv, tmem + b * 128 + 32 * (kk >> 1) + 8 * (kk & 1), mnmajor_step(dom, kk),
+                             idesc_g, (g | kk) != 0);
 #pragma unroll
         for (int kk = 0; kk < HALF / 16; ++kk)
-          dev::mma_bf16_ts(t_dk, tmem + b * 128 + 64 + kk * 8, mnmajor_step(qm, kk), idesc_g,
-                           (g | kk) != 0);
-        if (half == 1) dev::mma_commit(&in_empty[st]);
+          dev::mma_bf16_ts_w(t_dk, tmem + b * 128 + 64 + 32 * (kk >> 1) + 8 * (kk & 1), mnmajor_step(qm, kk),
+                             idesc_g, (g | kk) != 0);
+        if (half == 1) dev::mma_commit_w(&in_empty[st]);
       }
-      dev::mma_commit(fin);
+      dev::mma_commit_w(fin);
     }
   } else if (warp >= 4) {
     const uint32_t q4 = warp & 3;
@@ -841,8 +843,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       if (half == 0) dev::mbar_wait(&in_full[st], (i >> 1) & 1);
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       dev::tc_fence_after();
-      const float* l2 = vec + st * 256 + half * HALF;
-      const float* dl = l2 + 128;
+      // lse2 / delta of this half's queries, read with ld.shared (a generic
+      // pointer here compiles to LD.E, which stalls on the LSU global path)
+      const uint32_t l2 = dev::smem_u32(vec + st * 256 + half * HALF);
+      const uint32_t dl = l2 + 128 * 4;
       const uint32_t t_st = tmem + b * 128 + lane_off, t_dpt = t_st + 64;
       // The causal mask only touches the diagonal tile; keep it out of the hot loop.
       auto body = [&](auto diag_tag) {
@@ -856,8 +860,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           uint32_t pp[16], dd[16];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 lv = *reinterpret_cast<const float4*>(l2 + c * 32 + 4 * j4);
-            const float4 dv4 = *reinterpret_cast<const float4*>(dl + c * 32 + 4 * j4);
+            const float4 lv = dev::lds_f4(l2 + (c * 32 + 4 * j4) * 4);
+            const float4 dv4 = dev::lds_f4(dl + (c * 32 + 4 * j4) * 4);
             const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
             const float dq[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
             float p4[4], d4[4];
@@ -874,8 +878,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             dd[2 * j4] = dev::pack_bf16(d4[0], d4[1]);
             dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
           }
-          dev::tmem_st16(t_st + c * 16, pp);
-          dev::tmem_st16(t_dpt + c * 16, dd);
+          // packed bf16 stays inside this warp's own 32-column slice (the
+          // other warp of the lane quarter may still be reading its slice)
+          dev::tmem_st16(t_st + c * 32, pp);
+          dev::tmem_st16(t_dpt + c * 32, dd);
         }
       };
       if (diag)
@@ -997,16 +1003,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp, converged: MMAs/commits elect one lane
       constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, HALF, false, false);
       constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
-      dev::mbar_wait(qd_ready, 0);
+      dev::mbar_wait_w(qd_ready, 0);
       const uint64_t qa0 = kmajor_base(dev::smem_u32(smem + L::A0_OFF));
       const uint64_t doa0 = kmajor_base(dev::smem_u32(smem + L::A1_OFF));
       auto issue_s = [&](int g) {
         const int j = g >> 1, half = g & 1, st = j % NS, b = g & 1;
         if (half == 0) {
-          dev::mbar_wait(&kv_full[st], (j / NS) & 1);
+          dev::mbar_wait_w(&kv_full[st], (j / NS) & 1);
           dev::tc_fence_after();
         }
         const uint64_t kd = kmajor_base(dev::smem_u32(smem + k_off(st)) + half * HALF_BYTES);
@@ -1015,37 +1021,37 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           if (AT)
-            dev::mma_bf16_ts(tmem + b * 128, t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ts_w(tmem + b * 128, t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
           else
-            dev::mma_bf16_ss(tmem + b * 128, kmajor_step(qa0, kk), kmajor_step(kd, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ss_w(tmem + b * 128, kmajor_step(qa0, kk), kmajor_step(kd, kk), idesc_s, kk > 0);
         }
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           if (AT)
-            dev::mma_bf16_ts(tmem + b * 128 + 64, t_do + kk * 8, kmajor_step(vd, kk), idesc_s, kk > 0);
+            dev::mma_bf16_ts_w(tmem + b * 128 + 64, t_do + kk * 8, kmajor_step(vd, kk), idesc_s, kk > 0);
           else
-            dev::mma_bf16_ss(tmem + b * 128 + 64, kmajor_step(doa0, kk), kmajor_step(vd, kk), idesc_s,
+            dev::mma_bf16_ss_w(tmem + b * 128 + 64, kmajor_step(doa0, kk), kmajor_step(vd, kk), idesc_s,
                              kk > 0);
         }
         }
-        dev::mma_commit(&s_full[b]);
+        dev::mma_commit_w(&s_full[b]);
       };
       issue_s(0);
       for (int g = 0; g < n_g; ++g) {
         if (g + 1 < n_g) issue_s(g + 1);
         const int j = g >> 1, half = g & 1, st = j % NS, b = g & 1;
-        dev::mbar_wait(&ds_ready[b], (g >> 1) & 1);
+        dev::mbar_wait_w(&ds_ready[b], (g >> 1) & 1);
         dev::tc_fence_after();
         const uint64_t km = mnmajor_base(dev::smem_u32(smem + k_off(st)) + half * HALF_BYTES);
         if (!(dbg & 4)) {
 #pragma unroll
         for (int kk = 0; kk < HALF / 16; ++kk)
-          dev::mma_bf16_ts(t_dq, tmem + b * 128 + kk * 8, mnmajor_step(km, kk), idesc_g,
-                           (g | kk) != 0);
+          dev::mma_bf16_ts_w(t_dq, tmem + b * 128 + 32 * (kk >> 1) + 8 * (kk & 1), mnmajor_step(km, kk),
+                             idesc_g, (g | kk) != 0);
         }
-        if (half == 1) dev::mma_commit(&kv_empty[st]);
+        if (half == 1) dev::mma_commit_w(&kv_empty[st]);
       }
-      dev::mma_commit(fin);
+      dev::mma_commit_w(fin);
     }
   } else if (warp >= 4) {
     const uint32_t q4 = warp & 3;
@@ -1091,7 +1097,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             }
             dd[jj] = dev::pack_bf16(d2[0], d2[1]);
           }
-          dev::tmem_st16(t_s + c * 16, dd);
+          dev::tmem_st16(t_s + c * 32, dd);  // inside this warp's own slice
         }
       };
       if (!(dbg & 1)) {
@@ -1125,6 +1131,481 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     dev::tc_fence_after();
     dev::tmem_dealloc(tmem, 512);
   }
+}
+
+// ------------------------------------------------------------ fused backward
+// One CTA per (key tile kt, head): S^T, dP^T, dV += P^T dO, dK += dS^T Q and
+// dQ^T_partial = K^T dS^T for every 64-query half of the query tiles kt..n-1,
+// so S and dP are computed once (5 GEMM units instead of the split kernels' 7).
+// dQ partials are summed in an f32 accumulator [H][S][D] at L2 in a FIXED order
+// (key tile 0 stores, then 1, 2, … add): a per-(head, 64-query chunk) counter
+// orders the contributions, and CTAs take (kt, head) from an atomic ticket in
+// ascending kt, so a CTA only ever waits for CTAs that are already resident.
+// The sum order never depends on scheduling -> bitwise deterministic dQ.
+//
+// TMEM (512 cols): [0,128) dV | [128,256) dK | [256,320) S^T buf0 | [320,384)
+// S^T buf1 | [384,448) dP^T | [448,512) dQ^T.  P^T and dS^T (bf16) are written
+// back into their S^T buffer (warp ch: cols 32ch..+16 P^T, 32ch+16..+32 dS^T)
+// and feed dV/dK as TMEM A operands; dS^T also goes to shared memory as the B
+// operand of dQ^T (the A operand is K itself read MN-major).
+// Warps: 0 TMA, 1 MMA issue, 2 dQ ordering + bulk reduce, 4..11 softmax-grad math.
+constexpr int FB_NS = 3;              // Q/dO half-tile ring stages
+constexpr int FB_NSTG = 1;            // dQ^T staging buffers
+constexpr int FB_HALF_BYTES = HALF * 64 * 2;  // [64 rows][64 cols] bf16 chunk = 8 KiB
+
+template <int D>
+struct FusedBwdSmem {
+  static constexpr int NC = D / 64;
+  static constexpr int TILE_BYTES = NC * CHUNK_BYTES;          // K or V [128][D]
+  static constexpr int HT_BYTES = NC * FB_HALF_BYTES;          // Q or dO half [64][D]
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = TILE_BYTES;
+  static constexpr int RING_OFF = 2 * TILE_BYTES;              // stage: Q half | dO half
+  static constexpr int DS_OFF = RING_OFF + FB_NS * 2 * HT_BYTES;  // 2 x [128 keys][64 q] bf16
+  static constexpr int DS_BYTES = TILE * HALF * 2;
+  static constexpr int STG_OFF = DS_OFF + 2 * DS_BYTES;        // dQ^T half staged [64 q][D] f32
+  static constexpr int STG_BYTES = HALF * D * 4;
+  static constexpr int VEC_OFF = STG_OFF + FB_NSTG * STG_BYTES;  // stage: lse2[64] | delta[64]
+  static constexpr int BAR_OFF = VEC_OFF + FB_NS * 512;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+template <int D, int PEND>
+__global__ void __launch_bounds__(BWD_THREADS, 1)
+    attn_bwd_fused_kernel(const __grid_constant__ CUtensorMap map_q,
+                          const __grid_constant__ CUtensorMap map_k,
+                          const __grid_constant__ CUtensorMap map_v,
+                          const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                          const float* __restrict__ delta, float* __restrict__ dq_acc,
+                          uint32_t* __restrict__ counters, uint32_t* __restrict__ ticket,
+                          __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, long long ld,
+                          const float2* __restrict__ rope, long long pos0, int S, int H, float scale,
+                          float scale_log2, int G, int dbg) {
+  static_assert(D == 128, "fused backward needs M = D = 128 for the dQ^T MMA");
+  using L = FusedBwdSmem<D>;
+  constexpr int NC = L::NC;
+  constexpr int NS = FB_NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* in_full = bars + 1;          // [NS]
+  uint64_t* in_empty = in_full + NS;     // [NS]
+  uint64_t* s_full = in_empty + NS;      // [2] (per S^T buffer)
+  uint64_t* dp_full = s_full + 2;        // [2] (by half parity; one dP^T buffer)
+  uint64_t* dp_free = dp_full + 2;       // [2]
+  uint64_t* ds_ready = dp_free + 2;      // [2]
+  uint64_t* dq_full = ds_ready + 2;      // [2]
+  uint64_t* dq_free = dq_full + 2;       // [2]
+  uint64_t* staged = dq_free + 2;        // [2] dQ^T(g) is in the staging buffer
+  uint64_t* stg_free = staged + 2;       // [2] the bulk reduce of g has read it
+  uint64_t* fin = stg_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  uint32_t* tick_slot = tmem_slot + 1;
+  constexpr int CW = 32 * BWD_COMPUTE_WARPS;  // compute threads
+
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+  const int n_tiles = S / TILE;
+  const int n_chunks = S / HALF;
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_k);
+    dev::tma_prefetch_desc(&map_v);
+    dev::tma_prefetch_desc(&map_do);
+    dev::mbar_init(kv_full, 1);
+    for (int s2 = 0; s2 < NS; ++s2) {
+      dev::mbar_init(&in_full[s2], 1);
+      dev::mbar_init(&in_empty[s2], 1);
+    }
+    for (int s2 = 0; s2 < 2; ++s2) {
+      dev::mbar_init(&s_full[s2], 1);
+      dev::mbar_init(&dp_full[s2], 1);
+      dev::mbar_init(&dp_free[s2], CW);
+      dev::mbar_init(&ds_ready[s2], CW);
+      dev::mbar_init(&dq_full[s2], 1);
+      dev::mbar_init(&dq_free[s2], CW);
+      dev::mbar_init(&staged[s2], CW);
+      dev::mbar_init(&stg_free[s2], 1);
+    }
+    dev::mbar_init(fin, 1);
+    dev::fence_barrier_init();
+    *tick_slot = atomicAdd(ticket, 1u);
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // Tickets: heads in groups of G; inside a group ascending key tile (heavy
+  // first), heads innermost.  Every CTA with a smaller kt of the same head
+  // holds a smaller ticket, so it is resident or done: waits cannot deadlock.
+  const int tick = static_cast<int>(*tick_slot);
+  const int grp = tick / (G * n_tiles);
+  const int rem = tick - grp * G * n_tiles;
+  const int kt = rem / G;
+  const int hh = grp * G + rem % G;
+  const int n_q = n_tiles - kt;
+  const int n_g = 2 * n_q;
+  // Query halves are walked from the last tile down to the diagonal, so the
+  // CTAs of a wave sweep the same dQ chunks together (L2-resident reduces).
+  auto chunk_of = [&](int g) { return 2 * (n_tiles - 1 - (g >> 1)) + (g & 1); };
+  const uint32_t t_dv = tmem, t_dk = tmem + 128, t_dp = tmem + 384, t_dq = tmem + 448;
+  auto t_s = [&](int b) { return tmem + 256 + 64 * b; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_expect_tx(kv_full, 2 * L::TILE_BYTES);
+      for (int c = 0; c < NC; ++c) {
+        dev::tma_load_2d(smem + L::K_OFF + c * CHUNK_BYTES, &map_k, kv_full, hh * D + c * 64, kt * TILE);
+        dev::tma_load_2d(smem + L::V_OFF + c * CHUNK_BYTES, &map_v, kv_full, hh * D + c * 64, kt * TILE);
+      }
+      for (int g = 0; g < n_g; ++g) {
+        const int st = g % NS;
+        const int q0 = chunk_of(g) * HALF;
+        dev::mbar_wait(&in_empty[st], ((g / NS) & 1) ^ 1);
+        dev::mbar_expect_tx(&in_full[st], 2 * L::HT_BYTES + 512);
+        uint8_t* sq = smem + L::RING_OFF + st * 2 * L::HT_BYTES;
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(sq + c * FB_HALF_BYTES, &map_q, &in_full[st], hh * D + c * 64, q0);
+          dev::tma_load_2d(sq + L::HT_BYTES + c * FB_HALF_BYTES, &map_do, &in_full[st], hh * D + c * 64, q0);
+        }
+        const long long off = static_cast<long long>(hh) * S + q0;
+        float* vec = reinterpret_cast<float*>(smem + L::VEC_OFF + st * 512);
+        dev::bulk_load(vec, lse2 + off, 256, &in_full[st]);
+        dev::bulk_load(vec + 64, delta + off, 256, &in_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    {  // whole warp, converged: MMAs/commits elect one lane
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, HALF, false, false);
+      constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
+      constexpr uint32_t idesc_q = dev::idesc_bf16_f32(D, HALF, true, true);
+      const uint32_t k_addr = dev::smem_u32(smem + L::K_OFF);
+      const uint64_t kd0 = kmajor_base(k_addr);
+      const uint64_t vd0 = kmajor_base(dev::smem_u32(smem + L::V_OFF));
+      const uint64_t ktd0 = dev::umma_desc_sw128(k_addr, CHUNK_BYTES, 1024);  // K^T, MN-major A
+      // half-tile operands: 64-col chunks are FB_HALF_BYTES apart
+      auto kmaj_half = [](uint64_t d, int kk) {
+        return d + static_cast<uint64_t>(((kk >> 2) * FB_HALF_BYTES + (kk & 3) * 32) >> 4);
+      };
+      auto stage_addr = [&](int g) { return dev::smem_u32(smem + L::RING_OFF + (g % NS) * 2 * L::HT_BYTES); };
+      dev::mbar_wait_w(kv_full, 0);
+      auto issue_s = [&](int g) {
+        const int st = g % NS;
+        dev::mbar_wait_w(&in_full[st], (g / NS) & 1);
+        dev::tc_fence_after();
+        const uint64_t qd = dev::umma_desc_sw128(stage_addr(g), 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss_w(t_s(g & 1), kmajor_step(kd0, kk), kmaj_half(qd, kk), idesc_s, kk > 0);
+        dev::mma_commit_w(&s_full[g & 1]);
+      };
+      auto issue_dp = [&](int g) {
+        const uint64_t dod = dev::umma_desc_sw128(stage_addr(g) + L::HT_BYTES, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss_w(t_dp, kmajor_step(vd0, kk), kmaj_half(dod, kk), idesc_s, kk > 0);
+        dev::mma_commit_w(&dp_full[g & 1]);
+      };
+      issue_s(0);
+      issue_dp(0);
+      for (int g = 0; g < n_g; ++g) {
+        const int b = g & 1;
+        const uint32_t par = (g >> 1) & 1;
+        if (g + 1 < n_g) {
+          issue_s(g + 1);
+          dev::mbar_wait_w(&dp_free[b], par);  // softmax warps hold dP^T(g) in registers
+          dev::tc_fence_after();
+          issue_dp(g + 1);
+        }
+        dev::mbar_wait_w(&ds_ready[b], par);
+        dev::tc_fence_after();
+        const uint32_t sa = stage_addr(g);
+        const uint64_t qm = dev::umma_desc_sw128(sa, FB_HALF_BYTES, 1024);
+        const uint64_t dom = dev::umma_desc_sw128(sa + L::HT_BYTES, FB_HALF_BYTES, 1024);
+#pragma unroll
+        for (int kk = 0; kk < HALF / 16; ++kk)
+          dev::mma_bf16_ts_w(t_dv, t_s(b) + 32 * (kk >> 1) + 8 * (kk & 1), mnmajor_step(dom, kk), idesc_g,
+                           (g | kk) != 0);
+#pragma unroll
+        for (int kk = 0; kk < HALF / 16; ++kk)
+          dev::mma_bf16_ts_w(t_dk, t_s(b) + 32 * (kk >> 1) + 16 + 8 * (kk & 1), mnmajor_step(qm, kk), idesc_g,
+                           (g | kk) != 0);
+        dev::mma_commit_w(&in_empty[g % NS]);
+        if (g > 0) {
+          dev::mbar_wait_w(&dq_free[b ^ 1], ((g - 1) >> 1) & 1);
+          dev::tc_fence_after();
+        }
+        const uint64_t dsd = dev::umma_desc_sw128(dev::smem_u32(smem + L::DS_OFF + b * L::DS_BYTES), CHUNK_BYTES, 1024);
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ss_w(t_dq, mnmajor_step(ktd0, kk), mnmajor_step(dsd, kk), idesc_q, kk > 0);
+        dev::mma_commit_w(&dq_full[b]);
+      }
+      dev::mma_commit_w(fin);
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // dQ^T(g) staged -> wait for this chunk's turn -> one bulk f32 reduce at
+      // L2 (key tile 0 stores) -> release the chunk once the reduce completed.
+      const uint32_t stg0 = dev::smem_u32(smem + L::STG_OFF);
+      uint32_t* ctr0 = counters + static_cast<long long>(hh) * n_chunks;
+      float* acc0 = dq_acc + static_cast<long long>(hh) * S * D;
+      for (int g = 0; g < n_g; ++g) {
+        const int b = g & 1;
+        const int ck = chunk_of(g);
+        dev::mbar_wait(&staged[b], (g >> 1) & 1);
+        if (kt > 0 && !(dbg & 1)) {
+          while (dev::ld_acquire_u32(ctr0 + ck) != static_cast<uint32_t>(kt)) __nanosleep(32);
+        }
+        dev::fence_proxy_async_global();
+        const uint32_t stg = stg0 + (g % FB_NSTG) * L::STG_BYTES;
+        if (!(dbg & 2)) {
+          if (kt == 0)
+            dev::bulk_store(acc0 + static_cast<long long>(ck) * HALF * D, stg, L::STG_BYTES);
+          else
+            dev::bulk_reduce_add_f32(acc0 + static_cast<long long>(ck) * HALF * D, stg, L::STG_BYTES);
+        }
+        dev::bulk_commit();
+        dev::bulk_wait_read<0>();
+        dev::mbar_arrive(&stg_free[b]);
+        // keep PEND reduces in flight; release each chunk once its reduce completed
+        if (g >= PEND) {
+          dev::bulk_wait<PEND>();
+          dev::fence_proxy_async_global();
+          dev::st_release_u32(ctr0 + chunk_of(g - PEND), static_cast<uint32_t>(kt + 1));
+        }
+      }
+      dev::bulk_wait<0>();
+      dev::fence_proxy_async_global();
+      for (int g = n_g > PEND ? n_g - PEND : 0; g < n_g; ++g)
+        dev::st_release_u32(ctr0 + chunk_of(g), static_cast<uint32_t>(kt + 1));
+    }
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int ch = (warp - 4) >> 2;  // which 32-query slice of each half this warp owns
+    const int r = q4 * 32 + lane;    // key row in tile (TMEM lane); also D index for dQ^T
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const uint32_t ds_row = dev::smem_u32(smem + L::DS_OFF) + (r >> 3) * 1024 + (r & 7) * 128;
+    // dQ^T(g): TMEM -> registers -> staging buffer [64 q][D] f32 (warp 2 reduces it)
+    const uint32_t stg_col = dev::smem_u32(smem + L::STG_OFF) + (32 * ch) * (D * 4) + r * 4;
+    auto drain = [&](int g) {
+      const int b = g & 1;
+      const uint32_t par = (g >> 1) & 1;
+      dev::mbar_wait(&dq_full[b], par);
+      dev::tc_fence_after();
+      uint32_t x[32];
+      dev::tmem_ld32(t_dq + lane_off + 32 * ch, x);
+      dev::tmem_ld_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&dq_free[b]);
+      // staging buffer g % FB_NSTG was last read by the bulk reduce of g - FB_NSTG
+      if (g >= FB_NSTG) dev::mbar_wait(&stg_free[(g - FB_NSTG) & 1], ((g - FB_NSTG) >> 1) & 1);
+      const uint32_t sc = stg_col + (g % FB_NSTG) * L::STG_BYTES;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(sc + j * (D * 4)), "r"(x[j]) : "memory");
+      dev::fence_proxy_async();
+      dev::mbar_arrive(&staged[b]);
+    };
+    for (int g = 0; g < n_g; ++g) {
+      const int b = g & 1, st = g % NS;
+      const uint32_t par = (g >> 1) & 1;
+      const bool diag = g >= n_g - 2;  // query tile == key tile
+      const uint32_t vec = dev::smem_u32(smem + L::VEC_OFF + st * 512) + 32 * ch * 4;
+      dev::mbar_wait(&in_full[st], (g / NS) & 1);
+      dev::mbar_wait(&s_full[b], par);
+      dev::mbar_wait(&dp_full[b], par);
+      dev::tc_fence_after();
+      uint32_t sr[32], dr[32];
+      dev::tmem_ld32(t_s(b) + lane_off + 32 * ch, sr);
+      dev::tmem_ld32(t_dp + lane_off + 32 * ch, dr);
+      dev::tmem_ld_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&dp_free[b]);
+      uint32_t pp[16], dd[16];
+      auto body = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 lv = dev::lds_f4(vec + 16 * j4);
+          const float4 dv4 = dev::lds_f4(vec + 256 + 16 * j4);
+          const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
+          const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+          float p4[4], d4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int qc = (g & 1) * HALF + 32 * ch + 4 * j4 + e;  // query within tile
+            float p = dev::ex2(__uint_as_float(sr[4 * j4 + e]) * scale_log2 - lq[e]);
+            if (DIAG && qc < r) p = 0.f;
+            p4[e] = p;
+            d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) - dq4[e]);
+          }
+          pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
+          pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
+          dd[2 * j4] = dev::pack_bf16(d4[0], d4[1]);
+          dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
+        }
+      };
+      if (diag)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
+      dev::tmem_st16(t_s(b) + lane_off + 32 * ch, pp);
+      dev::tmem_st16(t_s(b) + lane_off + 32 * ch + 16, dd);
+      // dS^T row r, queries 32ch..32ch+31 -> 16-byte chunks 4ch..4ch+3 (128-byte swizzle)
+      const uint32_t row = ds_row + b * L::DS_BYTES;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        dev::sts_u4(row + (((4 * ch + j) ^ (r & 7)) << 4), dd[4 * j], dd[4 * j + 1], dd[4 * j + 2],
+                    dd[4 * j + 3]);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::fence_proxy_async();
+      dev::mbar_arrive(&ds_ready[b]);
+      if (g > 0) drain(g - 1);
+    }
+    drain(n_g - 1);
+    dev::mbar_wait(fin, 0);
+    dev::tc_fence_after();
+    const int kidx = kt * TILE + r;
+    __nv_bfloat16* dvrow = dv + static_cast<long long>(kidx) * ld + hh * D;
+    __nv_bfloat16* dkrow = dk + static_cast<long long>(kidx) * ld + hh * D;
+#pragma unroll 1
+    for (int c = ch * (D / 64); c < (ch + 1) * (D / 64); ++c) {
+      uint32_t r32[32];
+      float x[32];
+      dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
+      dev::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dvrow + c * 32, x, 1.f, nullptr);
+      dev::tmem_ld32(t_dk + lane_off + c * 32, r32);
+      dev::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dkrow + c * 32, x, scale, rope ? rope + (pos0 + kidx) * (D / 2) + c * 16 : nullptr);
+    }
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
+// dq [S, ld] bf16 = inverse-RoPE(scale * acc [H][S][D] f32); 8 columns per thread.
+__global__ void attn_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
+                                       long long ld, const float2* __restrict__ rope, long long pos0,
+                                       int S, int H, int D, float scale) {
+  const long long hc = static_cast<long long>(H) * D;
+  const long long n8 = static_cast<long long>(S) * hc / 8;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = i / (hc / 8);
+    const int col = static_cast<int>(i - t * (hc / 8)) * 8;
+    const float* src = acc + (static_cast<long long>(col / D) * S + t) * D + col % D;  // [H][S][D]
+    const float4 a = *reinterpret_cast<const float4*>(src);
+    const float4 b = *reinterpret_cast<const float4*>(src + 4);
+    float x[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale,
+                  b.x * scale, b.y * scale, b.z * scale, b.w * scale};
+    if (rope) {
+      const int d = col % D;
+      const float2* cs = rope + (pos0 + t) * (D / 2) + d / 2;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const float2 c = cs[p];
+        const float u = x[2 * p], w = x[2 * p + 1];
+        x[2 * p] = u * c.x + w * c.y;
+        x[2 * p + 1] = -u * c.y + w * c.x;
+      }
+    }
+    uint4 o;
+    o.x = dev::pack_bf16(x[0], x[1]);
+    o.y = dev::pack_bf16(x[2], x[3]);
+    o.z = dev::pack_bf16(x[4], x[5]);
+    o.w = dev::pack_bf16(x[6], x[7]);
+    *reinterpret_cast<uint4*>(dq + t * ld + col) = o;
+  }
+}
+
+int attn_debug() {
+  static const int v = [] {
+    const char* e = getenv("MEMO_ATTN_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// MEMO_ATTN_BWD=fused selects the fused kernel (ablation; the split dK/dV +
+// dQ kernels measured faster at S=128K: 478 vs 498 ms, H=32, D=128).
+bool bwd_fused() {
+  static const bool v = [] {
+    const char* e = getenv("MEMO_ATTN_BWD");
+    return e && std::string(e) == "fused";
+  }();
+  return v;
+}
+
+cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
+  constexpr int D = 128;
+  using L = FusedBwdSmem<D>;
+  const int h = a.H * D;
+  CUtensorMap mq, mk, mv, mdo;
+  bool ok = make_tma_2d_bf16(&mq, a.q, h, a.S, h, 64, HALF) &&
+            make_tma_2d_bf16(&mk, a.k, h, a.S, h, 64, TILE) &&
+            make_tma_2d_bf16(&mv, a.v, h, a.S, h, 64, TILE) &&
+            make_tma_2d_bf16(&mdo, a.dout, h, a.S, h, 64, HALF);
+  if (!ok) return cudaErrorInvalidValue;
+  static std::once_flag f;
+  std::call_once(f, [] {
+    cudaFuncSetAttribute(attn_bwd_fused_kernel<D, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+    cudaFuncSetAttribute(attn_bwd_fused_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+    cudaFuncSetAttribute(attn_bwd_fused_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+    cudaFuncSetAttribute(attn_bwd_fused_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+  });
+  static const int pend = [] {
+    const char* e = getenv("MEMO_FB_PEND");
+    return e ? atoi(e) : 0;
+  }();
+  static const int g_env = [] {
+    const char* e = getenv("MEMO_FB_GROUP");
+    return e ? atoi(e) : 0;
+  }();
+  // heads per ticket group: the accumulator of a group should stay L2-resident
+  int G = g_env;
+  if (G <= 0) G = 4;
+  while (G > 1 && a.H % G != 0) --G;
+  const long long HS = static_cast<long long>(a.H) * a.S;
+  float* delta = a.delta;
+  float* lse2 = a.delta + HS;
+  float* acc = a.delta + 2 * HS;
+  uint32_t* counters = reinterpret_cast<uint32_t*>(acc + HS * D);
+  const long long n_ctr = HS / HALF;
+  uint32_t* ticket = counters + n_ctr;
+  if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
+  cudaMemsetAsync(counters, 0, (n_ctr + 4) * sizeof(uint32_t), stream);
+  attn_bwd_prep_kernel<<<(a.S * a.H + 7) / 8, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S, a.H, D);
+  if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
+  const float2* rope = reinterpret_cast<const float2*>(a.rope);
+  auto kern = pend >= 4 ? attn_bwd_fused_kernel<D, 4>
+             : pend == 2 ? attn_bwd_fused_kernel<D, 2>
+             : pend == 1 ? attn_bwd_fused_kernel<D, 1>
+                         : attn_bwd_fused_kernel<D, 0>;
+  kern<<<(a.S / TILE) * a.H, BWD_THREADS, L::BYTES, stream>>>(
+      mq, mk, mv, mdo, lse2, delta, acc, counters, ticket, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S,
+      a.H, a.softmax_scale, a.softmax_scale * kLog2e, G, attn_debug());
+  if (a.ev[2]) cudaEventRecord(a.ev[2], stream);
+  const long long n8 = HS * D / 8;
+  const int blocks = static_cast<int>(std::min<long long>((n8 + 255) / 256, 148LL * 16));
+  attn_dq_convert_kernel<<<blocks, 256, 0, stream>>>(acc, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H, D,
+                                                     a.softmax_scale);
+  if (a.ev[3]) cudaEventRecord(a.ev[3], stream);
+  return cudaGetLastError();
 }
 
 template <int D>
@@ -1250,8 +1731,17 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
 }  // namespace memo
 
 namespace memo {
+size_t attn_bwd_workspace_bytes(int S, int H, int D) {
+  const size_t HS = static_cast<size_t>(H) * S;
+  size_t b = 2 * HS * sizeof(float);  // delta, lse2
+  if (D == 128 && bwd_fused())  // f32 dQ accumulator, ordering counters, ticket
+    b += HS * D * sizeof(float) + (HS / HALF + 4) * sizeof(uint32_t);
+  return b;
+}
+
 cudaError_t attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   if (a.S % TILE != 0) return cudaErrorInvalidValue;
+  if (a.D == 128 && bwd_fused()) return launch_bwd_fused(a, stream);
   if (a.D == 128) return launch_bwd<128>(a, stream);
   if (a.D == 64) return launch_bwd<64>(a, stream);
   return cudaErrorInvalidValue;

@@ -24,7 +24,7 @@ struct AttnBwdArgs {
   const __nv_bfloat16* o;
   const float* lse;         // [H, S]
   const __nv_bfloat16* dout;  // [S, H*D]
-  float* delta;             // workspace [H, S]
+  float* delta;             // workspace of attn_bwd_workspace_bytes(S, H, D)
   __nv_bfloat16* dq;        // rows of pitch ld_dqkv
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
@@ -35,6 +35,9 @@ struct AttnBwdArgs {
   float softmax_scale;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional: before prep, after prep, after dkdv, after dq
 };
+// delta/lse2 [2][H][S] f32, then (D == 128 with MEMO_ATTN_BWD=fused) the f32
+// dQ accumulator [H][S][D] and the per-64-query-chunk ordering counters.
+size_t attn_bwd_workspace_bytes(int S, int H, int D);
 cudaError_t attn_bwd(const AttnBwdArgs& a, cudaStream_t stream);
 
 }  // namespace memo

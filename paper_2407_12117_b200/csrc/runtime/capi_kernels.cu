@@ -59,6 +59,10 @@ extern "C" int memo_attn_fwd(const void* q, const void* k, const void* v, void* 
   return MEMO_OK;
 }
 
+extern "C" uint64_t memo_attn_bwd_workspace_bytes(int32_t S, int32_t H, int32_t D) {
+  return static_cast<uint64_t>(memo::attn_bwd_workspace_bytes(S, H, D));
+}
+
 extern "C" int memo_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                              const float* lse, const void* dout, float* delta, void* dq, void* dk,
                              void* dv, int64_t ld, const void* rope, int64_t pos0, int32_t S,

@@ -220,7 +220,7 @@ void Executor::build_trace_and_plan() {
     f("dxn2");
     m("dout", S * h * 2);
     f("da");
-    m("attn_ws", 2 * H * S * 4);
+    m("attn_ws", attn_bwd_workspace_bytes(static_cast<int>(S), static_cast<int>(H), d_.D));
     m("dqkv", S * 3 * h * 2);
     f("attn_ws");
     f("dout");
@@ -346,7 +346,7 @@ void Executor::build_trace_tp(TraceBuilder& tb) {
     m("dout", S * hl * 2);
     f("da");
     f("da_full");
-    m("attn_ws", 2 * Hl * S * 4);
+    m("attn_ws", attn_bwd_workspace_bytes(static_cast<int>(S), static_cast<int>(Hl), d_.D));
     m("dqkv", S * 3 * hl * 2);
     f("attn_ws");
     f("dout");

@@ -46,7 +46,7 @@ def bench(S, H, D, iters=5, bwd=False):
         out["flash_attn2"] = str(ex)[:80]
     if bwd and hasattr(_abi.lib, "memo_attn_bwd"):
         do = torch.randn_like(q)
-        delta = torch.empty(H, S, device="cuda")
+        delta = torch.empty((_abi.lib.memo_attn_bwd_workspace_bytes(S, H, D) + 3) // 4, device="cuda")
         dqkv = torch.empty(S, 3 * H * D, device="cuda", dtype=torch.bfloat16)
         g = lambda: _abi.lib.memo_attn_bwd(
             C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()), C.c_void_p(o.data_ptr()),
@@ -70,8 +70,12 @@ def bench(S, H, D, iters=5, bwd=False):
             C.c_void_p(dqkv.data_ptr()), C.c_void_p(dqkv.data_ptr() + 2 * H * D),
             C.c_void_p(dqkv.data_ptr() + 4 * H * D), C.c_int64(3 * H * D), None, C.c_int64(0), S, H, D, sc, None, ms3))
         out["prep_ms"], out["dkdv_ms"], out["dq_ms"] = list(ms3)
-        out["dkdv_tflops"] = 2 * flops / ms3[1] / 1e9
-        out["dq_tflops"] = 1.5 * flops / ms3[2] / 1e9
+        if D == 128 and os.environ.get("MEMO_ATTN_BWD") == "fused":
+            out["fused_tflops_algo"] = 2 * flops / ms3[1] / 1e9  # model bwd FLOPs (4 S^2 h)
+            out["fused_tflops_exec"] = 2.5 * flops / ms3[1] / 1e9  # 5 GEMM units executed
+        else:
+            out["dkdv_tflops"] = 2 * flops / ms3[1] / 1e9
+            out["dq_tflops"] = 1.5 * flops / ms3[2] / 1e9
     return out
 
 
