@@ -70,16 +70,18 @@ __device__ __forceinline__ uint64_t mnmajor_step(uint64_t d, int kk) {
 }
 
 
-// 2^x for x <= 0 on the FMA pipe: cubic on the fraction + exponent insert.
-// Max relative error 1.0e-4 (bf16 P needs 3.9e-3).
+// 2^x for x <= 0 without the MUFU: round-to-nearest via the 1.5*2^23 magic
+// add (no FRND/F2I, which would occupy the same XU pipe as MUFU.EX2), a
+// degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (max rel. error 7.6e-5;
+// bf16 P needs 3.9e-3), and the exponent added in the integer domain.
 __device__ __forceinline__ float exp2_fma(float x) {
-  const float fl = floorf(x);
-  const float f = x - fl;
-  float p = fmaf(f, 0.07826793330191018f, 0.22630764718276575f);
-  p = fmaf(p, f, 0.6954244195153241f);
-  p = fmaf(p, f, 1.0f);
-  const float r = __int_as_float(__float_as_int(p) + (static_cast<int>(fl) << 23));
-  return x < -126.f ? 0.f : r;
+  x = fmaxf(x, -126.f);  // round(x) >= -126 keeps the exponent field of the result >= 0
+  const float j = x + 12582912.f;  // low mantissa bits = round(x)
+  const float f = x - (j - 12582912.f);
+  float p = fmaf(f, 0.05517027f, 0.24260795f);
+  p = fmaf(p, f, 0.6932609f);
+  p = fmaf(p, f, 0.9999283f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
 
 // Each softmax/compute thread writes its own row (D bf16 from global) into
@@ -249,13 +251,15 @@ __global__ void __launch_bounds__(256, 1)
       dev::mbar_wait(&s_full[st], (j >> 1) & 1);
       dev::tc_fence_after();
       float s[128];
+      {
+        uint32_t r[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        dev::tmem_ld32(t_s[st] + lane_off + c * 32, r);
-        dev::tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) dev::tmem_ld32(t_s[st] + lane_off + c * 32, r[c]);
+        dev::tmem_ld_wait_regs(r[0], r[1], r[2], r[3]);  // one wait for all four loads
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);  // raw logits
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[c][i]);  // raw logits
       }
       if (j == qt) {  // diagonal tile: causal mask
 #pragma unroll
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
           dev::tmem_ld32(t_o + lane_off + c * 32, r);
-          dev::tmem_ld_wait();
+          dev::tmem_ld_wait_regs(r);
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
           dev::tmem_st32(t_o + lane_off + c * 32, r);
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int c = 0; c < D / 32; ++c) {
       uint32_t r[32];
       dev::tmem_ld32(t_o + lane_off + c * 32, r);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(r);
       uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -544,7 +548,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
         dev::tmem_ld32(t_s + c * 32, r);
-        dev::tmem_ld_wait();
+        dev::tmem_ld_wait_regs(r);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           float v = __uint_as_float(r[i]);
@@ -571,7 +575,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
         dev::tmem_ld32(t_s + c * 32, r);
-        dev::tmem_ld_wait();
+        dev::tmem_ld_wait_regs(r);
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
           dev::tmem_ld32(t_o + c * 32, r);
-          dev::tmem_ld_wait();
+          dev::tmem_ld_wait_regs(r);
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
           dev::tmem_st32(t_o + c * 32, r);
@@ -615,7 +619,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int c = 0; c < D / 32; ++c) {
       uint32_t r[32];
       dev::tmem_ld32(t_o + c * 32, r);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(r);
       uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -856,7 +860,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           uint32_t sr[32], dr[32];
           dev::tmem_ld32(t_st + c * 32, sr);
           dev::tmem_ld32(t_dpt + c * 32, dr);
-          dev::tmem_ld_wait();
+          dev::tmem_ld_wait_regs(sr, dr);
           uint32_t pp[16], dd[16];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
@@ -901,16 +905,239 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t r32[32];
       float x[32];
       dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(r32);
 #pragma unroll
       for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
       store_grad32(dvrow + c * 32, x, 1.f, nullptr);
       dev::tmem_ld32(t_dk + lane_off + c * 32, r32);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(r32);
 #pragma unroll
       for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
       store_grad32(dkrow + c * 32, x, scale,
                    rope ? rope + (pos0 + kidx) * (D / 2) + c * 16 : nullptr);
+    }
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------ dK/dV, K/V in TMEM
+// Same math as attn_bwd_dkdv_kernel, but K and V (fixed for the CTA) sit in
+// TMEM as the A operands of S^T = K Q^T and dP^T = V dO^T, so those MMAs read
+// only the 32-query B slice from shared memory instead of re-reading the whole
+// K/V tile per step (the SS form at N=64 ran at ~2/3 rate, smem-bound).  The
+// TMEM budget then gives 32-query steps, double-buffered:
+//   [0,128) dV | [128,256) dK | [256,320) K | [320,384) V | [384,448) buf0 | [448,512) buf1
+//   buf: S^T [0,32) | dP^T [32,64); warp ch writes P^T into [16ch,+8), dS^T into [32+16ch,+8)
+// K and V never touch shared memory; the ring holds 3 full Q/dO tiles.
+constexpr int KV_NS = 3;
+constexpr int QSTEP = 32;  // queries per pipeline step
+
+template <int D>
+struct DkdvTmSmem {
+  static constexpr int NC = D / 64;
+  static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
+  static constexpr int RQ_OFF = 0;                             // [KV_NS] Q tiles
+  static constexpr int RD_OFF = KV_NS * TILE_BYTES;            // [KV_NS] dO tiles
+  static constexpr int VEC_OFF = 2 * KV_NS * TILE_BYTES;       // [KV_NS][lse2 128 | delta 128]
+  static constexpr int BAR_OFF = VEC_OFF + KV_NS * 1024;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BWD_THREADS, 1)
+    attn_bwd_dkdv_tm_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
+                            const __grid_constant__ CUtensorMap map_q,
+                            const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                            const float* __restrict__ delta, __nv_bfloat16* __restrict__ dk,
+                            __nv_bfloat16* __restrict__ dv, long long ld, const float2* __restrict__ rope,
+                            long long pos0, int S, int H, float scale, float scale_log2) {
+  using L = DkdvTmSmem<D>;
+  constexpr int NC = L::NC;
+  constexpr int NS = KV_NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* kv_ready = bars + 0;
+  uint64_t* in_full = bars + 1;        // [NS]
+  uint64_t* in_empty = in_full + NS;   // [NS]
+  uint64_t* s_full = in_empty + NS;    // [2]
+  uint64_t* p_ready = s_full + 2;      // [2]
+  uint64_t* fin = p_ready + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  constexpr int CW = 32 * BWD_COMPUTE_WARPS;
+
+  const int n_tiles = S / TILE;
+  const int kt = blockIdx.x;  // key tile
+  const int hh = blockIdx.y;
+  const int n_q = n_tiles - kt;
+  const int n_g = n_q * (TILE / QSTEP);
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_do);
+    dev::mbar_init(kv_ready, CW);
+    for (int s2 = 0; s2 < NS; ++s2) {
+      dev::mbar_init(&in_full[s2], 1);
+      dev::mbar_init(&in_empty[s2], 1);
+    }
+    for (int s2 = 0; s2 < 2; ++s2) {
+      dev::mbar_init(&s_full[s2], 1);
+      dev::mbar_init(&p_ready[s2], CW);
+    }
+    dev::mbar_init(fin, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dv = tmem, t_dk = tmem + 128, t_k = tmem + 256, t_v = tmem + 320;
+  auto buf = [&](int b) { return tmem + 384 + 64 * b; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < n_q; ++i) {
+        const int qt = kt + i, st = i % NS;
+        dev::mbar_wait(&in_empty[st], ((i / NS) & 1) ^ 1);
+        dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::RQ_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q, &in_full[st],
+                           hh * D + c * 64, qt * TILE);
+          dev::tma_load_2d(smem + L::RD_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_do, &in_full[st],
+                           hh * D + c * 64, qt * TILE);
+        }
+        float* vec = reinterpret_cast<float*>(smem + L::VEC_OFF + st * 1024);
+        const long long off = static_cast<long long>(hh) * S + qt * TILE;
+        dev::bulk_load(vec, lse2 + off, 512, &in_full[st]);
+        dev::bulk_load(vec + 128, delta + off, 512, &in_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    {  // whole warp, converged: MMAs/commits elect one lane
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, QSTEP, false, false);
+      constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
+      dev::mbar_wait_w(kv_ready, 0);
+      dev::tc_fence_after();
+      auto issue_sd = [&](int g) {
+        const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+        if (qq == 0) {
+          dev::mbar_wait_w(&in_full[st], (i / NS) & 1);
+          dev::tc_fence_after();
+        }
+        const uint32_t roff = qq * QSTEP * 128;  // 32 rows of 128 B inside every 64-col chunk
+        const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
+        const uint64_t dod = kmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ts_w(buf(b), t_k + kk * 8, kmajor_step(qd, kk), idesc_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ts_w(buf(b) + 32, t_v + kk * 8, kmajor_step(dod, kk), idesc_s, kk > 0);
+        dev::mma_commit_w(&s_full[b]);
+      };
+      issue_sd(0);
+      for (int g = 0; g < n_g; ++g) {
+        if (g + 1 < n_g) issue_sd(g + 1);
+        const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+        dev::mbar_wait_w(&p_ready[b], (g >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t roff = qq * QSTEP * 128;
+        const uint64_t qm = mnmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
+        const uint64_t dom = mnmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
+#pragma unroll
+        for (int kk = 0; kk < QSTEP / 16; ++kk)
+          dev::mma_bf16_ts_w(t_dv, buf(b) + 16 * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
+#pragma unroll
+        for (int kk = 0; kk < QSTEP / 16; ++kk)
+          dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + 16 * kk, mnmajor_step(qm, kk), idesc_g, (g | kk) != 0);
+        if (qq == 3) dev::mma_commit_w(&in_empty[st]);
+      }
+      dev::mma_commit_w(fin);
+    }
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int ch = (warp - 4) >> 2;  // 16-query slice of each 32-query step
+    const int r = q4 * 32 + lane;    // key row in tile
+    const int kidx = kt * TILE + r;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const long long hcols = static_cast<long long>(H) * D;
+    // K (ch 0) / V (ch 1) row r -> TMEM A operand
+    row_to_tmem<D>((ch == 0 ? kg : vg) + kidx * hcols + hh * D, (ch == 0 ? t_k : t_v) + lane_off);
+    dev::tmem_st_wait();
+    dev::tc_fence_before();
+    dev::mbar_arrive(kv_ready);
+    for (int g = 0; g < n_g; ++g) {
+      const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+      const bool diag = i == 0;
+      if (qq == 0) dev::mbar_wait(&in_full[st], (i / NS) & 1);
+      const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + 16 * ch) * 4;
+      const uint32_t dl = l2 + 512;
+      dev::mbar_wait(&s_full[b], (g >> 1) & 1);
+      dev::tc_fence_after();
+      uint32_t sr[16], dr[16];
+      dev::tmem_ld16(buf(b) + lane_off + 16 * ch, sr);
+      dev::tmem_ld16(buf(b) + lane_off + 32 + 16 * ch, dr);
+      dev::tmem_ld_wait_regs(sr, dr);
+      uint32_t pp[8], dd[8];
+      auto body = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 lv = dev::lds_f4(l2 + 16 * j4);
+          const float4 dv4 = dev::lds_f4(dl + 16 * j4);
+          const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
+          const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+          float p4[4], d4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float p = dev::ex2(__uint_as_float(sr[4 * j4 + e]) * scale_log2 - lq[e]);
+            if (DIAG && qq * QSTEP + 16 * ch + 4 * j4 + e < r) p = 0.f;
+            p4[e] = p;
+            d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) - dq4[e]);
+          }
+          pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
+          pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
+          dd[2 * j4] = dev::pack_bf16(d4[0], d4[1]);
+          dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
+        }
+      };
+      if (diag)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
+      dev::tmem_st8(buf(b) + lane_off + 16 * ch, pp);
+      dev::tmem_st8(buf(b) + lane_off + 32 + 16 * ch, dd);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_ready[b]);
+    }
+    dev::mbar_wait(fin, 0);
+    dev::tc_fence_after();
+    __nv_bfloat16* dvrow = dv + static_cast<long long>(kidx) * ld + hh * D;
+    __nv_bfloat16* dkrow = dk + static_cast<long long>(kidx) * ld + hh * D;
+#pragma unroll 1
+    for (int c = ch * (D / 64); c < (ch + 1) * (D / 64); ++c) {
+      uint32_t r32[32];
+      float x[32];
+      dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
+      dev::tmem_ld_wait_regs(r32);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dvrow + c * 32, x, 1.f, nullptr);
+      dev::tmem_ld32(t_dk + lane_off + c * 32, r32);
+      dev::tmem_ld_wait_regs(r32);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dkrow + c * 32, x, scale, rope ? rope + (pos0 + kidx) * (D / 2) + c * 16 : nullptr);
     }
     dev::tc_fence_before();
   }
@@ -1083,7 +1310,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           uint32_t sr[32], dr[32];
           dev::tmem_ld32(t_s + c * 32, sr);
           dev::tmem_ld32(t_dp + c * 32, dr);
-          dev::tmem_ld_wait();
+          dev::tmem_ld_wait_regs(sr, dr);
           uint32_t dd[16];
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
@@ -1118,7 +1345,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t r32[32];
       float x[32];
       dev::tmem_ld32(t_dq + lane_off + c * 32, r32);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(r32);
 #pragma unroll
       for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
       store_grad32(dqrow + c * 32, x, scale,
@@ -1399,7 +1626,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       dev::tc_fence_after();
       uint32_t x[32];
       dev::tmem_ld32(t_dq + lane_off + 32 * ch, x);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(x);
       dev::tc_fence_before();
       dev::mbar_arrive(&dq_free[b]);
       // staging buffer g % FB_NSTG was last read by the bulk reduce of g - FB_NSTG
@@ -1423,7 +1650,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t sr[32], dr[32];
       dev::tmem_ld32(t_s(b) + lane_off + 32 * ch, sr);
       dev::tmem_ld32(t_dp + lane_off + 32 * ch, dr);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(sr, dr);
       dev::tc_fence_before();
       dev::mbar_arrive(&dp_free[b]);
       uint32_t pp[16], dd[16];
@@ -1479,12 +1706,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       uint32_t r32[32];
       float x[32];
       dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(r32);
 #pragma unroll
       for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
       store_grad32(dvrow + c * 32, x, 1.f, nullptr);
       dev::tmem_ld32(t_dk + lane_off + c * 32, r32);
-      dev::tmem_ld_wait();
+      dev::tmem_ld_wait_regs(r32);
 #pragma unroll
       for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
       store_grad32(dkrow + c * 32, x, scale, rope ? rope + (pos0 + kidx) * (D / 2) + c * 16 : nullptr);
@@ -1621,6 +1848,8 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   std::call_once(f, [] {
     cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1636,9 +1865,18 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   dim3 grid(a.S / TILE, a.H);
   if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
-  attn_bwd_dkdv_kernel<D><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
-      mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
-      scale_log2);
+  static const bool dkdv_smem = [] {  // MEMO_ATTN_DKDV=smem: K/V as shared-memory operands (ablation)
+    const char* e = getenv("MEMO_ATTN_DKDV");
+    return e && std::string(e) == "smem";
+  }();
+  if (dkdv_smem)
+    attn_bwd_dkdv_kernel<D><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
+        mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
+        scale_log2);
+  else
+    attn_bwd_dkdv_tm_kernel<D><<<grid, BWD_THREADS, DkdvTmSmem<D>::BYTES, stream>>>(
+        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+        scale_log2);
   if (a.ev[2]) cudaEventRecord(a.ev[2], stream);
   static const int dbg = [] {
     const char* e = getenv("MEMO_ATTN_DEBUG");

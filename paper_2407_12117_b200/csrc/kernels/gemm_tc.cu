@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         dev::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * BN + c * 32, r);
-        dev::tmem_ld_wait();
+        dev::tmem_ld_wait_regs(r);
         float x[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
