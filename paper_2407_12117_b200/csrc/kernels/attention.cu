@@ -366,6 +366,295 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 
+// ------------------------------------------------------------------ forward, split rows
+// Same pipeline as attn_fwd_kernel (Q in TMEM, double-buffered S, P over S),
+// but every query row is shared by two softmax warps on the same SMSP (warps
+// w and w+4 own columns [0,64) and [64,128) of the key tile).  The single
+// softmax warp per SMSP was the critical path (~1.8k clk per tile against
+// 1024 clk of MMA); two warps interleave their dependency chains.  The row
+// max is exchanged through shared memory behind a 64-thread named barrier,
+// each warp keeps its own partial row sum (combined once in the epilogue),
+// FFMA2/FADD2 process column pairs, and a quarter of the exponentials run on
+// the FMA pipe (exp2_fma) to keep MUFU below the MMA time.
+struct Fwd2wSmem {
+  static constexpr int TILE_BYTES = 2 * CHUNK_BYTES;  // D = 128
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + FWD_STAGES * TILE_BYTES;
+  static constexpr int X_OFF = V_OFF + FWD_STAGES * TILE_BYTES;  // [2 parity][2 half][128] f32
+  static constexpr int BAR_OFF = X_OFF + 2 * 2 * 128 * 4;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  return (static_cast<uint64_t>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, float b, float c) {  // a * b + c (b, c broadcast)
+  uint64_t r;
+  const uint64_t bb = f2_pack(b, b), cc = f2_pack(c, c);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(bb), "l"(cc));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <bool EMU>
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_2w_kernel(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
+                       float* __restrict__ lse, int S, int H, float scale_log2) {
+  constexpr int D = 128;
+  using L = Fwd2wSmem;
+  constexpr int NC = 2;
+  constexpr int NS = FWD_STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_ready = bars + 0;
+  uint64_t* k_full = bars + 1;        // [NS]
+  uint64_t* k_empty = k_full + NS;    // [NS]
+  uint64_t* v_full = k_empty + NS;    // [NS]
+  uint64_t* v_empty = v_full + NS;    // [NS]
+  uint64_t* s_full = v_empty + NS;    // [2]
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* o_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  const uint32_t xchg_s = dev::smem_u32(smem + L::X_OFF);
+
+  const int n_tiles = S / TILE;
+  const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
+  const int hh = blockIdx.y;
+  const int n_kv = qt + 1;
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_k);
+    dev::tma_prefetch_desc(&map_v);
+    dev::mbar_init(q_ready, 256);
+    for (int s = 0; s < NS; ++s) {
+      dev::mbar_init(&k_full[s], 1);
+      dev::mbar_init(&k_empty[s], 1);
+      dev::mbar_init(&v_full[s], 1);
+      dev::mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      dev::mbar_init(&s_full[s], 1);
+      dev::mbar_init(&p_full[s], 256);
+    }
+    dev::mbar_init(o_done, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s[2] = {tmem, tmem + 128};
+  const uint32_t t_o = tmem + 256;
+  const uint32_t t_q = tmem + 256 + D;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % NS;
+        const uint32_t ph = (j / NS) & 1;
+        uint8_t* sk = smem + L::K_OFF + st * L::TILE_BYTES;
+        uint8_t* sv = smem + L::V_OFF + st * L::TILE_BYTES;
+        dev::mbar_wait(&k_empty[st], ph ^ 1);
+        dev::mbar_expect_tx(&k_full[st], L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c)
+          dev::tma_load_2d(sk + c * CHUNK_BYTES, &map_k, &k_full[st], hh * D + c * 64, j * TILE);
+        dev::mbar_wait(&v_empty[st], ph ^ 1);
+        dev::mbar_expect_tx(&v_full[st], L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c)
+          dev::tma_load_2d(sv + c * CHUNK_BYTES, &map_v, &v_full[st], hh * D + c * 64, j * TILE);
+      }
+    }
+  } else if (warp == 1) {
+    {  // whole warp, converged: MMAs/commits elect one lane
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
+      dev::mbar_wait_w(q_ready, 0);
+      dev::tc_fence_after();
+      auto issue_s = [&](int j) {
+        const int st = j % NS;
+        dev::mbar_wait_w(&k_full[st], (j / NS) & 1);
+        dev::tc_fence_after();
+        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ts_w(t_s[j & 1], t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
+        dev::mma_commit_w(&s_full[j & 1]);
+        dev::mma_commit_w(&k_empty[st]);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_s(j + 1);
+        const int st = j % NS;
+        dev::mbar_wait_w(&p_full[j & 1], (j >> 1) & 1);
+        dev::mbar_wait_w(&v_full[st], (j / NS) & 1);
+        dev::tc_fence_after();
+        const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
+        // P of keys [0,64) sits in S cols [0,32), keys [64,128) in cols [64,96)
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ts_w(t_o, t_s[j & 1] + 8 * kk + 32 * (kk >> 2), mnmajor_step(vd, kk), idesc_o,
+                             (j | kk) != 0);
+        dev::mma_commit_w(o_done);
+        dev::mma_commit_w(&v_empty[st]);
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int hf = (warp - 4) >> 2;  // column half of the key tile (and of D for O)
+    const int row = q4 * 32 + lane;
+    const int qidx = qt * TILE + row;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const int bar_id = 1 + q4;       // warps w and w+4 (same rows)
+    {  // Q row elements [64hf, 64hf+64) -> TMEM cols [32hf, 32hf+32)
+      const uint4* s4 = reinterpret_cast<const uint4*>(q + static_cast<long long>(qidx) * H * D + hh * D + 64 * hf);
+      uint32_t r[32];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = s4[i];
+        r[4 * i + 0] = v.x;
+        r[4 * i + 1] = v.y;
+        r[4 * i + 2] = v.z;
+        r[4 * i + 3] = v.w;
+      }
+      dev::tmem_st32(t_q + lane_off + 32 * hf, r);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(q_ready);
+    }
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      dev::mbar_wait(&s_full[st], (j >> 1) & 1);
+      dev::tc_fence_after();
+      uint32_t r[2][32];
+      dev::tmem_ld32(t_s[st] + lane_off + 64 * hf, r[0]);
+      dev::tmem_ld32(t_s[st] + lane_off + 64 * hf + 32, r[1]);
+      dev::tmem_ld_wait_regs(r[0], r[1]);
+      if (j == qt) {  // diagonal tile: causal mask
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (64 * hf + i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
+      }
+      float mx8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(r[0][k]);
+#pragma unroll
+      for (int i = 8; i < 64; i += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(r[i >> 5][(i & 31) + k]));
+#pragma unroll
+      for (int k = 4; k > 0; k >>= 1)
+#pragma unroll
+        for (int q2 = 0; q2 < k; ++q2) mx8[q2] = fmaxf(mx8[q2], mx8[q2 + k]);
+      // row max across the two halves (explicit ld/st.shared: a generic
+      // pointer here compiles to LD.E/ST.E on the global path)
+      const uint32_t xp = xchg_s + (j & 1) * 1024;
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xp + (hf * 128 + row) * 4), "f"(mx8[0]) : "memory");
+      named_bar(bar_id, 64);
+      float other;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xp + ((hf ^ 1) * 128 + row) * 4) : "memory");
+      const float mx = fmaxf(mx8[0], other) * scale_log2;
+      const float cand = fmaxf(m, mx);
+      const bool need = j == 0 || cand > m + kRescaleThreshold;
+      const bool any = __any_sync(0xffffffffu, need);  // same rows, same vote in both warps
+      float factor = 1.f;
+      float m_new = m;
+      if (any) {
+        m_new = cand;
+        factor = j == 0 ? 0.f : dev::ex2(m - m_new);
+      }
+      uint64_t sum4[4] = {0, 0, 0, 0};
+      uint32_t p[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                          __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
+                                  scale_log2, -m_new);
+        float a, b;
+        if (EMU && (i & 3) == 3) {
+          a = exp2_fma(f2_lo(x2));
+          b = exp2_fma(f2_hi(x2));
+        } else {
+          a = dev::ex2(f2_lo(x2));
+          b = dev::ex2(f2_hi(x2));
+        }
+        sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
+        p[i] = dev::pack_bf16(a, b);
+      }
+      const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+      l = l * factor + (f2_lo(s01) + f2_hi(s01));
+      m = m_new;
+      dev::tmem_st32(t_s[st] + lane_off + 64 * hf, p);  // inside this warp's own columns
+      if (any && j > 0) {
+        // O must hold P(j-1)V(j-1) before it is rescaled; this warp owns D cols [64hf, 64hf+64)
+        dev::mbar_wait(o_done, (j - 1) & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t o[32];
+          dev::tmem_ld32(t_o + lane_off + 64 * hf + 32 * c, o);
+          dev::tmem_ld_wait_regs(o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+          dev::tmem_st32(t_o + lane_off + 64 * hf + 32 * c, o);
+        }
+      }
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_full[st]);
+    }
+    // epilogue: combine the two partial row sums, write O columns [64hf, 64hf+64) and the LSE
+    const uint32_t xp = xchg_s + (n_kv & 1) * 1024;
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(xp + (hf * 128 + row) * 4), "f"(l) : "memory");
+    named_bar(bar_id, 64);
+    float l_other;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(l_other) : "r"(xp + ((hf ^ 1) * 128 + row) * 4) : "memory");
+    const float lt = l + l_other;
+    dev::mbar_wait(o_done, (n_kv - 1) & 1);
+    dev::tc_fence_after();
+    const float inv = 1.f / lt;
+    __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D + 64 * hf;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      dev::tmem_ld32(t_o + lane_off + 64 * hf + 32 * c, o);
+      dev::tmem_ld_wait_regs(o);
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 u;
+        u.x = dev::pack_bf16(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
+        u.y = dev::pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
+        u.z = dev::pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
+        u.w = dev::pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
+        dst[i] = u;
+      }
+    }
+    if (hf == 0) lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(lt)) * kLn2;
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ forward, 2 query tiles
 // Two adjacent query tiles (2p, 2p+1) of one head share every K/V tile load,
 // halving the L2->SMEM streaming that bounds the 1-tile kernel, and their
@@ -1917,7 +2206,7 @@ void launch_fwd(const AttnFwdArgs& a, const CUtensorMap& mq, const CUtensorMap& 
 int fwd_variant() {
   static int v = [] {
     const char* e = getenv("MEMO_ATTN_FWD_VARIANT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 5;
   }();
   return v;
 }
@@ -1932,8 +2221,18 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   const float scale_log2 = a.softmax_scale * kLog2e;
   if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
-  const int v = fwd_variant();  // bit0: Q in TMEM, bit1: FMA exp2 share, 4: 2-tile kernel
-  if (v >= 4 && a.S % (2 * TILE) == 0) {
+  const int v = fwd_variant();  // 0-3: bit0 Q in TMEM, bit1 FMA exp2 share; 4: 2-tile; 5: split rows
+  if ((v == 5 || v == 6) && a.D != 128) {
+    launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
+  } else if (v == 5 || v == 6) {  // 6: without the FMA-pipe exp2 share
+    static std::once_flag f5;
+    std::call_once(f5, [] {
+      cudaFuncSetAttribute(attn_fwd_2w_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_2w_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
+    });
+    auto kern = v == 5 ? attn_fwd_2w_kernel<true> : attn_fwd_2w_kernel<false>;
+    kern<<<dim3(a.S / TILE, a.H), 384, Fwd2wSmem::BYTES, stream>>>(a.q, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
+  } else if (v == 4 && a.S % (2 * TILE) == 0) {
     dim3 grid2(a.S / (2 * TILE), a.H);
     if (a.D == 128) {
       static std::once_flag f2;

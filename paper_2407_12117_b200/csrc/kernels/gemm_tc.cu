@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread)
+    {
+      // ---------------- MMA issuer: whole warp converged, elect.sync picks the issuing lane
       constexpr uint32_t idesc = dev::idesc_bf16_f32(BM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -240,11 +240,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int buf = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
-        dev::mbar_wait(&tempty_bar[buf], acc_phase ^ 1);
+        dev::mbar_wait_w(&tempty_bar[buf], acc_phase ^ 1);
         dev::tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
-          dev::mbar_wait(&full_bar[stage], phase);
+          dev::mbar_wait_w(&full_bar[stage], phase);
           dev::tc_fence_after();
           const uint32_t sa = dev::smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_TILE_BYTES;
@@ -255,15 +255,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // only the start-address field moves with k (16-byte units)
             const uint64_t ad = ad0 + static_cast<uint64_t>((A_MN ? k * 2048 : k * 32) >> 4);
             const uint64_t bd = bd0 + static_cast<uint64_t>((B_MN ? k * 2048 : k * 32) >> 4);
-            dev::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            dev::mma_bf16_ss_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          dev::mma_commit(&empty_bar[stage]);
+          dev::mma_commit_w(&empty_bar[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        dev::mma_commit(&tfull_bar[buf]);
+        dev::mma_commit_w(&tfull_bar[buf]);
       }
     }
   } else {
