@@ -358,7 +358,8 @@ def main():
     achieved = dk["flops"] / dk["count"] / (dk["ms"] / dk["count"] * 1e-3) / 1e12 if dk["count"] else None
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+        # DRAM bytes of one launch at the bench shape, from the committed `ncu --set full` capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             traffic = json.load(f).get("attn_bwd_dkdv", {}).get("dram_bytes_per_launch")
     except OSError:
         pass

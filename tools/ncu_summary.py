@@ -26,6 +26,9 @@ METRICS = {
     "smsp__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_inst_pct",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_pct",
+    "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active": "tc_pipe_pct",
+    "sm__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
 }
 
 
