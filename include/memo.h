@@ -202,12 +202,21 @@ int memo_attn_bwd(const void* q, const void* k, const void* v, const void* o, co
                   const void* rope, int64_t pos0, int32_t S, int32_t H, int32_t D,
                   float softmax_scale, void* stream);
 /* As memo_attn_bwd; synchronises and writes the device ms of its three phases
- * (delta prep, main kernel — fused dK/dV/dQ at D=128, dK/dV at D=64 — and dQ
- * finish: f32->bf16 conversion at D=128, the dQ kernel at D=64) to ms3. */
+ * (delta prep, dK/dV, dQ) to ms3.  With MEMO_ATTN_BWD=fused (D=128 ablation)
+ * the second is the fused dK/dV/dQ kernel and the third its f32->bf16 dQ pass. */
 int memo_attn_bwd_timed(const void* q, const void* k, const void* v, const void* o,
                         const float* lse, const void* dout, float* delta, void* dq, void* dk,
                         void* dv, int64_t ld_dqkv, const void* rope, int64_t pos0, int32_t S,
                         int32_t H, int32_t D, float softmax_scale, void* stream, float* ms3);
+
+/* RMSNorm backward of y = (x + a) * rsqrt(mean((x + a)^2) + eps) * g (f32
+ * residual x [S, h], optional bf16 addend a, bf16 g [h], f32 dy): dx = dres +
+ * d(x+a) (f32, may alias dres), optional bf16 copy, dg (=|+=) sum over rows in
+ * a fixed order.  partial is an f32 workspace of memo_rmsnorm_bwd_partials(S)*h. */
+int32_t memo_rmsnorm_bwd_partials(int32_t S);
+int memo_rmsnorm_bwd(const float* x, const void* a, const void* g, const float* dy,
+                     const float* dres, float* dx, void* dx_bf16, float* partial, float* dg,
+                     int32_t S, int32_t h, float eps, int32_t accumulate_dg, void* stream);
 
 /* ---------------------------------------------------------------- executor
  * The real training step that replaces the reference's simulated executor

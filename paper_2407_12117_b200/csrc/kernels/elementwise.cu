@@ -234,6 +234,93 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(
   }
 }
 
+// Same contract, one HBM pass: a 256-thread block owns NORM_BWD_ROWS rows and
+// every thread a fixed slice of 4*V consecutive columns (h = 1024*V), so the
+// row (x, a, dy, dres) stays in registers between the reduction and the
+// output, g is loaded once, and the dg accumulators live in registers.  The
+// per-row (sum x^2, sum dy*g*x) reduction goes warp-shuffle -> 8 partials in
+// shared memory read back in fixed order (deterministic).
+template <int V>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_reg_kernel(
+    const float* __restrict__ x, const __nv_bfloat16* __restrict__ a,
+    const __nv_bfloat16* __restrict__ g, const float* __restrict__ dy, const float* dres,
+    float* dx, __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ partial, int S, float eps) {
+  constexpr int h = 1024 * V;
+  __shared__ float red[2][2][8];  // [row parity][ss|dot][warp]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = threadIdx.x * 4;  // columns c0 + 1024*v .. +3
+  float gg[V][4], acc[V][4];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    load_bf16x4(g + c0 + 1024 * v, gg[v]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[v][e] = 0.f;
+  }
+  const int row0 = blockIdx.x * NORM_BWD_ROWS;
+  for (int rr = 0; rr < NORM_BWD_ROWS; ++rr) {
+    const int row = row0 + rr;
+    if (row >= S) break;
+    const long long base = static_cast<long long>(row) * h + c0;
+    float xv[V][4], dv[V][4];
+    float ss = 0.f, dot = 0.f;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const float4 t = *reinterpret_cast<const float4*>(x + base + 1024 * v);
+      const float4 d = *reinterpret_cast<const float4*>(dy + base + 1024 * v);
+      xv[v][0] = t.x; xv[v][1] = t.y; xv[v][2] = t.z; xv[v][3] = t.w;
+      dv[v][0] = d.x; dv[v][1] = d.y; dv[v][2] = d.z; dv[v][3] = d.w;
+      if (a) {
+        float f[4];
+        load_bf16x4(a + base + 1024 * v, f);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) xv[v][e] += f[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        ss += xv[v][e] * xv[v][e];
+        dot += dv[v][e] * gg[v][e] * xv[v][e];
+      }
+    }
+    ss = warp_sum(ss);
+    dot = warp_sum(dot);
+    const int par = rr & 1;
+    if (lane == 0) {
+      red[par][0][warp] = ss;
+      red[par][1][warp] = dot;
+    }
+    __syncthreads();  // the other parity buffer makes one barrier per row enough
+    ss = 0.f;
+    dot = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      ss += red[par][0][w];
+      dot += red[par][1][w];
+    }
+    const float r = rsqrtf(ss / static_cast<float>(h) + eps);
+    const float c = r * r * r * dot / static_cast<float>(h);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float rv[4] = {0.f, 0.f, 0.f, 0.f};
+      if (dres) {
+        const float4 q = *reinterpret_cast<const float4*>(dres + base + 1024 * v);
+        rv[0] = q.x; rv[1] = q.y; rv[2] = q.z; rv[3] = q.w;
+      }
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        o[e] = rv[e] + (r * dv[v][e] * gg[v][e] - c * xv[v][e]);
+        acc[v][e] += dv[v][e] * xv[v][e] * r;
+      }
+      *reinterpret_cast<float4*>(dx + base + 1024 * v) = make_float4(o[0], o[1], o[2], o[3]);
+      if (dx_bf16) store_bf16x4(dx_bf16 + base + 1024 * v, o[0], o[1], o[2], o[3]);
+    }
+  }
+  float* prow = partial + static_cast<long long>(blockIdx.x) * h + c0;
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    *reinterpret_cast<float4*>(prow + 1024 * v) = make_float4(acc[v][0], acc[v][1], acc[v][2], acc[v][3]);
+}
+
 // dg[j] (=|+=) sum_p partial[p][j] in fixed order.
 __global__ void dg_reduce_kernel(const float* __restrict__ partial, float* __restrict__ dg, int P,
                                  int h, int accumulate) {
@@ -608,7 +695,19 @@ cudaError_t rmsnorm_bwd(const float* x, const __nv_bfloat16* a, const __nv_bfloa
                          200 * 1024);
     attr = true;
   }
-  rmsnorm_bwd_kernel<<<P, 256, smem, st>>>(x, a, g, dy, dres, dx, dx_bf16, partial, S, h, eps);
+  switch (h) {  // register-resident single-pass variant for the model widths
+    case 4096:
+      rmsnorm_bwd_reg_kernel<4><<<P, 256, 0, st>>>(x, a, g, dy, dres, dx, dx_bf16, partial, S, eps);
+      break;
+    case 5120:
+      rmsnorm_bwd_reg_kernel<5><<<P, 256, 0, st>>>(x, a, g, dy, dres, dx, dx_bf16, partial, S, eps);
+      break;
+    case 8192:
+      rmsnorm_bwd_reg_kernel<8><<<P, 256, 0, st>>>(x, a, g, dy, dres, dx, dx_bf16, partial, S, eps);
+      break;
+    default:
+      rmsnorm_bwd_kernel<<<P, 256, smem, st>>>(x, a, g, dy, dres, dx, dx_bf16, partial, S, h, eps);
+  }
   dg_reduce_kernel<<<(h + 255) / 256, 256, 0, st>>>(partial, dg, P, h, accumulate_dg);
   return cudaGetLastError();
 }

@@ -5,6 +5,7 @@
 
 #include "host/status.hpp"
 #include "kernels/attention.h"
+#include "kernels/elementwise.h"
 #include "kernels/gemm_tc.h"
 #include "memo.h"
 
@@ -108,5 +109,18 @@ extern "C" int memo_attn_bwd_timed(const void* q, const void* k, const void* v, 
     for (auto& x : ev) cudaEventDestroy(x);
   if (e != cudaSuccess)
     return set_error(MEMO_ERR_INTERNAL, std::string("memo_attn_bwd: ") + cudaGetErrorString(e));
+  return MEMO_OK;
+}
+
+extern "C" int32_t memo_rmsnorm_bwd_partials(int32_t S) { return memo::rmsnorm_bwd_partials(S); }
+
+extern "C" int memo_rmsnorm_bwd(const float* x, const void* a, const void* g, const float* dy,
+                                const float* dres, float* dx, void* dx_bf16, float* partial, float* dg,
+                                int32_t S, int32_t h, float eps, int32_t accumulate_dg, void* stream) {
+  cudaError_t e = memo::rmsnorm_bwd(x, static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(g),
+                                    dy, dres, dx, static_cast<__nv_bfloat16*>(dx_bf16), partial, dg, S, h, eps,
+                                    accumulate_dg != 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess)
+    return set_error(MEMO_ERR_INTERNAL, std::string("memo_rmsnorm_bwd: ") + cudaGetErrorString(e));
   return MEMO_OK;
 }
