@@ -405,7 +405,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <bool EMU>
+template <int EMU_EVERY>  // 0: all exps on MUFU; n: every n-th column pair on the FMA pipe
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_2w_kernel(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   dev::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s[2] = {tmem, tmem + 128};
+  auto t_s = [&](int b) { return tmem + 128 * b; };  // S buffers (no indexed array: it lands in local memory)
   const uint32_t t_o = tmem + 256;
   const uint32_t t_q = tmem + 256 + D;
 
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ts_w(t_s[j & 1], t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
+          dev::mma_bf16_ts_w(t_s(j & 1), t_q + kk * 8, kmajor_step(kd, kk), idesc_s, kk > 0);
         dev::mma_commit_w(&s_full[j & 1]);
         dev::mma_commit_w(&k_empty[st]);
       };
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(384, 1)
         // P of keys [0,64) sits in S cols [0,32), keys [64,128) in cols [64,96)
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts_w(t_o, t_s[j & 1] + 8 * kk + 32 * (kk >> 2), mnmajor_step(vd, kk), idesc_o,
+          dev::mma_bf16_ts_w(t_o, t_s(j & 1) + 8 * kk + 32 * (kk >> 2), mnmajor_step(vd, kk), idesc_o,
                              (j | kk) != 0);
         dev::mma_commit_w(o_done);
         dev::mma_commit_w(&v_empty[st]);
@@ -542,64 +542,75 @@ __global__ void __launch_bounds__(384, 1)
       dev::mbar_wait(&s_full[st], (j >> 1) & 1);
       dev::tc_fence_after();
       uint32_t r[2][32];
-      dev::tmem_ld32(t_s[st] + lane_off + 64 * hf, r[0]);
-      dev::tmem_ld32(t_s[st] + lane_off + 64 * hf + 32, r[1]);
+      dev::tmem_ld32(t_s(st) + lane_off + 64 * hf, r[0]);
+      dev::tmem_ld32(t_s(st) + lane_off + 64 * hf + 32, r[1]);
       dev::tmem_ld_wait_regs(r[0], r[1]);
-      if (j == qt) {  // diagonal tile: causal mask
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (64 * hf + i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
-      }
-      float mx8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(r[0][k]);
-#pragma unroll
-      for (int i = 8; i < 64; i += 8)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(r[i >> 5][(i & 31) + k]));
-#pragma unroll
-      for (int k = 4; k > 0; k >>= 1)
-#pragma unroll
-        for (int q2 = 0; q2 < k; ++q2) mx8[q2] = fmaxf(mx8[q2], mx8[q2 + k]);
-      // row max across the two halves (explicit ld/st.shared: a generic
-      // pointer here compiles to LD.E/ST.E on the global path)
-      const uint32_t xp = xchg_s + (j & 1) * 1024;
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xp + (hf * 128 + row) * 4), "f"(mx8[0]) : "memory");
-      named_bar(bar_id, 64);
-      float other;
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xp + ((hf ^ 1) * 128 + row) * 4) : "memory");
-      const float mx = fmaxf(mx8[0], other) * scale_log2;
-      const float cand = fmaxf(m, mx);
-      const bool need = j == 0 || cand > m + kRescaleThreshold;
-      const bool any = __any_sync(0xffffffffu, need);  // same rows, same vote in both warps
+      bool any = false;
       float factor = 1.f;
-      float m_new = m;
-      if (any) {
-        m_new = cand;
-        factor = j == 0 ? 0.f : dev::ex2(m - m_new);
-      }
-      uint64_t sum4[4] = {0, 0, 0, 0};
       uint32_t p[32];
+      // The causal mask only exists on the diagonal tile; a separate
+      // instantiation keeps the compiler from if-converting it into a
+      // compare+select per element on every tile.
+      auto tile = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+        if (DIAG) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
-                                          __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
-                                  scale_log2, -m_new);
-        float a, b;
-        if (EMU && (i & 3) == 3) {
-          a = exp2_fma(f2_lo(x2));
-          b = exp2_fma(f2_hi(x2));
-        } else {
-          a = dev::ex2(f2_lo(x2));
-          b = dev::ex2(f2_hi(x2));
+          for (int i = 0; i < 64; ++i)
+            if (64 * hf + i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
         }
-        sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
-        p[i] = dev::pack_bf16(a, b);
-      }
-      const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
-      l = l * factor + (f2_lo(s01) + f2_hi(s01));
-      m = m_new;
-      dev::tmem_st32(t_s[st] + lane_off + 64 * hf, p);  // inside this warp's own columns
+        float mx8[8];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = __uint_as_float(r[0][k2]);
+#pragma unroll
+        for (int i = 8; i < 64; i += 8)
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(mx8[k2], __uint_as_float(r[i >> 5][(i & 31) + k2]));
+#pragma unroll
+        for (int k2 = 4; k2 > 0; k2 >>= 1)
+#pragma unroll
+          for (int q2 = 0; q2 < k2; ++q2) mx8[q2] = fmaxf(mx8[q2], mx8[q2 + k2]);
+        // row max across the two halves (explicit ld/st.shared: a generic
+        // pointer here compiles to LD.E/ST.E on the global path)
+        const uint32_t xp = xchg_s + (j & 1) * 1024;
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xp + (hf * 128 + row) * 4), "f"(mx8[0]) : "memory");
+        named_bar(bar_id, 64);
+        float other;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xp + ((hf ^ 1) * 128 + row) * 4) : "memory");
+        const float mx = fmaxf(mx8[0], other) * scale_log2;
+        const float cand = fmaxf(m, mx);
+        const bool need = j == 0 || cand > m + kRescaleThreshold;
+        any = __any_sync(0xffffffffu, need);  // same rows, same vote in both warps
+        float m_new = m;
+        if (any) {
+          m_new = cand;
+          factor = j == 0 ? 0.f : dev::ex2(m - m_new);
+        }
+        uint64_t sum4[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                            __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
+                                    scale_log2, -m_new);
+          float a, b;
+          if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
+            a = exp2_fma(f2_lo(x2));
+            b = exp2_fma(f2_hi(x2));
+          } else {
+            a = dev::ex2(f2_lo(x2));
+            b = dev::ex2(f2_hi(x2));
+          }
+          sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
+          p[i] = dev::pack_bf16(a, b);
+        }
+        const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+        l = l * factor + (f2_lo(s01) + f2_hi(s01));
+        m = m_new;
+      };
+      if (j == qt)
+        tile(std::true_type{});
+      else
+        tile(std::false_type{});
+      dev::tmem_st32(t_s(st) + lane_off + 64 * hf, p);  // inside this warp's own columns
       if (any && j > 0) {
         // O must hold P(j-1)V(j-1) before it is rescaled; this warp owns D cols [64hf, 64hf+64)
         dev::mbar_wait(o_done, (j - 1) & 1);
@@ -2222,15 +2233,16 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   const float scale_log2 = a.softmax_scale * kLog2e;
   if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
   const int v = fwd_variant();  // 0-3: bit0 Q in TMEM, bit1 FMA exp2 share; 4: 2-tile; 5: split rows
-  if ((v == 5 || v == 6) && a.D != 128) {
+  if ((v == 5 || v == 6 || v == 7) && a.D != 128) {
     launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
-  } else if (v == 5 || v == 6) {  // 6: without the FMA-pipe exp2 share
+  } else if (v == 5 || v == 6 || v == 7) {  // FMA-pipe exp2 share: 5 -> 1/4, 7 -> 1/8, 6 -> none
     static std::once_flag f5;
     std::call_once(f5, [] {
-      cudaFuncSetAttribute(attn_fwd_2w_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
-      cudaFuncSetAttribute(attn_fwd_2w_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_2w_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_2w_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_2w_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
     });
-    auto kern = v == 5 ? attn_fwd_2w_kernel<true> : attn_fwd_2w_kernel<false>;
+    auto kern = v == 5 ? attn_fwd_2w_kernel<4> : v == 7 ? attn_fwd_2w_kernel<8> : attn_fwd_2w_kernel<0>;
     kern<<<dim3(a.S / TILE, a.H), 384, Fwd2wSmem::BYTES, stream>>>(a.q, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
   } else if (v == 4 && a.S % (2 * TILE) == 0) {
     dim3 grid2(a.S / (2 * TILE), a.H);
