@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm_tc.h"
@@ -299,6 +300,181 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair GEMM
+// Same contract and epilogues, on 256x256 output tiles computed by a CTA pair
+// (cluster of 2, tcgen05.mma.cta_group::2, M=256 N=256 K=16).  Each CTA
+// stages its own 128 rows of A and 128 of the 256 B rows, so per-CTA operand
+// traffic (TMA writes + MMA reads of shared memory) per FLOP drops by a
+// quarter, and the 32 KiB stage allows a 6-deep ring.  The leader CTA issues
+// every MMA; its commits multicast to both CTAs' "stage empty" / "accumulator
+// full" barriers.  Both CTAs' TMA loads complete on the leader's "stage full"
+// barrier, and both epilogues release the leader's "accumulator empty".
+constexpr int P_BM = 128;               // rows of A per CTA (pair tile M = 256)
+constexpr int P_BN = 256;               // pair tile N; each CTA stages 128 B rows
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = P_BM * BK * 2;         // 16 KiB
+constexpr int P_B_BYTES = (P_BN / 2) * BK * 2;   // 16 KiB
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int P_GROUP_M = 16;  // raster band of pair tiles (8 measured slower)
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                    int M, int N, int K, EpiParams ep) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + P_STAGES;
+  uint64_t* tfull_bar = empty_bar + P_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+  const uint32_t rank = dev::cluster_ctarank();
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+
+  const int m_tiles = (M + 2 * P_BM - 1) / (2 * P_BM);
+  const int n_tiles = (N + P_BN - 1) / P_BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_a);
+    dev::tma_prefetch_desc(&map_b);
+    for (int s = 0; s < P_STAGES; ++s) {
+      dev::mbar_init(&full_bar[s], 1);
+      dev::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      dev::mbar_init(&tfull_bar[b], 1);
+      dev::mbar_init(&tempty_bar[b], 2 * 128);  // epilogue threads of both CTAs
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc_cg2(tmem_slot, TMEM_COLS);
+  dev::tc_fence_before();
+  dev::cluster_sync();  // peer barriers initialised before any remote signal
+  dev::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int t, int& mb, int& nb) {
+    const int group_size = P_GROUP_M * n_tiles;
+    const int g = t / group_size;
+    const int first_m = g * P_GROUP_M;
+    const int gm = min(P_GROUP_M, m_tiles - first_m);
+    const int local = t - g * group_size;
+    mb = first_m + local % gm;
+    nb = local / gm;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs): own A rows and own half of B
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < num_tiles; t += n_clusters) {
+        int mb, nb;
+        tile_coords(t, mb, nb);
+        const int m0 = mb * 2 * P_BM + rank * P_BM;
+        const int n0 = nb * P_BN + rank * (P_BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * P_STAGE_BYTES;
+          uint8_t* sb = sa + P_A_BYTES;
+          const uint32_t fb = dev::mapa(dev::smem_u32(&full_bar[stage]), 0);  // leader's barrier
+          if (rank == 0) dev::mbar_expect_tx(&full_bar[stage], 2 * P_STAGE_BYTES);
+          if (!A_MN) {
+            dev::tma_load_2d_cg2(sa, &map_a, fb, kb * BK, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < P_BM / 64; ++j) dev::tma_load_2d_cg2(sa + j * 8192, &map_a, fb, m0 + j * 64, kb * BK);
+          }
+          if (!B_MN) {
+            dev::tma_load_2d_cg2(sb, &map_b, fb, kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < P_BN / 2 / 64; ++j)
+              dev::tma_load_2d_cg2(sb + j * 8192, &map_b, fb, n0 + j * 64, kb * BK);
+          }
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader CTA; whole warp converged, elect.sync issues)
+      constexpr uint32_t idesc = dev::idesc_bf16_f32(2 * P_BM, P_BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cluster; t < num_tiles; t += n_clusters, ++it) {
+        const int buf = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        dev::mbar_wait_w(&tempty_bar[buf], acc_phase ^ 1);
+        dev::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * P_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait_w(&full_bar[stage], phase);
+          dev::tc_fence_after();
+          const uint32_t sa = dev::smem_u32(smem + stage * P_STAGE_BYTES);
+          const uint32_t sb = sa + P_A_BYTES;
+          const uint64_t ad0 = A_MN ? dev::umma_desc_sw128(sa, 8192, 1024) : dev::umma_desc_sw128(sa, 16, 1024);
+          const uint64_t bd0 = B_MN ? dev::umma_desc_sw128(sb, 8192, 1024) : dev::umma_desc_sw128(sb, 16, 1024);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = ad0 + static_cast<uint64_t>((A_MN ? k * 2048 : k * 32) >> 4);
+            const uint64_t bd = bd0 + static_cast<uint64_t>((B_MN ? k * 2048 : k * 32) >> 4);
+            dev::mma2_bf16_ss_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          dev::mma2_commit_mc_w(&empty_bar[stage], 0x3);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        dev::mma2_commit_mc_w(&tfull_bar[buf], 0x3);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 of both CTAs; TMEM lane quarter = warp % 4
+    const uint32_t q = warp & 3;
+    int it = 0;
+    for (int t = cluster; t < num_tiles; t += n_clusters, ++it) {
+      int mb, nb;
+      tile_coords(t, mb, nb);
+      const int buf = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      dev::mbar_wait(&tfull_bar[buf], acc_phase);
+      dev::tc_fence_after();
+      const int m = mb * 2 * P_BM + rank * P_BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < P_BN / 32; ++c) {
+        uint32_t r[32];
+        dev::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * P_BN + c * 32, r);
+        dev::tmem_ld_wait_regs(r);
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
+        if (m < M) epilogue_chunk(ep, m, nb * P_BN + c * 32, N, x);
+      }
+      dev::tc_fence_before();
+      dev::mbar_arrive_cluster(dev::mapa(dev::smem_u32(&tempty_bar[buf]), 0));
+    }
+  }
+  dev::tc_fence_before();
+  dev::cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc_cg2(tmem_base, TMEM_COLS);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 template <bool A_MN, bool B_MN>
 cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
@@ -308,8 +484,15 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
     ok = make_tma_2d_bf16(&ma, d.a, d.K, d.M, d.lda, BK, BM);
   else
     ok = make_tma_2d_bf16(&ma, d.a, d.M, d.K, d.lda, 64, BK);
+  // MEMO_GEMM_PAIR=1: CTA-pair 256x256 tiles (ablation).  Correct (same per-row
+  // K order, bitwise swap parity holds) but not faster under the power cap on
+  // the 7B layer shapes: +6 % on QKV, -3..-13 % on the others (profiles/README.md).
+  static const bool pair = [] {
+    const char* e = getenv("MEMO_GEMM_PAIR");
+    return e && atoi(e) != 0;
+  }();
   if (!B_MN)
-    ok = ok && make_tma_2d_bf16(&mb, d.b, d.K, d.N, d.ldb, BK, BN);
+    ok = ok && make_tma_2d_bf16(&mb, d.b, d.K, d.N, d.ldb, BK, pair ? P_BN / 2 : BN);
   else
     ok = ok && make_tma_2d_bf16(&mb, d.b, d.N, d.K, d.ldb, 64, BK);
   if (!ok) return cudaErrorInvalidValue;
@@ -331,8 +514,16 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_tc2_kernel<A_MN, B_MN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
   });
   const int g_num_sms = num_sms();
+  if (pair) {  // CTA pairs on 256x256 tiles
+    const int tiles = ((d.M + 2 * P_BM - 1) / (2 * P_BM)) * ((d.N + P_BN - 1) / P_BN);
+    const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+    gemm_tc2_kernel<A_MN, B_MN><<<2 * clusters, NUM_THREADS, P_SMEM_BYTES, stream>>>(ma, mb, d.M, d.N, d.K, ep);
+    return cudaGetLastError();
+  }
   const int tiles = ((d.M + BM - 1) / BM) * ((d.N + BN - 1) / BN);
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   gemm_tc_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, d.M, d.N,

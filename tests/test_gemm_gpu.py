@@ -95,3 +95,22 @@ def test_gemm_qkv_rope_epilogue():
     torch.testing.assert_close(q.float(), rot(y[:, :h]).to(torch.bfloat16).float(), rtol=2e-2, atol=2e-2)
     torch.testing.assert_close(k.float(), rot(y[:, h:2 * h]).to(torch.bfloat16).float(), rtol=2e-2, atol=2e-2)
     torch.testing.assert_close(v.float(), y[:, 2 * h:], rtol=1e-2, atol=1e-2)
+
+
+def test_gemm_cta_pair_ablation():
+    """MEMO_GEMM_PAIR=1 (CTA-pair 256x256 tiles, cta_group::2): all three layouts,
+    ragged M and N, against the fp32 reference in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, torch; sys.path.insert(0, %r)\n"
+        "from tests.test_gemm_gpu import test_gemm_layouts\n"
+        "for shp in [(128, 256, 64), (200, 256, 192), (1024, 2048, 1024), (640, 288, 4096)]:\n"
+        "    for lay in ('fwd', 'dgrad', 'wgrad'):\n"
+        "        test_gemm_layouts(*shp, lay)\n"
+        "print('pair ok')\n" % root)
+    env = dict(os.environ, MEMO_GEMM_PAIR="1")
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "pair ok" in out.stdout, out.stdout + out.stderr

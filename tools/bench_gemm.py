@@ -60,7 +60,11 @@ def run(M, N, K, layout, iters=10):
 
 if __name__ == "__main__":
     S = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-    for (M, N, K, lay) in [(S, 12288, 4096, "fwd"), (S, 22016, 4096, "fwd"), (S, 4096, 11008, "fwd"),
-                           (S, 4096, 12288, "dgrad"), (S, 4096, 22016, "dgrad"),
-                           (4096, 11008, S, "wgrad"), (12288, 4096, S, "wgrad")]:
+    only = os.environ.get("GEMM_ONLY")  # comma-separated shape indices
+    shapes = [(S, 12288, 4096, "fwd"), (S, 22016, 4096, "fwd"), (S, 4096, 11008, "fwd"),
+              (S, 4096, 12288, "dgrad"), (S, 4096, 22016, "dgrad"),
+              (4096, 11008, S, "wgrad"), (12288, 4096, S, "wgrad")]
+    for i, (M, N, K, lay) in enumerate(shapes):
+        if only and str(i) not in only.split(","):
+            continue
         print(json.dumps(run(M, N, K, lay)), flush=True)
