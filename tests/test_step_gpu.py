@@ -41,6 +41,8 @@ CASES = [
     (4, 256, 2, 768, 512, 512, 0.5),    # D=128, two swapped layers
     (4, 256, 4, 768, 512, 1024, 0.25),  # D=64 (cfg1' shape family)
     (2, 256, 4, 768, 512, 512, 0.5),    # n=2: nothing swaps (reference rule)
+    (2, 256, 4, 768, 512, 4096, 0.5),   # BASELINE configs[0] (cfg1) exactly
+    (4, 256, 4, 768, 512, 4096, 0.5),   # cfg1' (4 layers, so swap+recompute happen)
 ]
 
 
