@@ -666,6 +666,278 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ------------------------------------------------------------------ forward, ping-pong
+// Two adjacent query tiles (A = 2p, B = 2p+1) of one head per CTA, each with
+// its own softmax warpgroup (one thread per row, all 128 columns in
+// registers).  The tensor pipe alternates between the groups:
+//   PV_A(j-1) S_A(j) PV_B(j-1) S_B(j) ...
+// so while group A turns S_A(j) into P_A(j) the pipe runs PV_B(j-1) and S_B(j)
+// (1024 cycles of work), and vice versa.  K and V tiles are shared by both
+// groups (half the L2->SMEM traffic per FLOP of the one-tile kernels).
+// TMEM: S_A | S_B | O_A | O_B (P overwrites its S), so Q stays in shared
+// memory (SS-mode S).  setmaxnreg moves registers from the TMA/MMA warpgroup
+// (56) to the softmax warpgroups (224) so a row's 128 logits stay resident.
+struct FwdPpSmem {
+  static constexpr int TILE_BYTES = 2 * CHUNK_BYTES;  // D = 128
+  static constexpr int QA_OFF = 0;
+  static constexpr int QB_OFF = TILE_BYTES;
+  static constexpr int K_OFF = 2 * TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;  // 2-stage K and V rings
+  static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+template <int EMU_EVERY>
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
+                       float* __restrict__ lse, int S, int H, float scale_log2) {
+  constexpr int D = 128;
+  using L = FwdPpSmem;
+  constexpr int NC = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2] per group
+  uint64_t* p_full = bars + 11;  // [2] per group
+  uint64_t* o_done = bars + 13;  // [2] per group
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+
+  const int n_pairs = S / (2 * TILE);
+  const int pp = n_pairs - 1 - static_cast<int>(blockIdx.x);  // heavy pairs first
+  const int hh = blockIdx.y;
+  const int qt0 = 2 * pp;
+  const int n_kv = qt0 + 2;  // key tiles of group B; group A uses n_kv - 1
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_k);
+    dev::tma_prefetch_desc(&map_v);
+    dev::mbar_init(q_full, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      dev::mbar_init(&k_full[s2], 1);
+      dev::mbar_init(&k_empty[s2], 1);
+      dev::mbar_init(&v_full[s2], 1);
+      dev::mbar_init(&v_empty[s2], 1);
+      dev::mbar_init(&s_full[s2], 1);
+      dev::mbar_init(&p_full[s2], 128);
+      dev::mbar_init(&o_done[s2], 1);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (warp == 0) {
+      if (lane == 0) {
+        dev::mbar_expect_tx(q_full, 2 * L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::QA_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, qt0 * TILE);
+          dev::tma_load_2d(smem + L::QB_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, (qt0 + 1) * TILE);
+        }
+        for (int j = 0; j < n_kv; ++j) {
+          const int st = j & 1;
+          const uint32_t ph = (j >> 1) & 1;
+          dev::mbar_wait(&k_empty[st], ph ^ 1);
+          dev::mbar_expect_tx(&k_full[st], L::TILE_BYTES);
+          for (int c = 0; c < NC; ++c)
+            dev::tma_load_2d(smem + L::K_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_k, &k_full[st],
+                             hh * D + c * 64, j * TILE);
+          dev::mbar_wait(&v_empty[st], ph ^ 1);
+          dev::mbar_expect_tx(&v_full[st], L::TILE_BYTES);
+          for (int c = 0; c < NC; ++c)
+            dev::tma_load_2d(smem + L::V_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_v, &v_full[st],
+                             hh * D + c * 64, j * TILE);
+        }
+      }
+    } else if (warp == 1) {
+      // whole warp, converged: MMAs/commits elect one lane
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
+      const uint64_t qd[2] = {kmajor_base(dev::smem_u32(smem + L::QA_OFF)),
+                              kmajor_base(dev::smem_u32(smem + L::QB_OFF))};
+      const int nA = n_kv - 1;
+      dev::mbar_wait_w(q_full, 0);
+      auto issue_s = [&](int g, int j) {  // S_g(j) = Q_g K_j^T ; group A always issues first for tile j
+        const int st = j & 1;
+        if (g == 0 || j == nA) {
+          dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
+          dev::tc_fence_after();
+        }
+        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ss_w(tmem + g * 128, kmajor_step(g ? qd[1] : qd[0], kk), kmajor_step(kd, kk), idesc_s,
+                             kk > 0);
+        dev::mma_commit_w(&s_full[g]);
+        if (g == 1) dev::mma_commit_w(&k_empty[st]);  // B is the last reader of K_j
+      };
+      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j
+        const int st = j & 1;
+        dev::mbar_wait_w(&p_full[g], j & 1);
+        if (g == 0 || j == nA) {
+          dev::mbar_wait_w(&v_full[st], (j >> 1) & 1);
+        }
+        dev::tc_fence_after();
+        const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
+                             (j | kk) != 0);
+        dev::mma_commit_w(&o_done[g]);
+        if (g == 1) dev::mma_commit_w(&v_empty[st]);
+      };
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j < nA) {
+          issue_pv(0, j);
+          if (j + 1 < nA) issue_s(0, j + 1);
+        }
+        issue_pv(1, j);
+        if (j + 1 < n_kv) issue_s(1, j + 1);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    const int g = (warp - 4) >> 2;  // softmax group: 0 -> tile A, 1 -> tile B
+    const uint32_t q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const int qt = qt0 + g;
+    const int qidx = qt * TILE + row;
+    const int n_my = qt + 1;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const uint32_t t_s = tmem + g * 128 + lane_off;
+    const uint32_t t_o = tmem + 256 + g * D + lane_off;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_my; ++j) {
+      dev::mbar_wait(&s_full[g], j & 1);
+      dev::tc_fence_after();
+      uint32_t r[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dev::tmem_ld32(t_s + c * 32, r[c]);
+      dev::tmem_ld_wait_regs(r[0], r[1], r[2], r[3]);
+      bool any = false;
+      float factor = 1.f;
+      uint32_t p[64];
+      auto tile = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+        if (DIAG) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
+        }
+        float mx8[8];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = __uint_as_float(r[0][k2]);
+#pragma unroll
+        for (int i = 8; i < 128; i += 8)
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(mx8[k2], __uint_as_float(r[i >> 5][(i & 31) + k2]));
+#pragma unroll
+        for (int k2 = 4; k2 > 0; k2 >>= 1)
+#pragma unroll
+          for (int q2 = 0; q2 < k2; ++q2) mx8[q2] = fmaxf(mx8[q2], mx8[q2 + k2]);
+        const float cand = fmaxf(m, mx8[0] * scale_log2);
+        const bool need = j == 0 || cand > m + kRescaleThreshold;
+        any = __any_sync(0xffffffffu, need);
+        float m_new = m;
+        if (any) {
+          m_new = cand;
+          factor = j == 0 ? 0.f : dev::ex2(m - m_new);
+        }
+        uint64_t sum4[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                            __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
+                                    scale_log2, -m_new);
+          float a, b;
+          if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
+            a = exp2_fma(f2_lo(x2));
+            b = exp2_fma(f2_hi(x2));
+          } else {
+            a = dev::ex2(f2_lo(x2));
+            b = dev::ex2(f2_hi(x2));
+          }
+          sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
+          p[i] = dev::pack_bf16(a, b);
+        }
+        const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+        l = l * factor + (f2_lo(s01) + f2_hi(s01));
+        m = m_new;
+      };
+      if (j == qt)
+        tile(std::true_type{});
+      else
+        tile(std::false_type{});
+      {
+        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&p[0]);
+        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&p[32]);
+        dev::tmem_st32(t_s, p0);
+        dev::tmem_st32(t_s + 32, p1);
+      }
+      if (any && j > 0) {
+        // O_g must hold P(j-1)V(j-1) before it is rescaled
+        dev::mbar_wait(&o_done[g], (j - 1) & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          dev::tmem_ld32(t_o + c * 32, o);
+          dev::tmem_ld_wait_regs(o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+          dev::tmem_st32(t_o + c * 32, o);
+        }
+      }
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_full[g]);
+    }
+    dev::mbar_wait(&o_done[g], (n_my - 1) & 1);
+    dev::tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      dev::tmem_ld32(t_o + c * 32, o);
+      dev::tmem_ld_wait_regs(o);
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 u;
+        u.x = dev::pack_bf16(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
+        u.y = dev::pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
+        u.z = dev::pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
+        u.w = dev::pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
+        dst[i] = u;
+      }
+    }
+    lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(l)) * kLn2;
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ forward, 2 query tiles
 // Two adjacent query tiles (2p, 2p+1) of one head share every K/V tile load,
 // halving the L2->SMEM streaming that bounds the 1-tile kernel, and their
@@ -2217,7 +2489,7 @@ void launch_fwd(const AttnFwdArgs& a, const CUtensorMap& mq, const CUtensorMap& 
 int fwd_variant() {
   static int v = [] {
     const char* e = getenv("MEMO_ATTN_FWD_VARIANT");
-    return e ? atoi(e) : 5;
+    return e ? atoi(e) : 8;
   }();
   return v;
 }
@@ -2232,8 +2504,21 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   const float scale_log2 = a.softmax_scale * kLog2e;
   if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
-  const int v = fwd_variant();  // 0-3: bit0 Q in TMEM, bit1 FMA exp2 share; 4: 2-tile; 5: split rows
-  if ((v == 5 || v == 6 || v == 7) && a.D != 128) {
+  // 0-3: one softmax warp per row (bit0 Q in TMEM, bit1 FMA exp2 share); 4: 2-tile two-pass;
+  // 5-7: split rows; 8-10: ping-pong two Q tiles (default 8)
+  const int v = fwd_variant();
+  if (v >= 8 && a.D == 128 && a.S % (2 * TILE) == 0) {  // ping-pong (two Q tiles, setmaxnreg)
+    // FMA-pipe exp2 share: 8 -> 1/4, 9 -> none, 10 -> 1/8
+    static std::once_flag f8;
+    std::call_once(f8, [] {
+      cudaFuncSetAttribute(attn_fwd_pp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_pp_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_pp_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+    });
+    auto kern = v == 9 ? attn_fwd_pp_kernel<0> : v == 10 ? attn_fwd_pp_kernel<8> : attn_fwd_pp_kernel<4>;
+    kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
+                                                                        scale_log2);
+  } else if (v >= 5 && a.D != 128) {
     launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
   } else if (v == 5 || v == 6 || v == 7) {  // FMA-pipe exp2 share: 5 -> 1/4, 7 -> 1/8, 6 -> none
     static std::once_flag f5;
