@@ -137,7 +137,7 @@ def test_training_trajectory_across_alpha_matches_fp32():
     cfg = model(n, h, H, F, V, S)
     ocfg = O.make_cfg(n, h, H, F, V, S)
     toks, labels = O.tokens(17, V, S)
-    lr, b1, b2, eps, wd = 3e-3, 0.9, 0.95, 1e-8, 0.01
+    lr, b1, b2, eps, wd = 1e-3, 0.9, 0.95, 1e-8, 0.01  # 3e-3 turns unstable by step 6 (loss rises)
     opts = dict(seed=7, optimizer=1, lr=lr, beta1=b1, beta2=b2, adam_eps=eps, weight_decay=wd, ce_chunk=256)
     with Executor(cfg, HW, alpha=0.5, swap_enabled=0, **opts) as ex:
         base = [ex.step(toks, labels) for _ in range(steps)]
