@@ -213,6 +213,8 @@ def run_reference(args, rank):
     v = statistics.median(vals)
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            # one full workload step at the sampled rate (extrapolated from the bounded sample)
+            "ms_per_step": n_cfg[5] / v * 1e3 if v else None, "ms_per_step_extrapolated": True,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": n_cfg[6], "cpu": "oracle port"},
             "cpu_baseline": {**base, "value": v},
