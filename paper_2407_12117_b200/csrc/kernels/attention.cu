@@ -399,6 +399,17 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ uint64_t ffma2_v(uint64_t a, float b, uint64_t c) {  // a * b + c (b broadcast)
+  uint64_t r;
+  const uint64_t bb = f2_pack(b, b);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(bb), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
 __device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -1214,7 +1225,7 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ============================================================== backward
-// delta[h][t] = sum_d dO*O ; lse2[h][t] = lse * log2(e)
+// ndelta[h][t] = -sum_d dO*O ; nlse2[h][t] = -lse * log2(e)  (the delta / lse2 workspace)
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                      const __nv_bfloat16* __restrict__ dout,
                                      const float* __restrict__ lse, float* __restrict__ delta,
@@ -1235,8 +1246,8 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) {
     const long long i = static_cast<long long>(hh) * S + t;
-    delta[i] = acc;
-    lse2[i] = lse[i] * kLog2e;
+    delta[i] = -acc;            // stored negated: consumers add (FFMA2/FADD2, no negation)
+    lse2[i] = -lse[i] * kLog2e;
   }
 }
 
@@ -1444,10 +1455,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int qc = c * 32 + 4 * j4 + e;
-              float p = dev::ex2(__uint_as_float(sr[4 * j4 + e]) * scale_log2 - lq[e]);
+              float p = dev::ex2(fmaf(__uint_as_float(sr[4 * j4 + e]), scale_log2, lq[e]));
               if (DIAG && half * HALF + qc < r) p = 0.f;
               p4[e] = p;
-              d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) - dq[e]);
+              d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) + dq[e]);
             }
             pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
             pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
@@ -1670,11 +1681,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
           float p4[4], d4[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float p = dev::ex2(__uint_as_float(sr[4 * j4 + e]) * scale_log2 - lq[e]);
-            if (DIAG && qq * QSTEP + 16 * ch + 4 * j4 + e < r) p = 0.f;
-            p4[e] = p;
-            d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) - dq4[e]);
+          for (int e = 0; e < 4; e += 2) {  // column pairs: FFMA2 / FADD2 / FMUL2
+            const uint64_t x2 = ffma2_v(f2_pack(__uint_as_float(sr[4 * j4 + e]), __uint_as_float(sr[4 * j4 + e + 1])),
+                                        scale_log2, f2_pack(lq[e], lq[e + 1]));
+            float pa = dev::ex2(f2_lo(x2)), pb = dev::ex2(f2_hi(x2));
+            if (DIAG && qq * QSTEP + 16 * ch + 4 * j4 + e < r) pa = 0.f;
+            if (DIAG && qq * QSTEP + 16 * ch + 4 * j4 + e + 1 < r) pb = 0.f;
+            const uint64_t pv = f2_pack(pa, pb);
+            const uint64_t d2 = fmul2(pv, fadd2(f2_pack(__uint_as_float(dr[4 * j4 + e]), __uint_as_float(dr[4 * j4 + e + 1])),
+                                               f2_pack(dq4[e], dq4[e + 1])));
+            p4[e] = pa;
+            p4[e + 1] = pb;
+            d4[e] = f2_lo(d2);
+            d4[e + 1] = f2_hi(d2);
           }
           pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
           pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
@@ -1885,16 +1904,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           dev::tmem_ld_wait_regs(sr, dr);
           uint32_t dd[16];
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            float d2[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int kc = half * HALF + c * 32 + 2 * jj + e;
-              float p = dev::ex2(__uint_as_float(sr[2 * jj + e]) * scale_log2 - my_lse2);
-              if (DIAG && kc > r) p = 0.f;
-              d2[e] = p * (__uint_as_float(dr[2 * jj + e]) - my_delta);
-            }
-            dd[jj] = dev::pack_bf16(d2[0], d2[1]);
+          for (int jj = 0; jj < 16; ++jj) {  // key pairs: FFMA2 / FADD2 / FMUL2
+            const int kc = half * HALF + c * 32 + 2 * jj;
+            const uint64_t x2 = ffma2(f2_pack(__uint_as_float(sr[2 * jj]), __uint_as_float(sr[2 * jj + 1])),
+                                      scale_log2, my_lse2);
+            float pa = dev::ex2(f2_lo(x2)), pb = dev::ex2(f2_hi(x2));
+            if (DIAG && kc > r) pa = 0.f;
+            if (DIAG && kc + 1 > r) pb = 0.f;
+            const uint64_t d2 = fmul2(f2_pack(pa, pb),
+                                      fadd2(f2_pack(__uint_as_float(dr[2 * jj]), __uint_as_float(dr[2 * jj + 1])),
+                                            f2_pack(my_delta, my_delta)));
+            dd[jj] = dev::pack_bf16(f2_lo(d2), f2_hi(d2));
           }
           dev::tmem_st16(t_s + c * 32, dd);  // inside this warp's own slice
         }
@@ -2238,10 +2258,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int qc = (g & 1) * HALF + 32 * ch + 4 * j4 + e;  // query within tile
-            float p = dev::ex2(__uint_as_float(sr[4 * j4 + e]) * scale_log2 - lq[e]);
+            float p = dev::ex2(fmaf(__uint_as_float(sr[4 * j4 + e]), scale_log2, lq[e]));
             if (DIAG && qc < r) p = 0.f;
             p4[e] = p;
-            d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) - dq4[e]);
+            d4[e] = p * (__uint_as_float(dr[4 * j4 + e]) + dq4[e]);
           }
           pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
           pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
