@@ -101,3 +101,33 @@ def test_tp_rank_plan_bit_exact_and_sized(t):
     assert info["rb_bytes"] * t == pytest.approx(
         sum(info["skeletal_components"]) * t, rel=0)
     assert info["split"][0] + info["split"][1] == cfg.seq_len
+
+
+@pytest.mark.parametrize("name,t", [("cfg3_7b_1m", 8), ("cfg4_13b_512k", 2), ("cfg4_13b_512k", 4),
+                                    ("cfg4_13b_512k", 8)])
+def test_multi_gpu_configs_fit_one_b200_per_rank(name, t):
+    """BASELINE configs[2] (7B, 32 layers, S=1M, TP=SP=8) and configs[3] (13B,
+    40 layers, S=512K, TP=SP in {2,4,8}) on the paper's node: 2 TiB host shared
+    by the t GPUs in use, cpu_mem = 2 TiB / t per GPU (SURVEY §8 HW row,
+    discovery 3; this pool's 196 GB host is CpuInfeasible for them, code 4).  Each rank's planned device
+    allocation (arena + rounding buffers + bf16 params + f32 grads, one
+    cudaMalloc) fits a 180 GB B200; the arena plan is optimal and bit-exact with
+    the reference planner; alpha comes from solve_alpha."""
+    if name.startswith("cfg3"):
+        cfg = llama(32, 4096, 32, 11008, 32000, 1 << 20)
+    else:
+        cfg = llama(40, 5120, 40, 13824, 32000, 1 << 19)
+    cfg.tp_degree = t
+    hw = P.HardwareConfig(pcie_bandwidth=50e9, cpu_mem=2048 * P.GiB // t, gpu_mem=180 * 10 ** 9,
+                          peak_flops=2.25e15, efficiency=0.5)
+    ex = Executor(cfg, hw, dry_run=1, optimizer=0)
+    info = ex.info()
+    plan = json.loads(ex.plan_json())
+    assert plan["optimal"] is True
+    assert info["device_bytes"] < 180 * 10 ** 9, (name, t, info["device_bytes"] / 1e9)
+    sw = info["swap"]
+    assert sw.swapped_layers == cfg.n_layers - 2
+    assert 0.0 < sw.alpha <= 1.0
+    assert info["pinned_bytes"] <= sw.cpu_footprint <= hw.cpu_mem
+    if os.path.exists(PROBE):
+        assert _ref_plan(ex.trace_text()) == ex.plan_json()
