@@ -29,6 +29,8 @@ struct NcclApi {
                                  cudaStream_t) = nullptr;
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
   bool ok() const { return h && init_rank; }
 };
@@ -49,6 +51,7 @@ NcclApi& nccl() {
     api.all_gather = reinterpret_cast<decltype(api.all_gather)>(sym("ncclAllGather"));
     api.reduce_scatter = reinterpret_cast<decltype(api.reduce_scatter)>(sym("ncclReduceScatter"));
     api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(sym("ncclAllReduce"));
+    api.reduce = reinterpret_cast<decltype(api.reduce)>(sym("ncclReduce"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
   });
   return api;
@@ -87,6 +90,9 @@ class NcclComm final : public Comm {
                   cudaStream_t st) override {
     nck(nccl().all_reduce(send, recv, count, ndt(dt), op == CommOp::Sum ? ncclSum : ncclMax, comm_, st),
         "ncclAllReduce");
+  }
+  void reduce(const void* send, void* recv, size_t count, CommDtype dt, int root, cudaStream_t st) override {
+    nck(nccl().reduce(send, recv, count, ndt(dt), ncclSum, root, comm_, st), "ncclReduce");
   }
 
  private:
@@ -177,6 +183,11 @@ class LoopbackComm final : public Comm {
                   cudaStream_t st) override {
     publish(send, st);
     reduce(recv, count, 0, dt, op == CommOp::Max, st);
+    finish(st);
+  }
+  void reduce(const void* send, void* recv, size_t count, CommDtype dt, int root, cudaStream_t st) override {
+    publish(send, st);
+    if (rank_ == root) reduce(recv, count, 0, dt, false, st);
     finish(st);
   }
 

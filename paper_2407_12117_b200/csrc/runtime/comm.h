@@ -1,9 +1,10 @@
 // comm.h — tensor/sequence-parallel collectives for the executor.
 //
-// Megatron-style SP+TP needs exactly three collectives on the
-// layer path: all-gather along the sequence before the column-parallel GEMMs,
+// Megatron-style SP+TP needs these collectives on the layer path:
+// all-gather along the sequence before the column-parallel GEMMs, the
 // reduce-scatter along the sequence after the row-parallel GEMMs (and their
-// adjoints in backward), plus small all-reduces for the vocab-parallel
+// adjoints in backward) -- issued as t per-row-block reduces so the partial
+// buffer is S/t rows -- plus small all-reduces for the vocab-parallel
 // cross-entropy and the replicated parameters' gradients.
 //
 // Two interchangeable backends:
@@ -41,6 +42,11 @@ class Comm {
                               cudaStream_t st) = 0;
   virtual void all_reduce(const void* send, void* recv, size_t count, CommDtype dt, CommOp op,
                           cudaStream_t st) = 0;
+  // recv[count] on rank `root` = sum over ranks of send[count] (recv ignored elsewhere).
+  // The row-chunked reduce-scatter: rank k's rows are reduced to rank k while the
+  // next chunk's GEMM runs, with a partial buffer of S/t rows instead of S.
+  virtual void reduce(const void* send, void* recv, size_t count, CommDtype dt, int root,
+                      cudaStream_t st) = 0;
 };
 
 // NCCL backend.  `unique_id` is the 128-byte ncclUniqueId produced by

@@ -273,7 +273,7 @@ void Executor::build_trace_tp(TraceBuilder& tb) {
     sk(i, C_V);
     f("xn_full");
     sk(i, C_O);
-    m("a_part", S * h * 4);
+    m("a_part", Sl * h * 4);
     m("a_red", Sl * h * 4);
     f("a_part");
     sk(i, C_A);
@@ -284,7 +284,7 @@ void Executor::build_trace_tp(TraceBuilder& tb) {
     sk(i, C_GU);
     sk(i, C_ACT);
     f("xn2_full");
-    m("d_part", S * h * 4);
+    m("d_part", Sl * h * 4);
     m("d_red", Sl * h * 4);
     f("d_part");
     f("d_red");
@@ -318,7 +318,7 @@ void Executor::build_trace_tp(TraceBuilder& tb) {
     if (R > 0) {  // recompute transients, carried by every layer
       m("r_xn_full", S * h * 2);
       f("r_xn_full");
-      m("r_a_part", S * h * 4);
+      m("r_a_part", Sl * h * 4);
       m("r_a_red", Sl * h * 4);
       f("r_a_part");
       m("r_x1", Sl * h * 4);
@@ -331,7 +331,7 @@ void Executor::build_trace_tp(TraceBuilder& tb) {
     m("dact", S * Fl * 2);
     m("dgu", S * 2 * Fl * 2);
     f("dact");
-    m("dxn2_part", S * h * 4);
+    m("dxn2_part", Sl * h * 4);
     m("dxn2", Sl * h * 4);
     f("dxn2_part");
     m("b_xn2_full", S * h * 2);
@@ -350,7 +350,7 @@ void Executor::build_trace_tp(TraceBuilder& tb) {
     m("dqkv", S * 3 * hl * 2);
     f("attn_ws");
     f("dout");
-    m("dxn_part", S * h * 4);
+    m("dxn_part", Sl * h * 4);
     m("dxn", Sl * h * 4);
     f("dxn_part");
     m("b_xn_full", S * h * 2);
@@ -937,6 +937,20 @@ inline void rs(Comm* c, const float* src, float* dst, size_t count, cudaStream_t
 }
 }  // namespace
 
+void Executor::gemm_reduce_rows(GemmDesc g, float* part, float* out) {
+  const int t = d_.t, Sl = d_.Sl;
+  const auto* a = static_cast<const __nv_bfloat16*>(g.a);
+  const size_t count = static_cast<size_t>(Sl) * g.N;
+  g.M = Sl;
+  g.c = part;
+  g.ldc = g.N;
+  for (int k = 0; k < t; ++k) {  // same per-row K order as one S-row GEMM: bitwise equal rows
+    g.a = a + static_cast<Bytes>(k) * Sl * g.lda;
+    gemm(g);
+    comm_->reduce(part, k == d_.r ? out : part, count, CommDtype::F32, k, cs_);
+  }
+}
+
 void Executor::layer_fwd_tp(int i) {
   const int S = d_.S, Sl = d_.Sl, h = d_.h, hl = d_.hl, Fl = d_.Fl, Hl = d_.Hl, D = d_.D;
   if (i >= 2 && swaps(i - 2)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 2], 0));  // F3
@@ -971,15 +985,13 @@ void Executor::layer_fwd_tp(int i) {
   gemm(g);
   AttnFwdArgs fa{Q, K, Vv, O, LSE, S, Hl, D, 1.0f / std::sqrt(static_cast<float>(D))};
   attention_fwd(fa);
-  gemm(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, a_part, h));
-  rs(comm_.get(), a_part, a_red, shard, cs_);
+  gemm_reduce_rows(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, nullptr, h), a_part, a_red);
   G(resid_round(X, a_red, A, x1, static_cast<long long>(shard), cs_));
   G(rmsnorm_fwd(x1, nullptr, P("g2"), XN2, Sl, h, opt_.eps, cs_));
   ag(comm_.get(), XN2, xn2_full, shard, cs_);
   gemm(gd(S, 2 * Fl, h, xn2_full, h, 0, P("wgu"), h, 0, GEMM_EPI_BF16, GU, 2 * Fl));
   G(swiglu_fwd(GU, ACT, S, Fl, cs_));
-  gemm(gd(S, h, Fl, ACT, Fl, 0, P("wd"), Fl, 0, GEMM_EPI_F32, d_part, h));
-  rs(comm_.get(), d_part, d_red, shard, cs_);
+  gemm_reduce_rows(gd(S, h, Fl, ACT, Fl, 0, P("wd"), Fl, 0, GEMM_EPI_F32, nullptr, h), d_part, d_red);
   float* out = i + 1 < d_.n ? reinterpret_cast<float*>(comp(i + 1, C_X))
                             : static_cast<float*>(arena_ptr(seg_emb_fwd_, "x_final"));
   if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 1], 0));  // RB drained
@@ -1029,8 +1041,7 @@ void Executor::layer_recompute_tp(int i) {
       gemm(g);
     }
     // attn_proj needs every rank's partial: redo the out-projection + RS exactly as forward
-    gemm(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, a_part, h));
-    rs(comm_.get(), a_part, a_red, shard, cs_);
+    gemm_reduce_rows(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, nullptr, h), a_part, a_red);
     if (Rl > 0) {
       G(resid_round(X + r0 * h, a_red + r0 * h, A + r0 * h, x1 + r0 * h,
                     static_cast<long long>(Rl) * h, cs_));
@@ -1091,8 +1102,7 @@ void Executor::layer_bwd_tp(int i) {
   gemm(gd(S, Fl, h, dy_full, h, 0, P("wd"), Fl, 1, GEMM_EPI_BF16, dact, Fl));
   gemm(gd(h, Fl, S, dy_full, h, 1, ACT, Fl, 1, GEMM_EPI_F32, Gr("wd"), Fl));
   G(swiglu_bwd(GU, dact, dgu, S, Fl, cs_));
-  gemm(gd(S, h, 2 * Fl, dgu, 2 * Fl, 0, P("wgu"), h, 1, GEMM_EPI_F32, dxn2_part, h));
-  rs(comm_.get(), dxn2_part, dxn2, shard, cs_);
+  gemm_reduce_rows(gd(S, h, 2 * Fl, dgu, 2 * Fl, 0, P("wgu"), h, 1, GEMM_EPI_F32, nullptr, h), dxn2_part, dxn2);
   ag(comm_.get(), XN2, xn2_full, shard, cs_);
   gemm(gd(2 * Fl, h, S, dgu, 2 * Fl, 1, xn2_full, h, 1, GEMM_EPI_F32, Gr("wgu"), h));
   G(rmsnorm_bwd(X, A, P("g2"), dxn2, dxc, dxc, da, part2, Gr("g2"), Sl, h, opt_.eps, false, cs_));
@@ -1107,8 +1117,7 @@ void Executor::layer_bwd_tp(int i) {
   ba.softmax_scale = 1.0f / std::sqrt(static_cast<float>(D));
   attention_bwd(ba);
   // QKV projection (column-parallel)
-  gemm(gd(S, h, 3 * hl, dqkv, 3 * hl, 0, P("wqkv"), h, 1, GEMM_EPI_F32, dxn_part, h));
-  rs(comm_.get(), dxn_part, dxn, shard, cs_);
+  gemm_reduce_rows(gd(S, h, 3 * hl, dqkv, 3 * hl, 0, P("wqkv"), h, 1, GEMM_EPI_F32, nullptr, h), dxn_part, dxn);
   ag(comm_.get(), XN, xn_full, shard, cs_);
   gemm(gd(3 * hl, h, S, dqkv, 3 * hl, 1, xn_full, h, 1, GEMM_EPI_F32, Gr("wqkv"), h));
   G(rmsnorm_bwd(X, nullptr, P("g1"), dxn, dxc, dxc, dxb, part1, Gr("g1"), Sl, h, opt_.eps, false, cs_));

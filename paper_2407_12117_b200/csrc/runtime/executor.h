@@ -133,6 +133,10 @@ class Executor {
   void prefetch(int i);
   void mark(int stream, int kind, int layer, bool begin);
   void gemm(const GemmDesc& g);
+  // Row-parallel GEMM (A [S, K] bf16 K-major, f32 output) followed by the
+  // sequence reduce-scatter, one rank's row block at a time: part holds S/t
+  // rows; rank k's block is reduced onto rank k's out.
+  void gemm_reduce_rows(GemmDesc g, float* part, float* out);
   void attention_fwd(AttnFwdArgs a);
   void attention_bwd(AttnBwdArgs a);
   struct OpMark {
