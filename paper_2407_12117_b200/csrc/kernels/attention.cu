@@ -1531,8 +1531,10 @@ struct DkdvTmSmem {
   static constexpr int BYTES = BAR_OFF + 256 + 1024;
 };
 
-template <int D>
-__global__ void __launch_bounds__(BWD_THREADS, 1)
+// WPQ: softmax-gradient warps per TMEM lane quarter (2: 16 query columns each;
+// 4: 8 columns each, compacted P/dS write-back behind a per-quarter named barrier)
+template <int D, int WPQ>
+__global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     attn_bwd_dkdv_tm_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
                             const __grid_constant__ CUtensorMap map_q,
                             const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
@@ -1553,7 +1555,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* p_ready = s_full + 2;      // [2]
   uint64_t* fin = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
-  constexpr int CW = 32 * BWD_COMPUTE_WARPS;
+  constexpr int CW = 32 * 4 * WPQ;
+  constexpr int COLS = QSTEP / WPQ;  // query columns per compute warp per step
 
   const int n_tiles = S / TILE;
   const int kt = blockIdx.x;  // key tile
@@ -1638,23 +1641,24 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const uint64_t dom = mnmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
 #pragma unroll
         for (int kk = 0; kk < QSTEP / 16; ++kk)
-          dev::mma_bf16_ts_w(t_dv, buf(b) + 16 * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
+          dev::mma_bf16_ts_w(t_dv, buf(b) + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
 #pragma unroll
         for (int kk = 0; kk < QSTEP / 16; ++kk)
-          dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + 16 * kk, mnmajor_step(qm, kk), idesc_g, (g | kk) != 0);
+          dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(qm, kk), idesc_g,
+                             (g | kk) != 0);
         if (qq == 3) dev::mma_commit_w(&in_empty[st]);
       }
       dev::mma_commit_w(fin);
     }
   } else if (warp >= 4) {
     const uint32_t q4 = warp & 3;
-    const int ch = (warp - 4) >> 2;  // 16-query slice of each 32-query step
+    const int ch = (warp - 4) >> 2;  // COLS-query slice of each 32-query step
     const int r = q4 * 32 + lane;    // key row in tile
     const int kidx = kt * TILE + r;
     const uint32_t lane_off = (q4 * 32) << 16;
     const long long hcols = static_cast<long long>(H) * D;
     // K (ch 0) / V (ch 1) row r -> TMEM A operand
-    row_to_tmem<D>((ch == 0 ? kg : vg) + kidx * hcols + hh * D, (ch == 0 ? t_k : t_v) + lane_off);
+    if (ch < 2) row_to_tmem<D>((ch == 0 ? kg : vg) + kidx * hcols + hh * D, (ch == 0 ? t_k : t_v) + lane_off);
     dev::tmem_st_wait();
     dev::tc_fence_before();
     dev::mbar_arrive(kv_ready);
@@ -1662,19 +1666,24 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
       const bool diag = i == 0;
       if (qq == 0) dev::mbar_wait(&in_full[st], (i / NS) & 1);
-      const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + 16 * ch) * 4;
+      const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + COLS * ch) * 4;
       const uint32_t dl = l2 + 512;
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       dev::tc_fence_after();
-      uint32_t sr[16], dr[16];
-      dev::tmem_ld16(buf(b) + lane_off + 16 * ch, sr);
-      dev::tmem_ld16(buf(b) + lane_off + 32 + 16 * ch, dr);
+      uint32_t sr[COLS], dr[COLS];
+      if constexpr (COLS == 16) {
+        dev::tmem_ld16(buf(b) + lane_off + 16 * ch, sr);
+        dev::tmem_ld16(buf(b) + lane_off + 32 + 16 * ch, dr);
+      } else {
+        dev::tmem_ld8(buf(b) + lane_off + 8 * ch, sr);
+        dev::tmem_ld8(buf(b) + lane_off + 32 + 8 * ch, dr);
+      }
       dev::tmem_ld_wait_regs(sr, dr);
-      uint32_t pp[8], dd[8];
+      uint32_t pp[COLS / 2], dd[COLS / 2];
       auto body = [&](auto diag_tag) {
         constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
-        for (int j4 = 0; j4 < 4; ++j4) {
+        for (int j4 = 0; j4 < COLS / 4; ++j4) {
           const float4 lv = dev::lds_f4(l2 + 16 * j4);
           const float4 dv4 = dev::lds_f4(dl + 16 * j4);
           const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
@@ -1685,11 +1694,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             const uint64_t x2 = ffma2_v(f2_pack(__uint_as_float(sr[4 * j4 + e]), __uint_as_float(sr[4 * j4 + e + 1])),
                                         scale_log2, f2_pack(lq[e], lq[e + 1]));
             float pa = dev::ex2(f2_lo(x2)), pb = dev::ex2(f2_hi(x2));
-            if (DIAG && qq * QSTEP + 16 * ch + 4 * j4 + e < r) pa = 0.f;
-            if (DIAG && qq * QSTEP + 16 * ch + 4 * j4 + e + 1 < r) pb = 0.f;
-            const uint64_t pv = f2_pack(pa, pb);
-            const uint64_t d2 = fmul2(pv, fadd2(f2_pack(__uint_as_float(dr[4 * j4 + e]), __uint_as_float(dr[4 * j4 + e + 1])),
-                                               f2_pack(dq4[e], dq4[e + 1])));
+            if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e < r) pa = 0.f;
+            if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e + 1 < r) pb = 0.f;
+            const uint64_t d2 = fmul2(f2_pack(pa, pb),
+                                      fadd2(f2_pack(__uint_as_float(dr[4 * j4 + e]), __uint_as_float(dr[4 * j4 + e + 1])),
+                                            f2_pack(dq4[e], dq4[e + 1])));
             p4[e] = pa;
             p4[e + 1] = pb;
             d4[e] = f2_lo(d2);
@@ -1705,8 +1714,18 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         body(std::true_type{});
       else
         body(std::false_type{});
-      dev::tmem_st8(buf(b) + lane_off + 16 * ch, pp);
-      dev::tmem_st8(buf(b) + lane_off + 32 + 16 * ch, dd);
+      if constexpr (COLS == 16) {
+        // packed bf16 stays inside this warp's own 16-column slice
+        dev::tmem_st8(buf(b) + lane_off + 16 * ch, pp);
+        dev::tmem_st8(buf(b) + lane_off + 32 + 16 * ch, dd);
+      } else {
+        // compacted: queries 8ch..8ch+7 -> cols 4ch..4ch+3, contiguous per 16-query
+        // k-step.  Those columns belong to another warp's slice, so every warp of
+        // this lane quarter must have finished its loads first.
+        named_bar(1 + q4, 128);
+        dev::tmem_st4(buf(b) + lane_off + 4 * ch, pp);
+        dev::tmem_st4(buf(b) + lane_off + 32 + 4 * ch, dd);
+      }
       dev::tmem_st_wait();
       dev::tc_fence_before();
       dev::mbar_arrive(&p_ready[b]);
@@ -1716,7 +1735,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     __nv_bfloat16* dvrow = dv + static_cast<long long>(kidx) * ld + hh * D;
     __nv_bfloat16* dkrow = dk + static_cast<long long>(kidx) * ld + hh * D;
 #pragma unroll 1
-    for (int c = ch * (D / 64); c < (ch + 1) * (D / 64); ++c) {
+    for (int c = ch; c < D / 32; c += WPQ) {  // 32-column chunks of dV/dK spread over the quarter's warps
       uint32_t r32[32];
       float x[32];
       dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
@@ -2362,6 +2381,14 @@ int attn_debug() {
 
 // MEMO_ATTN_BWD=fused selects the fused kernel (ablation; the split dK/dV +
 // dQ kernels measured faster at S=128K: 478 vs 498 ms, H=32, D=128).
+int dkdv_wpq() {  // MEMO_ATTN_DKDV_WPQ: softmax-gradient warps per lane quarter (2 or 4)
+  static const int v = [] {
+    const char* e = getenv("MEMO_ATTN_DKDV_WPQ");
+    return e && atoi(e) == 4 ? 4 : 2;
+  }();
+  return v;
+}
+
 bool bwd_fused() {
   static const bool v = [] {
     const char* e = getenv("MEMO_ATTN_BWD");
@@ -2440,7 +2467,9 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   std::call_once(f, [] {
     cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
-    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
@@ -2465,8 +2494,12 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
     attn_bwd_dkdv_kernel<D><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
         mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
         scale_log2);
+  else if (dkdv_wpq() == 4)
+    attn_bwd_dkdv_tm_kernel<D, 4><<<grid, 32 * (4 + 16), DkdvTmSmem<D>::BYTES, stream>>>(
+        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+        scale_log2);
   else
-    attn_bwd_dkdv_tm_kernel<D><<<grid, BWD_THREADS, DkdvTmSmem<D>::BYTES, stream>>>(
+    attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
         a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
         scale_log2);
   if (a.ev[2]) cudaEventRecord(a.ev[2], stream);
