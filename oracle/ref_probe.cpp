@@ -332,7 +332,7 @@ Json goldens_schedule() {
 int usage() {
   std::cerr << "usage: ref_probe goldens <dir> | plan <trace> <cap> <budget> <align> | "
                "dsa <trace> <cap> <budget> <align> | synth <config.json> | "
-               "report <config.json> [alpha] | bench_report <config.json> <iters>\n";
+               "report <config.json> [alpha] | bench_report <config.json> <iters> | frag <trace> [cap]\n";
   return 2;
 }
 
@@ -362,6 +362,23 @@ int main(int argc, char** argv) {
         auto inst = make_dsa_instance(extract_lifespans(trace).lifespans, cap, align);
         std::cout << dsa_result_json(solve_exact(inst, budget)).dump() << "\n";
       }
+      return 0;
+    }
+    if (op == "frag" && argc >= 3) {
+      // The reference CLI's `frag` (actmem.cpp:194-225) on a given trace: plan it,
+      // replay it through the caching-allocator simulator (capacity = plan + 10 %
+      // unless given) and through the static plan, and print the comparison.
+      auto trace = parse_trace(read_file(argv[2]));
+      GlobalPlan gp = plan_model(trace, 0, 60.0, 512);
+      const Bytes capacity = argc >= 4 ? std::stoull(argv[3]) : gp.total_peak + gp.total_peak / 10;
+      CachingAllocatorConfig acfg;
+      acfg.capacity = capacity;
+      FragReport caching = simulate_caching_allocator(trace, acfg, false);
+      FragReport planned = simulate_planned(trace, gp, 0, false);
+      Json j = to_json(compare(caching, planned));
+      j["capacity"] = capacity;
+      j["plan_total_peak"] = gp.total_peak;
+      std::cout << j.dump() << "\n";
       return 0;
     }
     if (op == "synth" && argc >= 3) {
