@@ -808,7 +808,9 @@ __global__ void __launch_bounds__(384, 1)
         for (int kk = 0; kk < TILE / 16; ++kk)
           dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
                              (j | kk) != 0);
-        dev::mma_commit_w(&o_done[g]);
+        // S_g(j+1) is issued after PV_g(j), so s_full already orders the
+        // softmax's O rescale after PV_g(j); o_done only serves the epilogue.
+        if (j == (g ? n_kv - 1 : nA - 1)) dev::mma_commit_w(&o_done[g]);
         if (g == 1) dev::mma_commit_w(&v_empty[st]);
       };
       issue_s(0, 0);
@@ -902,9 +904,7 @@ __global__ void __launch_bounds__(384, 1)
         dev::tmem_st32(t_s + 32, p1);
       }
       if (any && j > 0) {
-        // O_g must hold P(j-1)V(j-1) before it is rescaled
-        dev::mbar_wait(&o_done[g], (j - 1) & 1);
-        dev::tc_fence_after();
+        // O_g holds P(j-1)V(j-1): PV_g(j-1) completed before s_full_g(j) fired
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t o[32];
@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(384, 1)
       dev::tc_fence_before();
       dev::mbar_arrive(&p_full[g]);
     }
-    dev::mbar_wait(&o_done[g], (n_my - 1) & 1);
+    dev::mbar_wait(&o_done[g], 0);  // committed once, after the group's last PV
     dev::tc_fence_after();
     const float inv = 1.f / l;
     __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D;
