@@ -270,9 +270,11 @@ def main():
         except Exception as ex:  # noqa: BLE001
             print(f"[bench] SP+TP unavailable ({ex}); running replicas", file=sys.stderr)
             mode = "replicas"
-    cfg = P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
-                        batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True,
-                        tp_degree=world if mode == "tp" else 1)
+    def model_cfg():
+        return P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
+                             batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True,
+                             tp_degree=world if mode == "tp" else 1)
+    cfg = model_cfg()
     link = host_link_bandwidth(torch)
     host_mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
     gpus_on_node = max(torch.cuda.device_count(), world)
@@ -285,7 +287,25 @@ def main():
 
     # Calibrate: one step with the analytic layer time, then re-solve alpha with
     # the measured forward-layer time (swap.hpp:105 with SwapOptions.t_layer).
-    with Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, op_timing=0) as ex:
+    ex, err = None, None
+    try:
+        ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, op_timing=0)
+    except Exception as e:  # noqa: BLE001
+        err = e
+    if mode == "tp":  # every rank must agree before falling back (collective decision)
+        ok = torch.tensor([0 if err else 1], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            print(f"[bench] SP+TP executor unavailable ({err}); running replicas", file=sys.stderr)
+            if ex is not None:
+                ex.close()
+            mode, tp_spec = "replicas", None
+            cfg = model_cfg()
+            toks, labels = synthetic_batch(1234 + rank, V, S)
+            ex, err = Executor(cfg, hw, alpha=forced_alpha, op_timing=0), None
+    if err is not None:
+        raise err
+    with ex:
         ex.step(toks, labels)
         tl = ex.timeline()
     t_fwd = [e.end - e.start for e in tl if e.kind == "layer_fwd"]
