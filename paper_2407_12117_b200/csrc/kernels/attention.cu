@@ -949,281 +949,6 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-// ------------------------------------------------------------------ forward, 2 query tiles
-// Two adjacent query tiles (2p, 2p+1) of one head share every K/V tile load,
-// halving the L2->SMEM streaming that bounds the 1-tile kernel, and their
-// softmax groups ping-pong on the tensor pipe: while group A turns S_A(j)
-// into P_A(j), the pipe runs P_B(j-1)V + Q_B K(j)^T, and vice versa.
-// TMEM: S_A | S_B | O_A | O_B (P aliases its S).  The softmax makes two
-// passes over S in TMEM (max, then exp/pack) to stay within 170 registers.
-template <int D>
-struct Fwd2Smem {
-  static constexpr int NC = D / 64;
-  static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
-  static constexpr int QA_OFF = 0;
-  static constexpr int QB_OFF = TILE_BYTES;
-  static constexpr int K_OFF = 2 * TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;  // 2-stage K and V rings
-  static constexpr int BAR_OFF = V_OFF + 2 * TILE_BYTES;
-  static constexpr int BYTES = BAR_OFF + 256 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(384, 1)
-    attn_fwd2_kernel(const __grid_constant__ CUtensorMap map_q,
-                     const __grid_constant__ CUtensorMap map_k,
-                     const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
-                     float* __restrict__ lse, int S, int H, float scale_log2) {
-  using L = Fwd2Smem<D>;
-  constexpr int NC = L::NC;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;   // [2]
-  uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2] per group
-  uint64_t* p_full = bars + 11;  // [2] per group
-  uint64_t* o_done = bars + 13;  // [2] per group
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-
-  const int n_pairs = S / (2 * TILE);
-  const int pp = n_pairs - 1 - static_cast<int>(blockIdx.x);  // heavy pairs first
-  const int hh = blockIdx.y;
-  const int qt0 = 2 * pp;             // group A query tile; group B = qt0 + 1
-  const int n_kv = qt0 + 2;            // key tiles needed by group B; A uses n_kv - 1
-  const uint32_t warp = dev::warp_id();
-  const uint32_t lane = dev::lane_id();
-
-  if (warp == 0 && lane == 0) {
-    dev::tma_prefetch_desc(&map_q);
-    dev::tma_prefetch_desc(&map_k);
-    dev::tma_prefetch_desc(&map_v);
-    dev::mbar_init(q_full, 1);
-    for (int s2 = 0; s2 < 2; ++s2) {
-      dev::mbar_init(&k_full[s2], 1);
-      dev::mbar_init(&k_empty[s2], 1);
-      dev::mbar_init(&v_full[s2], 1);
-      dev::mbar_init(&v_empty[s2], 1);
-      dev::mbar_init(&s_full[s2], 1);
-      dev::mbar_init(&p_full[s2], 128);
-      dev::mbar_init(&o_done[s2], 1);
-    }
-    dev::fence_barrier_init();
-  }
-  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
-  dev::tc_fence_before();
-  __syncthreads();
-  dev::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // group g: S at g*128, O at 256 + g*D
-  if (warp == 0) {
-    if (lane == 0) {
-      dev::mbar_expect_tx(q_full, 2 * L::TILE_BYTES);
-      for (int c = 0; c < NC; ++c) {
-        dev::tma_load_2d(smem + L::QA_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, qt0 * TILE);
-        dev::tma_load_2d(smem + L::QB_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, (qt0 + 1) * TILE);
-      }
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        dev::mbar_wait(&k_empty[st], ph ^ 1);
-        dev::mbar_expect_tx(&k_full[st], L::TILE_BYTES);
-        for (int c = 0; c < NC; ++c)
-          dev::tma_load_2d(smem + L::K_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_k, &k_full[st],
-                           hh * D + c * 64, j * TILE);
-        dev::mbar_wait(&v_empty[st], ph ^ 1);
-        dev::mbar_expect_tx(&v_full[st], L::TILE_BYTES);
-        for (int c = 0; c < NC; ++c)
-          dev::tma_load_2d(smem + L::V_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_v, &v_full[st],
-                           hh * D + c * 64, j * TILE);
-      }
-    }
-  } else if (warp == 1) {
-    {  // whole warp, converged: MMAs/commits elect one lane
-      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
-      constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
-      const uint64_t qd[2] = {kmajor_base(dev::smem_u32(smem + L::QA_OFF)),
-                              kmajor_base(dev::smem_u32(smem + L::QB_OFF))};
-      dev::mbar_wait_w(q_full, 0);
-      // S_g(j) = Q_g K_j^T
-      auto issue_s = [&](int g, int j) {
-        const int st = j & 1;
-        if (g == 0) {  // group A issues first for every tile: wait for K here
-          dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
-          dev::tc_fence_after();
-        }
-        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss_w(tmem + g * 128, kmajor_step(qd[g], kk), kmajor_step(kd, kk), idesc_s, kk > 0);
-        dev::mma_commit_w(&s_full[g]);
-      };
-      // O_g += P_g(j) V_j
-      auto issue_pv = [&](int g, int j, int uses) {
-        const int st = j & 1;
-        dev::mbar_wait_w(&p_full[g], uses & 1);
-        if (g == 0 || j == n_kv - 1) {  // first PV of tile j waits for V
-          dev::mbar_wait_w(&v_full[st], (j >> 1) & 1);
-        }
-        dev::tc_fence_after();
-        const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
-#pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
-                           (uses | kk) != 0);
-        dev::mma_commit_w(&o_done[g]);
-      };
-      const int nA = n_kv - 1;
-      // the last key tile (diagonal of B) is never used by A: group B's K wait for it
-      auto issue_s_b_last = [&](int j) {
-        const int st = j & 1;
-        dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
-        dev::tc_fence_after();
-        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss_w(tmem + 128, kmajor_step(qd[1], kk), kmajor_step(kd, kk), idesc_s, kk > 0);
-        dev::mma_commit_w(&s_full[1]);
-      };
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        if (j < nA) {
-          issue_pv(0, j, j);
-          if (j + 1 < nA) issue_s(0, j + 1);
-        }
-        issue_pv(1, j, j);
-        dev::mma_commit_w(&k_empty[st]);
-        dev::mma_commit_w(&v_empty[st]);
-        if (j + 1 < n_kv) {
-          if (j + 1 < nA)
-            issue_s(1, j + 1);
-          else
-            issue_s_b_last(j + 1);
-        }
-      }
-    }
-  } else if (warp >= 4) {
-    const int g = (warp - 4) >> 2;  // softmax group: 0 -> tile A, 1 -> tile B
-    const uint32_t q4 = warp & 3;
-    const int row = q4 * 32 + lane;
-    const int qt = qt0 + g;
-    const int qidx = qt * TILE + row;
-    const int n_my = qt + 1;
-    const uint32_t lane_off = (q4 * 32) << 16;
-    const uint32_t t_s = tmem + g * 128 + lane_off;
-    const uint32_t t_o = tmem + 256 + g * D + lane_off;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_my; ++j) {
-      dev::mbar_wait(&s_full[g], j & 1);
-      dev::tc_fence_after();
-      const bool diag = j == qt;
-      // pass 1: row max of the raw logits
-      float mx8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        dev::tmem_ld32(t_s + c * 32, r);
-        dev::tmem_ld_wait_regs(r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float v = __uint_as_float(r[i]);
-          if (diag && c * 32 + i > row) v = -INFINITY;
-          mx8[i & 7] = fmaxf(mx8[i & 7], v);
-        }
-      }
-#pragma unroll
-      for (int k = 4; k > 0; k >>= 1)
-#pragma unroll
-        for (int q2 = 0; q2 < k; ++q2) mx8[q2] = fmaxf(mx8[q2], mx8[q2 + k]);
-      const float cand = fmaxf(m, mx8[0] * scale_log2);
-      const bool need = j == 0 || cand > m + kRescaleThreshold;
-      const bool any = __any_sync(0xffffffffu, need);
-      float factor = 1.f;
-      float m_new = m;
-      if (any) {
-        m_new = cand;
-        factor = j == 0 ? 0.f : dev::ex2(m - m_new);
-      }
-      // pass 2: P = 2^(s*scale - m) packed to bf16 over the S columns
-      float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        dev::tmem_ld32(t_s + c * 32, r);
-        dev::tmem_ld_wait_regs(r);
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float a = dev::ex2(fmaf(__uint_as_float(r[2 * i]), scale_log2, -m_new));
-          float b = dev::ex2(fmaf(__uint_as_float(r[2 * i + 1]), scale_log2, -m_new));
-          if (diag && c * 32 + 2 * i > row) a = 0.f;
-          if (diag && c * 32 + 2 * i + 1 > row) b = 0.f;
-          sum8[i & 7] += a + b;
-          pk[i] = dev::pack_bf16(a, b);
-        }
-        dev::tmem_st16(t_s + c * 16, pk);
-      }
-#pragma unroll
-      for (int k = 4; k > 0; k >>= 1)
-#pragma unroll
-        for (int q2 = 0; q2 < k; ++q2) sum8[q2] += sum8[q2 + k];
-      l = l * factor + sum8[0];
-      m = m_new;
-      if (any && j > 0) {
-        dev::mbar_wait(&o_done[g], (j - 1) & 1);
-        dev::tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t r[32];
-          dev::tmem_ld32(t_o + c * 32, r);
-          dev::tmem_ld_wait_regs(r);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * factor);
-          dev::tmem_st32(t_o + c * 32, r);
-        }
-      }
-      dev::tmem_st_wait();
-      dev::tc_fence_before();
-      dev::mbar_arrive(&p_full[g]);
-    }
-    dev::mbar_wait(&o_done[g], (n_my - 1) & 1);
-    dev::tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      dev::tmem_ld32(t_o + c * 32, r);
-      dev::tmem_ld_wait_regs(r);
-      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint4 u;
-        u.x = dev::pack_bf16(__uint_as_float(r[8 * i + 0]) * inv, __uint_as_float(r[8 * i + 1]) * inv);
-        u.y = dev::pack_bf16(__uint_as_float(r[8 * i + 2]) * inv, __uint_as_float(r[8 * i + 3]) * inv);
-        u.z = dev::pack_bf16(__uint_as_float(r[8 * i + 4]) * inv, __uint_as_float(r[8 * i + 5]) * inv);
-        u.w = dev::pack_bf16(__uint_as_float(r[8 * i + 6]) * inv, __uint_as_float(r[8 * i + 7]) * inv);
-        dst[i] = u;
-      }
-    }
-    lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(l)) * kLn2;
-    dev::tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    dev::tc_fence_after();
-    dev::tmem_dealloc(tmem, 512);
-  }
-}
-
 // ============================================================== backward
 // ndelta[h][t] = -sum_d dO*O ; nlse2[h][t] = -lse * log2(e)  (the delta / lse2 workspace)
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
@@ -2557,8 +2282,8 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   const float scale_log2 = a.softmax_scale * kLog2e;
   if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
-  // 0-3: one softmax warp per row (bit0 Q in TMEM, bit1 FMA exp2 share); 4: 2-tile two-pass;
-  // 5-7: split rows; 8-10: ping-pong two Q tiles (default 8)
+  // 0-3: one softmax warp per row (bit0 Q in TMEM, bit1 FMA exp2 share); 5-7: split rows;
+  // 8-10: ping-pong two Q tiles (default 8)
   const int v = fwd_variant();
   if (v >= 8 && a.D == 128 && a.S % (2 * TILE) == 0) {  // ping-pong (two Q tiles, setmaxnreg)
     // FMA-pipe exp2 share: 8 -> 1/4, 9 -> none, 10 -> 1/8
@@ -2582,25 +2307,6 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
     });
     auto kern = v == 5 ? attn_fwd_2w_kernel<4> : v == 7 ? attn_fwd_2w_kernel<8> : attn_fwd_2w_kernel<0>;
     kern<<<dim3(a.S / TILE, a.H), 384, Fwd2wSmem::BYTES, stream>>>(a.q, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
-  } else if (v == 4 && a.S % (2 * TILE) == 0) {
-    dim3 grid2(a.S / (2 * TILE), a.H);
-    if (a.D == 128) {
-      static std::once_flag f2;
-      std::call_once(f2, [] {
-        cudaFuncSetAttribute(attn_fwd2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Fwd2Smem<128>::BYTES);
-      });
-      attn_fwd2_kernel<128><<<grid2, 384, Fwd2Smem<128>::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
-                                                                         a.H, scale_log2);
-    } else {
-      static std::once_flag f2;
-      std::call_once(f2, [] {
-        cudaFuncSetAttribute(attn_fwd2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Fwd2Smem<64>::BYTES);
-      });
-      attn_fwd2_kernel<64><<<grid2, 384, Fwd2Smem<64>::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
-                                                                       a.H, scale_log2);
-    }
   } else if (a.D == 128) {
     switch (v) {
       case 0: launch_fwd<128, false, false>(a, mq, mk, mv, scale_log2, stream); break;
