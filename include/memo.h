@@ -296,10 +296,19 @@ typedef struct memo_loopback_group memo_loopback_group;
 memo_loopback_group* memo_comm_loopback_group(int32_t size);
 void memo_comm_loopback_group_destroy(memo_loopback_group* g);
 int memo_comm_unique_id(uint8_t out[128]);
-/* kind 0: loopback (handle = memo_loopback_group*), kind 1: NCCL (handle = unique id bytes) */
+/* kind 0: loopback (handle = memo_loopback_group*), kind 1: NCCL (handle = unique id bytes),
+ * kind 2: peer memory over CUDA IPC, one process per GPU (handle unused; call
+ *         memo_exec_peer_handle on every rank, exchange the bytes, then
+ *         memo_exec_peer_connect with all of them in rank order before the first step),
+ * kind 3: peer memory between t threads on one GPU (handle = memo_loopback_group*).
+ * Peer kinds run the fused all-gather->GEMM and GEMM->reduce-scatter paths. */
 int memo_exec_create_tp(const memo_model_config* cfg, const memo_hardware_config* hw,
                         const memo_exec_options* opt, int32_t kind, const void* handle,
                         int32_t rank, memo_exec** out);
+/* kind 2 bootstrap: this rank's handle (*len bytes; returns 2 if cap is too small). */
+int memo_exec_peer_handle(memo_exec* ctx, void* out, size_t cap, size_t* len);
+/* kind 2 bootstrap: all ranks' handles concatenated in rank order (t * len bytes). */
+int memo_exec_peer_connect(memo_exec* ctx, const void* all, size_t bytes);
 
 /* Synchronous copy of a named tensor (as memo_exec_tensor) into host memory. */
 int memo_exec_read(memo_exec* ctx, const char* name, int32_t layer, void* host, size_t bytes);

@@ -80,13 +80,17 @@ extern "C" int memo_exec_create_tp(const memo_model_config* cfg, const memo_hard
                                    const memo_exec_options* o, int32_t kind, const void* handle,
                                    int32_t rank, memo_exec** out) {
   return guard([&] {
-    if (!cfg || !hw || !o || !out || !handle) throw memo::ConfigError("null argument");
+    if (!cfg || !hw || !o || !out || (!handle && kind != 2)) throw memo::ConfigError("null argument");
     const int t = static_cast<int>(cfg->tp_degree);
     std::unique_ptr<memo::Comm> comm;
     if (kind == 0)
       comm = memo::make_loopback_comm(static_cast<const memo_loopback_group*>(handle)->g, rank);
     else if (kind == 1)
       comm = memo::make_nccl_comm(handle, rank, t);
+    else if (kind == 2)
+      comm = memo::make_ipc_comm(rank, t);
+    else if (kind == 3)
+      comm = memo::make_peer_local_comm(static_cast<const memo_loopback_group*>(handle)->g, rank);
     else
       throw memo::ConfigError("unknown communicator kind");
     auto* ctx = new memo_exec{nullptr};
@@ -97,6 +101,28 @@ extern "C" int memo_exec_create_tp(const memo_model_config* cfg, const memo_hard
       throw;
     }
     *out = ctx;
+  });
+}
+
+extern "C" int memo_exec_peer_handle(memo_exec* ctx, void* out, size_t cap, size_t* len) {
+  return guard([&] {
+    if (!ctx || !len) throw memo::ConfigError("null argument");
+    memo::Comm* c = ctx->ex->comm();
+    if (!c || c->handle_bytes() == 0) throw memo::ConfigError("executor has no IPC peer communicator (kind 2)");
+    *len = c->handle_bytes();
+    if (!out || cap < *len) throw memo::ConfigError("handle buffer too small");
+    c->export_handle(out);
+  });
+}
+
+extern "C" int memo_exec_peer_connect(memo_exec* ctx, const void* all, size_t bytes) {
+  return guard([&] {
+    if (!ctx || !all) throw memo::ConfigError("null argument");
+    memo::Comm* c = ctx->ex->comm();
+    if (!c || c->handle_bytes() == 0) throw memo::ConfigError("executor has no IPC peer communicator (kind 2)");
+    if (bytes != c->handle_bytes() * static_cast<size_t>(c->size()))
+      throw memo::ConfigError("expected tp_degree handles of memo_exec_peer_handle's length");
+    c->connect(all);
   });
 }
 

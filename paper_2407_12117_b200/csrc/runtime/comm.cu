@@ -1,5 +1,6 @@
 // comm.cu — NCCL (dlopen) and single-GPU loopback backends of runtime/comm.h.
 #include "runtime/comm.h"
+#include "runtime/loopback_group.h"
 
 #include <cuda_bf16.h>
 #include <dlfcn.h>
@@ -122,39 +123,6 @@ __global__ void loopback_reduce_kernel(SrcPtrs src, int n, size_t offset, size_t
 }
 
 }  // namespace
-
-struct LoopbackGroup {
-  explicit LoopbackGroup(int n) : size(n), send(n), ready(n), done(n) {
-    for (int k = 0; k < n; ++k) {
-      cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
-    }
-  }
-  ~LoopbackGroup() {
-    for (int k = 0; k < size; ++k) {
-      cudaEventDestroy(ready[k]);
-      cudaEventDestroy(done[k]);
-    }
-  }
-  void barrier() {
-    std::unique_lock<std::mutex> lk(mu);
-    const unsigned long long gen = generation;
-    if (++arrived == size) {
-      arrived = 0;
-      ++generation;
-      cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return generation != gen; });
-    }
-  }
-  int size;
-  std::vector<const void*> send;
-  std::vector<cudaEvent_t> ready, done;
-  std::mutex mu;
-  std::condition_variable cv;
-  int arrived = 0;
-  unsigned long long generation = 0;
-};
 
 namespace {
 

@@ -47,7 +47,30 @@ class Comm {
   // next chunk's GEMM runs, with a partial buffer of S/t rows instead of S.
   virtual void reduce(const void* send, void* recv, size_t count, CommDtype dt, int root,
                       cudaStream_t st) = 0;
+
+  // ---- peer memory (symmetric allocation), used by the fused GEMM+collective
+  // paths of the executor.  Every rank attaches ONE allocation of identical
+  // layout (the executor's single cudaMalloc), so a local pointer p maps to
+  // peer k's copy at peer_base[k] + (p - base).  Backends without peer memory
+  // (NCCL, loopback) keep the defaults and the executor uses the collectives.
+  virtual void attach(void* /*base*/, size_t /*bytes*/) {}
+  virtual bool peer_ready() const { return false; }
+  virtual void* peer_ptr(int /*k*/, const void* /*local*/) const { return nullptr; }
+  // Stream-ordered point-to-point signals on channel ch (< kPeerChannels): the
+  // n-th wait(src, ch) on a rank completes once src's n-th signal(dst, ch) to
+  // it has executed in stream order.  All signals of one (dst, ch) must be
+  // issued on one stream (device order == host order).
+  virtual void signal(int /*dst*/, int /*ch*/, cudaStream_t /*st*/) {}
+  virtual void wait(int /*src*/, int /*ch*/, cudaStream_t /*st*/) {}
+  // IPC bootstrap (multi-process peer backend): export this rank's handle
+  // after attach, then connect with every rank's handle (rank order).
+  virtual size_t handle_bytes() const { return 0; }
+  virtual void export_handle(void* /*out*/) const {}
+  virtual void connect(const void* /*all_handles*/) {}
 };
+
+constexpr int kPeerChannels = 8;
+constexpr int kMaxPeers = 8;
 
 // NCCL backend.  `unique_id` is the 128-byte ncclUniqueId produced by
 // memo_comm_unique_id on rank 0 and broadcast by the launcher.
@@ -59,5 +82,24 @@ bool nccl_get_unique_id(void* out128);
 struct LoopbackGroup;
 std::shared_ptr<LoopbackGroup> make_loopback_group(int size);
 std::unique_ptr<Comm> make_loopback_comm(std::shared_ptr<LoopbackGroup> g, int rank);
+
+// Peer-memory backends (runtime/peer.cu).  Collectives are pulls over peer
+// pointers (copy engine for gathers, a fixed-order reduction kernel for sums:
+// bitwise equal to the loopback backend), synchronised by stream-ordered
+// signals instead of NCCL:
+//   IPC    one process per GPU; the attached allocation and a 512-byte flag
+//          page are exported with cudaIpcGetMemHandle and mapped by every
+//          peer; signals are cuStreamWriteValue64 (release) into the peer's
+//          flag page and cuStreamWaitValue64 (>=) on the local one, so no SM
+//          spins and the host never blocks.
+//   local  t ranks as threads of one process on one GPU (testing the same
+//          algorithms on one B200): pointers are exchanged in-process and a
+//          signal is an event the receiver's stream waits on.
+std::unique_ptr<Comm> make_ipc_comm(int rank, int size);
+std::unique_ptr<Comm> make_peer_local_comm(std::shared_ptr<LoopbackGroup> g, int rank);
+
+// acc = first ? remote : acc + remote  (f32, count % 4 == 0, 16-byte aligned);
+// one pull step of the executor's staggered reduce-scatter.
+cudaError_t peer_accumulate(const float* remote, float* acc, size_t count, bool first, cudaStream_t st);
 
 }  // namespace memo

@@ -478,6 +478,14 @@ void Executor::allocate() {
   mk(ev_pre_mand_);
   mk(ev_pre_done_);
   ck(cudaEventCreate(&ev_start_), "event");
+  if (comm_ && d_.t > 1) {
+    comm_->attach(dev_, dev_bytes_);  // peer backends: the single allocation is the symmetric heap
+    ck(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking), "stream");
+    ev_blk_.resize(d_.t);
+    for (auto& e : ev_blk_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_cs2xs_, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_xs2cs_, cudaEventDisableTiming), "event");
+  }
 
   // RoPE table (cos, sin) in double -> f32, identical to the CPU oracle.
   std::vector<float2> cs(static_cast<size_t>(S) * (d_.D / 2));
@@ -542,8 +550,12 @@ Executor::~Executor() {
   if (cs_) cudaStreamSynchronize(cs_);
   if (os_) cudaStreamSynchronize(os_);
   if (ps_) cudaStreamSynchronize(ps_);
-  for (auto* v : {&ev_fwd_done_, &ev_bwd_done_, &ev_off_done_, &ev_pre_mand_, &ev_pre_done_, &ev_pool_})
+  if (xs_) cudaStreamSynchronize(xs_);
+  for (auto* v : {&ev_fwd_done_, &ev_bwd_done_, &ev_off_done_, &ev_pre_mand_, &ev_pre_done_, &ev_pool_, &ev_blk_})
     for (auto e : *v) cudaEventDestroy(e);
+  for (auto e : {ev_cs2xs_, ev_xs2cs_})
+    if (e) cudaEventDestroy(e);
+  if (xs_) cudaStreamDestroy(xs_);
   if (ev_start_) cudaEventDestroy(ev_start_);
   if (cs_) cudaStreamDestroy(cs_);
   if (os_) cudaStreamDestroy(os_);
@@ -935,20 +947,124 @@ inline void ag(Comm* c, const __nv_bfloat16* src, __nv_bfloat16* dst, size_t cou
 inline void rs(Comm* c, const float* src, float* dst, size_t count, cudaStream_t st) {
   c->reduce_scatter(src, dst, count, CommDtype::F32, st);
 }
+
+// Signal channels of the fused peer paths (0 and 1 belong to the collectives).
+constexpr int CH_AG_READY = 2;  // shard written (cs_ -> peers' xs_)
+constexpr int CH_AG_DONE = 3;   // peer finished pulling my shard (xs_ -> owner's cs_)
+constexpr int CH_RS_READY = 4;  // partial row block written (cs_ -> owner's xs_)
+constexpr int CH_RS_FREE = 5;   // owner finished pulling my partial (xs_ -> producer's cs_)
+
+// Rows [r0, r0 + m) of a GEMM whose A is K-major.
+GemmDesc rows_of(GemmDesc g, int r0, int m) {
+  g.a = static_cast<const char*>(g.a) + static_cast<Bytes>(r0) * g.lda * 2;
+  switch (g.epi) {
+    case GEMM_EPI_BF16:
+      g.c = static_cast<char*>(g.c) + static_cast<Bytes>(r0) * g.ldc * 2;
+      break;
+    case GEMM_EPI_F32:
+    case GEMM_EPI_F32_ACC:
+      g.c = static_cast<char*>(g.c) + static_cast<Bytes>(r0) * g.ldc * 4;
+      break;
+    case GEMM_EPI_QKV_ROPE:
+      g.q += static_cast<Bytes>(r0) * g.hidden;
+      g.k += static_cast<Bytes>(r0) * g.hidden;
+      g.v += static_cast<Bytes>(r0) * g.hidden;
+      g.pos0 += r0;
+      break;
+    default:
+      throw std::logic_error("rows_of: unsupported epilogue");
+  }
+  g.M = m;
+  return g;
+}
 }  // namespace
 
 void Executor::gemm_reduce_rows(GemmDesc g, float* part, float* out) {
-  const int t = d_.t, Sl = d_.Sl;
+  const int t = d_.t, Sl = d_.Sl, r = d_.r;
   const auto* a = static_cast<const __nv_bfloat16*>(g.a);
   const size_t count = static_cast<size_t>(Sl) * g.N;
   g.M = Sl;
   g.c = part;
   g.ldc = g.N;
-  for (int k = 0; k < t; ++k) {  // same per-row K order as one S-row GEMM: bitwise equal rows
-    g.a = a + static_cast<Bytes>(k) * Sl * g.lda;
-    gemm(g);
-    comm_->reduce(part, k == d_.r ? out : part, count, CommDtype::F32, k, cs_);
+  if (!peer()) {
+    for (int k = 0; k < t; ++k) {  // same per-row K order as one S-row GEMM: bitwise equal rows
+      g.a = a + static_cast<Bytes>(k) * Sl * g.lda;
+      gemm(g);
+      comm_->reduce(part, k == r ? out : part, count, CommDtype::F32, k, cs_);
+    }
+    return;
   }
+  // Staggered reduce-scatter over peer memory.  At step j rank r computes the
+  // partial of row block b = r-j-1 (mod t) into `part` while, on the comm
+  // stream, it pulls the partial of its OWN block from producer p = r+j+1 and
+  // accumulates it into `out`: every rank reads from a different peer at
+  // every step, so all links carry traffic at once (the row-chunked reduce
+  // above funnels each block into one root).  The own block comes last and is
+  // added by the GEMM epilogue itself (F32_ACC), so out = p_{r+1} + ... + p_{r-1}
+  // + p_r in a fixed order (bitwise the loopback sum for t = 2).
+  ck(cudaEventRecord(ev_cs2xs_, cs_), "record");
+  ck(cudaStreamWaitEvent(xs_, ev_cs2xs_, 0), "wait");  // previous readers of `out` are done
+  int prev = -1;  // owner of the block last written into `part`
+  for (int j = 0; j < t; ++j) {
+    const int b = ((r - j - 1) % t + t) % t;
+    if (b != r) {
+      if (prev >= 0) comm_->wait(prev, CH_RS_FREE, cs_);
+      GemmDesc gj = g;
+      gj.a = a + static_cast<Bytes>(b) * Sl * g.lda;
+      gemm(gj);
+      comm_->signal(b, CH_RS_READY, cs_);
+      prev = b;
+    }
+    const int p = (r + j + 1) % t;
+    if (p != r) {
+      comm_->wait(p, CH_RS_READY, xs_);
+      ck(peer_accumulate(static_cast<const float*>(comm_->peer_ptr(p, part)), out, count, j == 0, xs_),
+         "peer_accumulate");
+      comm_->signal(p, CH_RS_FREE, xs_);
+    }
+  }
+  ck(cudaEventRecord(ev_xs2cs_, xs_), "record");
+  ck(cudaStreamWaitEvent(cs_, ev_xs2cs_, 0), "wait");
+  GemmDesc go = g;  // own block: out += p_r in the epilogue
+  go.a = a + static_cast<Bytes>(r) * Sl * g.lda;
+  go.c = out;
+  go.epi = GEMM_EPI_F32_ACC;
+  gemm(go);
+  if (prev >= 0) comm_->wait(prev, CH_RS_FREE, cs_);  // `part` may be rewritten after this
+  stats_.kernel_launches += t - 1;
+}
+
+void Executor::gather_gemm(const __nv_bfloat16* shard, __nv_bfloat16* full, GemmDesc g, int row0) {
+  const int t = d_.t, Sl = d_.Sl, r = d_.r, S = d_.S;
+  const size_t shard_elems = static_cast<size_t>(Sl) * g.K;
+  if (!peer()) {
+    ag(comm_.get(), shard, full, shard_elems, cs_);
+    if (row0 < S) gemm(rows_of(g, row0, S - row0));
+    return;
+  }
+  for (int k = 0; k < t; ++k)
+    if (k != r) comm_->signal(k, CH_AG_READY, cs_);
+  ck(cudaEventRecord(ev_cs2xs_, cs_), "record");
+  ck(cudaStreamWaitEvent(xs_, ev_cs2xs_, 0), "wait");  // own shard written, `full` free
+  const Bytes blk = shard_elems * 2;
+  for (int j = 0; j < t; ++j) {
+    const int k = (r + j) % t;
+    if (k != r) comm_->wait(k, CH_AG_READY, xs_);
+    const void* src = k == r ? static_cast<const void*>(shard) : comm_->peer_ptr(k, shard);
+    ck(cudaMemcpyAsync(reinterpret_cast<char*>(full) + k * blk, src, blk, cudaMemcpyDeviceToDevice, xs_),
+       "peer gather copy");
+    ck(cudaEventRecord(ev_blk_[j], xs_), "record");
+  }
+  for (int k = 0; k < t; ++k)
+    if (k != r) comm_->signal(k, CH_AG_DONE, xs_);
+  for (int j = 0; j < t; ++j) {
+    const int k = (r + j) % t;
+    ck(cudaStreamWaitEvent(cs_, ev_blk_[j], 0), "wait");
+    const int lo = std::max(row0, k * Sl), hi = (k + 1) * Sl;
+    if (lo < hi) gemm(rows_of(g, lo, hi - lo));
+  }
+  for (int k = 0; k < t; ++k)
+    if (k != r) comm_->wait(k, CH_AG_DONE, cs_);  // nobody reads my shard any more
 }
 
 void Executor::layer_fwd_tp(int i) {
@@ -979,17 +1095,15 @@ void Executor::layer_fwd_tp(int i) {
   const size_t shard = static_cast<size_t>(Sl) * h;
 
   G(rmsnorm_fwd(X, nullptr, P("g1"), XN, Sl, h, opt_.eps, cs_));
-  ag(comm_.get(), XN, xn_full, shard, cs_);
   GemmDesc g = gd(S, 3 * hl, h, xn_full, h, 0, P("wqkv"), h, 0, GEMM_EPI_QKV_ROPE, nullptr, 0);
   g.q = Q; g.k = K; g.v = Vv; g.hidden = hl; g.head_dim = D; g.rope = rope_; g.pos0 = 0;
-  gemm(g);
+  gather_gemm(XN, xn_full, g, 0);
   AttnFwdArgs fa{Q, K, Vv, O, LSE, S, Hl, D, 1.0f / std::sqrt(static_cast<float>(D))};
   attention_fwd(fa);
   gemm_reduce_rows(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, nullptr, h), a_part, a_red);
   G(resid_round(X, a_red, A, x1, static_cast<long long>(shard), cs_));
   G(rmsnorm_fwd(x1, nullptr, P("g2"), XN2, Sl, h, opt_.eps, cs_));
-  ag(comm_.get(), XN2, xn2_full, shard, cs_);
-  gemm(gd(S, 2 * Fl, h, xn2_full, h, 0, P("wgu"), h, 0, GEMM_EPI_BF16, GU, 2 * Fl));
+  gather_gemm(XN2, xn2_full, gd(S, 2 * Fl, h, xn2_full, h, 0, P("wgu"), h, 0, GEMM_EPI_BF16, GU, 2 * Fl), 0);
   G(swiglu_fwd(GU, ACT, S, Fl, cs_));
   gemm_reduce_rows(gd(S, h, Fl, ACT, Fl, 0, P("wd"), Fl, 0, GEMM_EPI_F32, nullptr, h), d_part, d_red);
   float* out = i + 1 < d_.n ? reinterpret_cast<float*>(comp(i + 1, C_X))
@@ -1003,7 +1117,7 @@ void Executor::layer_fwd_tp(int i) {
 }
 
 void Executor::layer_recompute_tp(int i) {
-  const int S = d_.S, Sl = d_.Sl, h = d_.h, hl = d_.hl, Fl = d_.Fl, D = d_.D;
+  const int S = d_.S, h = d_.h, hl = d_.hl, Fl = d_.Fl, D = d_.D;
   const int sw = static_cast<int>(split_.swap_tokens), R = static_cast<int>(split_.recompute_tokens);
   const int swl = static_cast<int>(split_l_.swap_tokens), Rl = static_cast<int>(split_l_.recompute_tokens);
   G(cudaStreamWaitEvent(cs_, ev_pre_mand_[i], 0));  // B3 (+ prefetch-before-recompute)
@@ -1027,18 +1141,13 @@ void Executor::layer_recompute_tp(int i) {
     float* a_red = static_cast<float*>(A_("r_a_red"));
     float* x1 = static_cast<float*>(A_("r_x1"));
     auto* xn2_full = static_cast<__nv_bfloat16*>(A_("r_xn2_full"));
-    const size_t shard = static_cast<size_t>(Sl) * h;
     const Bytes r0 = static_cast<Bytes>(swl);
     // local suffix rows of the input norm, then the full gathered input
     if (Rl > 0) G(rmsnorm_fwd(X + r0 * h, nullptr, P("g1"), XN + r0 * h, Rl, h, opt_.eps, cs_));
-    ag(comm_.get(), XN, xn_full, shard, cs_);
-    if (R > 0) {
-      GemmDesc g = gd(R, 3 * hl, h, xn_full + static_cast<Bytes>(sw) * h, h, 0, P("wqkv"), h, 0,
-                      GEMM_EPI_QKV_ROPE, nullptr, 0);
-      g.q = Q + static_cast<Bytes>(sw) * hl; g.k = K + static_cast<Bytes>(sw) * hl;
-      g.v = Vv + static_cast<Bytes>(sw) * hl;
-      g.hidden = hl; g.head_dim = D; g.rope = rope_; g.pos0 = sw;
-      gemm(g);
+    {
+      GemmDesc g = gd(S, 3 * hl, h, xn_full, h, 0, P("wqkv"), h, 0, GEMM_EPI_QKV_ROPE, nullptr, 0);
+      g.q = Q; g.k = K; g.v = Vv; g.hidden = hl; g.head_dim = D; g.rope = rope_; g.pos0 = 0;
+      gather_gemm(XN, xn_full, g, sw);  // suffix rows [sw, S) only
     }
     // attn_proj needs every rank's partial: redo the out-projection + RS exactly as forward
     gemm_reduce_rows(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, nullptr, h), a_part, a_red);
@@ -1047,10 +1156,8 @@ void Executor::layer_recompute_tp(int i) {
                     static_cast<long long>(Rl) * h, cs_));
       G(rmsnorm_fwd(x1 + r0 * h, nullptr, P("g2"), XN2 + r0 * h, Rl, h, opt_.eps, cs_));
     }
-    ag(comm_.get(), XN2, xn2_full, shard, cs_);
+    gather_gemm(XN2, xn2_full, gd(S, 2 * Fl, h, xn2_full, h, 0, P("wgu"), h, 0, GEMM_EPI_BF16, GU, 2 * Fl), sw);
     if (R > 0) {
-      gemm(gd(R, 2 * Fl, h, xn2_full + static_cast<Bytes>(sw) * h, h, 0, P("wgu"), h, 0,
-              GEMM_EPI_BF16, GU + static_cast<Bytes>(sw) * 2 * Fl, 2 * Fl));
       G(swiglu_fwd(GU + static_cast<Bytes>(sw) * 2 * Fl, ACT + static_cast<Bytes>(sw) * Fl, R, Fl, cs_));
     }
     stats_.kernel_launches += 5;
@@ -1098,8 +1205,7 @@ void Executor::layer_bwd_tp(int i) {
   const size_t shard = static_cast<size_t>(Sl) * h;
 
   // MLP (down is row-parallel: its input gradient is the gathered output grad)
-  ag(comm_.get(), dxb, dy_full, shard, cs_);
-  gemm(gd(S, Fl, h, dy_full, h, 0, P("wd"), Fl, 1, GEMM_EPI_BF16, dact, Fl));
+  gather_gemm(dxb, dy_full, gd(S, Fl, h, dy_full, h, 0, P("wd"), Fl, 1, GEMM_EPI_BF16, dact, Fl), 0);
   gemm(gd(h, Fl, S, dy_full, h, 1, ACT, Fl, 1, GEMM_EPI_F32, Gr("wd"), Fl));
   G(swiglu_bwd(GU, dact, dgu, S, Fl, cs_));
   gemm_reduce_rows(gd(S, h, 2 * Fl, dgu, 2 * Fl, 0, P("wgu"), h, 1, GEMM_EPI_F32, nullptr, h), dxn2_part, dxn2);
@@ -1107,8 +1213,7 @@ void Executor::layer_bwd_tp(int i) {
   gemm(gd(2 * Fl, h, S, dgu, 2 * Fl, 1, xn2_full, h, 1, GEMM_EPI_F32, Gr("wgu"), h));
   G(rmsnorm_bwd(X, A, P("g2"), dxn2, dxc, dxc, da, part2, Gr("g2"), Sl, h, opt_.eps, false, cs_));
   // attention output projection (row-parallel)
-  ag(comm_.get(), da, da_full, shard, cs_);
-  gemm(gd(S, hl, h, da_full, h, 0, P("wo"), hl, 1, GEMM_EPI_BF16, dout, hl));
+  gather_gemm(da, da_full, gd(S, hl, h, da_full, h, 0, P("wo"), hl, 1, GEMM_EPI_BF16, dout, hl), 0);
   gemm(gd(h, hl, S, da_full, h, 1, O, hl, 1, GEMM_EPI_F32, Gr("wo"), hl));
   AttnBwdArgs ba;
   ba.q = Q; ba.k = K; ba.v = Vv; ba.o = O; ba.lse = LSE; ba.dout = dout; ba.delta = ws;

@@ -104,6 +104,7 @@ class Executor {
   bool tensor(const std::string& name, int layer, void** ptr, size_t* bytes) const;
   bool swap_enabled() const { return swap_on_; }
   void* stream() const { return cs_; }
+  Comm* comm() const { return comm_.get(); }
 
  private:
   struct Buf {
@@ -137,6 +138,13 @@ class Executor {
   // sequence reduce-scatter, one rank's row block at a time: part holds S/t
   // rows; rank k's block is reduced onto rank k's out.
   void gemm_reduce_rows(GemmDesc g, float* part, float* out);
+  // Sequence all-gather of `shard` ([S/t, K] bf16) into `full` ([S, K]) fused
+  // with the column-parallel GEMM g (A = full, rows [row0, S)).  On a peer
+  // backend the row blocks are pulled by the copy engine on the comm stream
+  // (own block first) and the GEMM of block k starts as soon as k has landed;
+  // otherwise it is the collective followed by one GEMM.
+  void gather_gemm(const __nv_bfloat16* shard, __nv_bfloat16* full, GemmDesc g, int row0);
+  bool peer() const { return comm_ && comm_->peer_ready(); }
   void attention_fwd(AttnFwdArgs a);
   void attention_bwd(AttnBwdArgs a);
   struct OpMark {
@@ -188,6 +196,9 @@ class Executor {
 
   // streams / events
   cudaStream_t cs_ = nullptr, os_ = nullptr, ps_ = nullptr;
+  cudaStream_t xs_ = nullptr;  // peer-collective stream (pulls overlapped with the GEMMs on cs_)
+  std::vector<cudaEvent_t> ev_blk_;  // per row block landed (xs_ -> cs_)
+  cudaEvent_t ev_cs2xs_ = nullptr, ev_xs2cs_ = nullptr;
   cudaEvent_t ev_start_ = nullptr;
   std::vector<cudaEvent_t> ev_fwd_done_, ev_bwd_done_, ev_off_done_, ev_pre_mand_, ev_pre_done_;
   struct Mark {

@@ -46,6 +46,8 @@ lib.memo_comm_loopback_group_destroy.argtypes = [C.c_void_p]
 lib.memo_exec_stream.restype = C.c_void_p
 lib.memo_exec_stream.argtypes = [C.c_void_p]
 lib.memo_exec_destroy.argtypes = [C.c_void_p]
+lib.memo_exec_peer_handle.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+lib.memo_exec_peer_connect.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
 
 
 def default_options() -> ExecOptionsC:
@@ -58,8 +60,11 @@ class Executor:
     """One B200 training-step context (arena, rounding buffers, copy streams)."""
 
     def __init__(self, cfg: ModelConfig, hw: HardwareConfig, tp=None, **options):
-        """tp: None (single GPU) or (kind, handle, rank) with kind 0 = LoopbackGroup,
-        kind 1 = 128-byte NCCL unique id; cfg.tp_degree is the group size."""
+        """tp: None (single GPU) or (kind, handle, rank); cfg.tp_degree is the group size.
+        kind 0 (KIND_LOOPBACK) = LoopbackGroup, 1 (KIND_NCCL) = 128-byte NCCL unique id,
+        2 (KIND_IPC) = peer memory over CUDA IPC (handle None; then exchange
+        peer_handle() bytes and call peer_connect), 3 (KIND_PEER_LOCAL) = peer
+        memory between the threads of a LoopbackGroup on one GPU."""
         o = default_options()
         for k, v in options.items():
             if not hasattr(o, k):
@@ -72,9 +77,26 @@ class Executor:
                                        C.byref(self._h)))
         else:
             kind, handle, rank = tp
-            h = handle.ptr if isinstance(handle, LoopbackGroup) else C.c_char_p(bytes(handle))
+            if isinstance(handle, LoopbackGroup):
+                h = handle.ptr
+            elif handle is None:
+                h = None
+            else:
+                h = C.c_char_p(bytes(handle))
             check(lib.memo_exec_create_tp(C.byref(cfg.to_c()), C.byref(hw.to_c()), C.byref(o),
                                           kind, h, rank, C.byref(self._h)))
+
+    def peer_handle(self) -> bytes:
+        """This rank's CUDA IPC handle bytes (kind 2)."""
+        n = C.c_size_t()
+        buf = (C.c_uint8 * 512)()
+        check(lib.memo_exec_peer_handle(self._h, buf, C.c_size_t(512), C.byref(n)))
+        return bytes(buf[:n.value])
+
+    def peer_connect(self, handles) -> None:
+        """Map every rank's allocation (handles in rank order, kind 2)."""
+        blob = b"".join(handles)
+        check(lib.memo_exec_peer_connect(self._h, C.c_char_p(blob), C.c_size_t(len(blob))))
 
     def close(self):
         if self._h:
@@ -175,6 +197,9 @@ class Executor:
         check(lib.memo_exec_read(self._h, name.encode(), layer, out.ctypes.data_as(C.c_void_p),
                                  C.c_size_t(nbytes)))
         return out
+
+
+KIND_LOOPBACK, KIND_NCCL, KIND_IPC, KIND_PEER_LOCAL = 0, 1, 2, 3
 
 
 class LoopbackGroup:

@@ -8,7 +8,8 @@ import pytest
 
 from oracle import oracle as O
 from paper_2407_12117_b200 import planner as P
-from paper_2407_12117_b200.executor import Executor, LoopbackGroup, run_ranks
+from paper_2407_12117_b200.executor import (KIND_LOOPBACK, KIND_PEER_LOCAL, Executor, LoopbackGroup,
+                                            run_ranks)
 
 pytestmark = pytest.mark.gpu
 
@@ -45,11 +46,11 @@ def assemble(ocfg, shards, t, get):
     return np.concatenate(parts)
 
 
-def run_tp(cfg, t, toks, labels, **opts):
+def run_tp(cfg, t, toks, labels, kind=KIND_LOOPBACK, **opts):
     g = LoopbackGroup(t)
 
     def rank(r):
-        with Executor(cfg, HW, tp=(0, g, r), **opts) as ex:
+        with Executor(cfg, HW, tp=(kind, g, r), **opts) as ex:
             params = {(n, l): ex.read(n, l, dtype="bf16") for n, l, _, _ in O.layout(ocfg_of(cfg))}
             loss = ex.step(toks, labels)
             grads = {(n, l): ex.read("grad/" + n, l) for n, l, _, _ in O.layout(ocfg_of(cfg))}
@@ -63,18 +64,18 @@ def ocfg_of(cfg):
                       cfg.seq_len)
 
 
-@pytest.mark.parametrize("alpha", [0.5])
-def test_tp2_matches_oracle(alpha):
-    n, h, H, F, V, S, t = 4, 256, 2, 768, 512, 512, 2
+@pytest.mark.parametrize("t,kind", [(2, KIND_LOOPBACK), (2, KIND_PEER_LOCAL), (4, KIND_PEER_LOCAL)])
+def test_tp_matches_oracle(t, kind):
+    n, h, H, F, V, S = 4, 256, 4, 768, 512, 1024
     cfg = model(n, h, H, F, V, S, t)
     ocfg = ocfg_of(cfg)
     params = O.init_params(ocfg, 1234)
     toks, labels = O.tokens(1234, V, S)
-    res = run_tp(cfg, t, toks, labels, seed=1234, alpha=alpha, optimizer=0, ce_chunk=256)
+    res = run_tp(cfg, t, toks, labels, kind=kind, seed=1234, alpha=0.5, optimizer=0, ce_chunk=256)
     full_params = assemble(ocfg, None, t, lambda r, n_, l_: res[r][1][(n_, l_)])
     assert np.array_equal(full_params, params), "sharded init differs from slices of the full model"
     losses = [r[0] for r in res]
-    assert losses[0] == losses[1]
+    assert all(x == losses[0] for x in losses)
     ref_loss, ref = O.step(ocfg, params, toks, labels)
     assert abs(losses[0] - ref_loss) <= 5e-3 * abs(ref_loss), (losses, ref_loss)
     grads = assemble(ocfg, None, t, lambda r, n_, l_: res[r][2][(n_, l_)])
@@ -87,13 +88,28 @@ def test_tp2_matches_oracle(alpha):
         assert P.validate_schedule(res[r][3], n, res[r][4]["swap"]) == []
 
 
-def test_tp2_swap_bitwise_equals_no_swap():
-    n, h, H, F, V, S, t = 4, 256, 2, 768, 512, 1024, 2
+@pytest.mark.parametrize("t,kind", [(2, KIND_LOOPBACK), (4, KIND_PEER_LOCAL)])
+def test_tp_swap_bitwise_equals_no_swap(t, kind):
+    n, h, H, F, V, S = 4, 256, 4, 768, 512, 1024
     cfg = model(n, h, H, F, V, S, t)
     toks, labels = O.tokens(77, V, S)
-    on = run_tp(cfg, t, toks, labels, seed=9, alpha=0.5, optimizer=0, ce_chunk=512, swap_enabled=1)
-    off = run_tp(cfg, t, toks, labels, seed=9, alpha=0.5, optimizer=0, ce_chunk=512, swap_enabled=0)
+    on = run_tp(cfg, t, toks, labels, kind=kind, seed=9, alpha=0.5, optimizer=0, ce_chunk=512, swap_enabled=1)
+    off = run_tp(cfg, t, toks, labels, kind=kind, seed=9, alpha=0.5, optimizer=0, ce_chunk=512, swap_enabled=0)
     for r in range(t):
         assert on[r][0] == off[r][0]
         for k in on[r][2]:
             assert np.array_equal(on[r][2][k], off[r][2][k]), k
+
+
+def test_tp2_peer_paths_bitwise_equal_loopback():
+    """For t = 2 the staggered reduce-scatter sums p_{r+1} + p_r, the loopback
+    reduce p_0 + p_1: the same IEEE sums, so every result is bitwise equal."""
+    n, h, H, F, V, S, t = 4, 256, 4, 768, 512, 1024, 2
+    cfg = model(n, h, H, F, V, S, t)
+    toks, labels = O.tokens(5, V, S)
+    a = run_tp(cfg, t, toks, labels, kind=KIND_LOOPBACK, seed=3, alpha=0.5, optimizer=0, ce_chunk=512)
+    b = run_tp(cfg, t, toks, labels, kind=KIND_PEER_LOCAL, seed=3, alpha=0.5, optimizer=0, ce_chunk=512)
+    for r in range(t):
+        assert a[r][0] == b[r][0]
+        for k in a[r][2]:
+            assert np.array_equal(a[r][2][k], b[r][2][k]), (r, k)
