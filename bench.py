@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="SP+TP collectives: peer memory over CUDA IPC (fused AG->GEMM / GEMM->RS) or NCCL")
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
                     help="N>1: Megatron SP+TP over NCCL (strong scaling of one sequence) or "
                          "independent replicas (weak scaling)")
@@ -249,27 +251,49 @@ def main():
 
     import numpy as np
     import torch
-    torch.cuda.set_device(local)
+    # more ranks than GPUs (a test of the multi-process path on a one-GPU box):
+    # ranks share devices, the process group runs on gloo, and only the
+    # peer-memory (CUDA IPC) communicator works -- NCCL rejects shared devices
+    shared_gpu = world > torch.cuda.device_count()
+    torch.cuda.set_device(local % torch.cuda.device_count())
     dist = None
+    ddev = "cpu" if shared_gpu else "cuda"  # device of the small control tensors
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_12117_b200 import planner as P
     from paper_2407_12117_b200.executor import Executor
 
     n, h, H, inter, V, S, desc = CONFIGS[args.config]
     mode = "single" if world == 1 else args.parallel
     tp_spec = None
-    if mode == "tp":
-        # one NCCL communicator for the SP+TP group; fall back to replicas if it cannot start
+    from paper_2407_12117_b200.executor import KIND_IPC, KIND_NCCL
+    comm = args.comm
+
+    def nccl_spec():
         from paper_2407_12117_b200.executor import nccl_unique_id
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        return (KIND_NCCL, uid[0], rank)
+
+    if mode == "tp":
+        # peer memory over CUDA IPC (default) or one NCCL communicator for the SP+TP
+        # group; fall back to NCCL, then to replicas, if it cannot start
         try:
-            uid = [nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            tp_spec = (1, uid[0], rank)
+            tp_spec = (KIND_IPC, None, rank) if comm == "peer" else nccl_spec()
         except Exception as ex:  # noqa: BLE001
             print(f"[bench] SP+TP unavailable ({ex}); running replicas", file=sys.stderr)
             mode = "replicas"
+
+    def connect(e):
+        """kind 2: exchange the CUDA IPC handles and map every rank's allocation."""
+        if tp_spec is not None and tp_spec[0] == KIND_IPC:
+            hs = [None] * world
+            dist.all_gather_object(hs, e.peer_handle())
+            e.peer_connect(hs)
     def model_cfg():
         return P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
                              batch=1, seq_len=S, dtype_bytes=2, untied_classifier=True,
@@ -280,7 +304,7 @@ def main():
     gpus_on_node = max(torch.cuda.device_count(), world)
     cpu_mem = int(min(host_mem * 0.6 / gpus_on_node, 2 ** 40))  # per-GPU pinned budget
     hw = P.HardwareConfig(pcie_bandwidth=link["d2h"], cpu_mem=cpu_mem,
-                          gpu_mem=torch.cuda.get_device_properties(local).total_memory,
+                          gpu_mem=torch.cuda.get_device_properties(local % torch.cuda.device_count()).total_memory,
                           peak_flops=B200_SPEC_BF16, efficiency=0.5)
     toks, labels = synthetic_batch(1234 + (rank if mode == "replicas" else 0), V, S)
     forced_alpha = 0.5 if args.config == "cfg1p" else -1.0
@@ -292,8 +316,28 @@ def main():
         ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, op_timing=0)
     except Exception as e:  # noqa: BLE001
         err = e
+    if mode == "tp" and tp_spec[0] == KIND_IPC:  # collective decision: IPC, else NCCL
+        ok = torch.tensor([0 if err else 1], device=ddev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 1:
+            try:
+                connect(ex)
+            except Exception as e:  # noqa: BLE001
+                err = e
+            ok = torch.tensor([0 if err else 1], device=ddev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            print(f"[bench] peer-memory SP+TP unavailable ({err}); using NCCL", file=sys.stderr)
+            if ex is not None:
+                ex.close()
+            comm, err, ex = "nccl", None, None
+            tp_spec = nccl_spec()
+            try:
+                ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, op_timing=0)
+            except Exception as e:  # noqa: BLE001
+                err = e
     if mode == "tp":  # every rank must agree before falling back (collective decision)
-        ok = torch.tensor([0 if err else 1], device="cuda")
+        ok = torch.tensor([0 if err else 1], device=ddev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if ok.item() == 0:
             print(f"[bench] SP+TP executor unavailable ({err}); running replicas", file=sys.stderr)
@@ -311,12 +355,13 @@ def main():
     t_fwd = [e.end - e.start for e in tl if e.kind == "layer_fwd"]
     t_layer = float(np.median(t_fwd))
     if dist:  # SPMD: every rank solves alpha from the same (slowest) layer time
-        tt = torch.tensor([t_layer], device="cuda")
+        tt = torch.tensor([t_layer], device=ddev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_layer = tt.item()
     torch.cuda.synchronize()
     free0, _ = torch.cuda.mem_get_info()
     ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, t_layer=t_layer, op_timing=1)
+    connect(ex)
     free1, _ = torch.cuda.mem_get_info()
     info0 = ex.info()
     stream = torch.cuda.ExternalStream(ex.stream)
@@ -342,7 +387,7 @@ def main():
     launches = info["kernel_launches"] * args.steps
     t_max = ms
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=ddev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = t.item()
     seqs = world if mode == "replicas" else 1  # sequences processed by the job per step
@@ -359,7 +404,7 @@ def main():
         e2e_ms.append(a.elapsed_time(b))
     e2e = statistics.mean(e2e_ms)
     if dist:
-        t = torch.tensor([e2e], device="cuda")
+        t = torch.tensor([e2e], device=ddev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = t.item()
 
@@ -395,7 +440,7 @@ def main():
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (splitmix64 tokens, counter-hash random-init weights)",
         "config": {"workload": desc, "model": "llama-7b-arch", "n_layers": n, "global_batch": world,
-                   "seq_len": S, "parallelism": {"single": "single", "tp": f"sp+tp{world}",
+                   "seq_len": S, "parallelism": {"single": "single", "tp": f"sp+tp{world} ({comm})",
                                                  "replicas": f"replicas{world}"}[mode],
                    "l2": "working set (GB of activations) >> 126 MB L2; no flush needed",
                    "alpha": swap.alpha, "swap_tokens": info0["split"][0],
