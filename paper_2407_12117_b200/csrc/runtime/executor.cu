@@ -27,6 +27,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -475,6 +477,7 @@ void Executor::allocate() {
   mk(ev_fwd_done_);
   mk(ev_bwd_done_);
   mk(ev_off_done_);
+  mk(ev_off_x_);
   mk(ev_pre_mand_);
   mk(ev_pre_done_);
   ck(cudaEventCreate(&ev_start_), "event");
@@ -551,7 +554,7 @@ Executor::~Executor() {
   if (os_) cudaStreamSynchronize(os_);
   if (ps_) cudaStreamSynchronize(ps_);
   if (xs_) cudaStreamSynchronize(xs_);
-  for (auto* v : {&ev_fwd_done_, &ev_bwd_done_, &ev_off_done_, &ev_pre_mand_, &ev_pre_done_, &ev_pool_, &ev_blk_})
+  for (auto* v : {&ev_fwd_done_, &ev_bwd_done_, &ev_off_done_, &ev_off_x_, &ev_pre_mand_, &ev_pre_done_, &ev_pool_, &ev_blk_})
     for (auto e : *v) cudaEventDestroy(e);
   for (auto e : {ev_cs2xs_, ev_xs2cs_})
     if (e) cudaEventDestroy(e);
@@ -726,6 +729,7 @@ void Executor::offload(int i) {
     moved += b;
   };
   put(C_X, sk_.components[C_X].second);
+  ck(cudaEventRecord(ev_off_x_[i], os_), "record");  // layer_input out: RB(i) may take layer i+2's input
   put(C_O, sk_.components[C_O].second);
   for (int c = 0; c < C_N; ++c)
     if (c != C_X && c != C_O) put(c, split_of(c).swap_tokens * row_bytes_[c]);
@@ -794,7 +798,11 @@ void Executor::layer_fwd(int i) {
   G(swiglu_fwd(GU, ACT, S, F, cs_));
   float* out = i + 1 < d_.n ? reinterpret_cast<float*>(comp(i + 1, C_X))
                             : static_cast<float*>(arena_ptr(seg_emb_fwd_, "x_final"));
-  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 1], 0));  // RB drained
+  // The output is layer i+1's input, in the rounding buffer layer i-1 is still
+  // being offloaded from.  Only the layer_input rows must have left (they are
+  // copied first); everything else of RB(i+1) is written by fwd(i+1), which F3
+  // holds until offload(i-1) is complete.
+  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_x_[i - 1], 0));
   g = gd(S, h, F, ACT, F, 0, P("wd"), F, 0, GEMM_EPI_RESID, nullptr, 0);
   g.out_f32 = out; g.resid = x1; g.ld_f32 = h;
   gemm(g);
@@ -1108,7 +1116,11 @@ void Executor::layer_fwd_tp(int i) {
   gemm_reduce_rows(gd(S, h, Fl, ACT, Fl, 0, P("wd"), Fl, 0, GEMM_EPI_F32, nullptr, h), d_part, d_red);
   float* out = i + 1 < d_.n ? reinterpret_cast<float*>(comp(i + 1, C_X))
                             : static_cast<float*>(arena_ptr(seg_emb_fwd_, "x_final"));
-  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_done_[i - 1], 0));  // RB drained
+  // The output is layer i+1's input, in the rounding buffer layer i-1 is still
+  // being offloaded from.  Only the layer_input rows must have left (they are
+  // copied first); everything else of RB(i+1) is written by fwd(i+1), which F3
+  // holds until offload(i-1) is complete.
+  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_x_[i - 1], 0));
   G(resid_round(x1, d_red, nullptr, out, static_cast<long long>(shard), cs_));
   stats_.kernel_launches += 5;
   mark(0, static_cast<int>(Kind::LayerFwd), i, false);
@@ -1390,6 +1402,23 @@ Timeline Executor::timeline() const {
     st.op_ms[o.cls] += ms;
     st.op_flops[o.cls] += o.flops;
     st.op_count[o.cls] += 1;
+  }
+  // Diagnostics: MEMO_OP_TRACE=<file> appends every timed op (class, start, end in
+  // ms from step start) and every timeline event, for gap analysis of the step.
+  if (const char* path = std::getenv("MEMO_OP_TRACE")) {
+    if (FILE* f = std::fopen(path, "a")) {
+      for (const OpMark& o : ops_) {
+        float a = 0, b = 0;
+        ck(cudaEventElapsedTime(&a, ev_start_, o.a), "elapsed");
+        ck(cudaEventElapsedTime(&b, ev_start_, o.b), "elapsed");
+        std::fprintf(f, "op,%d,%.4f,%.4f\n", o.cls, a, b);
+      }
+      for (const auto& e : t.events)
+        std::fprintf(f, "ev,%d,%d,%d,%.4f,%.4f\n", static_cast<int>(e.stream), static_cast<int>(e.kind), e.layer,
+                     e.start * 1e3, e.end * 1e3);
+      std::fprintf(f, "step,%.4f\n", st.step_ms);
+      std::fclose(f);
+    }
   }
   return t;
 }

@@ -200,7 +200,7 @@ class Executor {
   std::vector<cudaEvent_t> ev_blk_;  // per row block landed (xs_ -> cs_)
   cudaEvent_t ev_cs2xs_ = nullptr, ev_xs2cs_ = nullptr;
   cudaEvent_t ev_start_ = nullptr;
-  std::vector<cudaEvent_t> ev_fwd_done_, ev_bwd_done_, ev_off_done_, ev_pre_mand_, ev_pre_done_;
+  std::vector<cudaEvent_t> ev_fwd_done_, ev_bwd_done_, ev_off_done_, ev_off_x_, ev_pre_mand_, ev_pre_done_;
   struct Mark {
     int stream, kind, layer;
     cudaEvent_t b, e;
