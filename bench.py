@@ -233,6 +233,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step kernel by kernel (no CUDA graph)")
     ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                     help="SP+TP collectives: peer memory over CUDA IPC (fused AG->GEMM / GEMM->RS) or NCCL")
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
@@ -360,7 +361,9 @@ def main():
         t_layer = tt.item()
     torch.cuda.synchronize()
     free0, _ = torch.cuda.mem_get_info()
-    ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, t_layer=t_layer, op_timing=1)
+    # single-GPU step as one CUDA graph (captured on the second step, replayed after)
+    use_graph = 1 if (cfg.tp_degree == 1 and not args.no_graph) else 0
+    ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, t_layer=t_layer, op_timing=1, cuda_graph=use_graph)
     connect(ex)
     free1, _ = torch.cuda.mem_get_info()
     info0 = ex.info()
@@ -414,6 +417,9 @@ def main():
     p_total = P.count_params(cfg)["total"]
     sim = P.simulate(tl, cfg, hw, p_total)
     flops = P.estimate_flops_per_sample(cfg, p_total)
+    n_rec = sum(e.kind == "recompute" for e in tl)
+    f_int = inter  # SwiGLU width
+    recompute_flops = n_rec * 2.0 * info0["split"][1] * (4.0 * h * h + 2.0 * h * f_int)  # whole job
     mfu = seqs * flops / (t_max * 1e-3) / (world * B200_SPEC_BF16)
     burst, sustained, hbm, peak_src = measured_peaks()
     off = [e for e in tl if e.kind == "offload"]
@@ -446,9 +452,12 @@ def main():
                    "alpha": swap.alpha, "swap_tokens": info0["split"][0],
                    "recompute_tokens": info0["split"][1], "t_layer_measured_s": t_layer,
                    "host_link_d2h_GBps": link["d2h"] / 1e9, "host_link_h2d_GBps": link["h2d"] / 1e9,
-                   "cpu_mem_budget": cpu_mem},
+                   "cpu_mem_budget": cpu_mem, "cuda_graph": bool(use_graph)},
         "tokens_per_s_per_gpu": value / world,
         "mfu": mfu, "mfu_vs_measured_peak": mfu * B200_SPEC_BF16 / (burst * 1e12),
+        # HFU adds the recomputed suffix rows of every swapped layer: QKV, out-projection
+        # and gate/up GEMMs (the attention output itself is swapped, not recomputed)
+        "hfu": (seqs * flops + seqs * recompute_flops) / (t_max * 1e-3) / (world * B200_SPEC_BF16),
         "e2e": {"value": seqs * S / (e2e * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(info["h2d_bytes"]), "d2h_bytes_per_step": int(info["d2h_bytes"])},
         "roofline": {"kernel": "attn_bwd_dkdv (causal FlashAttention dK/dV, tcgen05)",

@@ -242,6 +242,7 @@ typedef struct memo_exec_options {
   uint64_t alignment;         /* planner alignment (512) */
   int32_t op_timing;          /* 1: CUDA events around every GEMM/attention launch */
   int32_t dry_run;            /* 1: plan only (trace, arena plan, alpha, sizes) — no CUDA */
+  int32_t cuda_graph;         /* 1: capture the step as a CUDA graph on the 2nd call, replay after (tp 1) */
 } memo_exec_options;
 
 typedef struct memo_exec_info {

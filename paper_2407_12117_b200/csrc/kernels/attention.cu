@@ -2158,10 +2158,10 @@ cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
   uint32_t* counters = reinterpret_cast<uint32_t*>(acc + HS * D);
   const long long n_ctr = HS / HALF;
   uint32_t* ticket = counters + n_ctr;
-  if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
+  if (a.ev[0]) record_timing_event(a.ev[0], stream);
   cudaMemsetAsync(counters, 0, (n_ctr + 4) * sizeof(uint32_t), stream);
   attn_bwd_prep_kernel<<<(a.S * a.H + 7) / 8, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S, a.H, D);
-  if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
+  if (a.ev[1]) record_timing_event(a.ev[1], stream);
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   auto kern = pend >= 4 ? attn_bwd_fused_kernel<D, 4>
              : pend == 2 ? attn_bwd_fused_kernel<D, 2>
@@ -2170,12 +2170,12 @@ cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
   kern<<<(a.S / TILE) * a.H, BWD_THREADS, L::BYTES, stream>>>(
       mq, mk, mv, mdo, lse2, delta, acc, counters, ticket, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S,
       a.H, a.softmax_scale, a.softmax_scale * kLog2e, G, attn_debug());
-  if (a.ev[2]) cudaEventRecord(a.ev[2], stream);
+  if (a.ev[2]) record_timing_event(a.ev[2], stream);
   const long long n8 = HS * D / 8;
   const int blocks = static_cast<int>(std::min<long long>((n8 + 255) / 256, 148LL * 16));
   attn_dq_convert_kernel<<<blocks, 256, 0, stream>>>(acc, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H, D,
                                                      a.softmax_scale);
-  if (a.ev[3]) cudaEventRecord(a.ev[3], stream);
+  if (a.ev[3]) record_timing_event(a.ev[3], stream);
   return cudaGetLastError();
 }
 
@@ -2204,13 +2204,13 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   float* delta = a.delta;
   float* lse2 = a.delta + static_cast<long long>(a.H) * a.S;
   const int rows = a.S * a.H;
-  if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
+  if (a.ev[0]) record_timing_event(a.ev[0], stream);
   attn_bwd_prep_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S,
                                                             a.H, D);
   const float scale_log2 = a.softmax_scale * kLog2e;
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   dim3 grid(a.S / TILE, a.H);
-  if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
+  if (a.ev[1]) record_timing_event(a.ev[1], stream);
   static const bool dkdv_smem = [] {  // MEMO_ATTN_DKDV=smem: K/V as shared-memory operands (ablation)
     const char* e = getenv("MEMO_ATTN_DKDV");
     return e && std::string(e) == "smem";
@@ -2227,7 +2227,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
     attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
         a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
         scale_log2);
-  if (a.ev[2]) cudaEventRecord(a.ev[2], stream);
+  if (a.ev[2]) record_timing_event(a.ev[2], stream);
   static const int dbg = [] {
     const char* e = getenv("MEMO_ATTN_DEBUG");
     return e ? atoi(e) : 0;
@@ -2244,7 +2244,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
     attn_bwd_dq_kernel<D, false><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
         a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
         a.softmax_scale, scale_log2, dbg);
-  if (a.ev[3]) cudaEventRecord(a.ev[3], stream);
+  if (a.ev[3]) record_timing_event(a.ev[3], stream);
   return cudaGetLastError();
 }
 
@@ -2281,7 +2281,7 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
             make_tma_2d_bf16(&mv, a.v, h, a.S, h, 64, TILE);
   if (!ok) return cudaErrorInvalidValue;
   const float scale_log2 = a.softmax_scale * kLog2e;
-  if (a.ev[0]) cudaEventRecord(a.ev[0], stream);
+  if (a.ev[0]) record_timing_event(a.ev[0], stream);
   // 0-3: one softmax warp per row (bit0 Q in TMEM, bit1 FMA exp2 share); 5-7: split rows;
   // 8-10: ping-pong two Q tiles (default 8)
   const int v = fwd_variant();
@@ -2317,7 +2317,7 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   } else {
     launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
   }
-  if (a.ev[1]) cudaEventRecord(a.ev[1], stream);
+  if (a.ev[1]) record_timing_event(a.ev[1], stream);
   return cudaGetLastError();
 }
 

@@ -505,11 +505,19 @@ __global__ void sum_kernel(const float* __restrict__ v, long long n, float scale
 }
 
 // ------------------------------------------------------------------ optimizer
+// t += 1; bias corrections of step t (double, rounded once)
+__global__ void adam_step_kernel(int* step, float2* c12, float b1, float b2) {
+  const int t = ++*step;
+  *c12 = make_float2(static_cast<float>(1.0 / (1.0 - pow(static_cast<double>(b1), t))),
+                     static_cast<float>(1.0 / (1.0 - pow(static_cast<double>(b2), t))));
+}
+
 // Fused AdamW over the flat parameter buffer: f32 master/m/v, bf16 working copy.
 __global__ void adamw_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
                              const float* __restrict__ grad, float* __restrict__ m,
                              float* __restrict__ v, long long n, float lr, float b1, float b2,
-                             float eps, float wd, float c1, float c2) {
+                             float eps, float wd, const float2* __restrict__ c12) {
+  const float c1 = c12->x, c2 = c12->y;
   const long long n4 = n / 4;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -807,13 +815,12 @@ cudaError_t sum_scaled(const float* v, long long n, float scale, float* out, cud
 }
 
 cudaError_t adamw(float* master, __nv_bfloat16* w, const float* grad, float* m, float* v,
-                  long long n, float lr, float b1, float b2, float eps, float wd, int step,
-                  cudaStream_t st) {
+                  long long n, float lr, float b1, float b2, float eps, float wd, int* step,
+                  float2* c12, cudaStream_t st) {
   if (n % 4) return cudaErrorInvalidValue;
-  const float c1 = 1.f / (1.f - powf(b1, static_cast<float>(step)));
-  const float c2 = 1.f / (1.f - powf(b2, static_cast<float>(step)));
+  adam_step_kernel<<<1, 1, 0, st>>>(step, c12, b1, b2);
   adamw_kernel<<<stride_grid(n, 4, 256), 256, 0, st>>>(master, w, grad, m, v, n, lr, b1, b2, eps,
-                                                       wd, c1, c2);
+                                                       wd, c12);
   return cudaGetLastError();
 }
 

@@ -31,9 +31,12 @@ cudaError_t swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_
 cudaError_t cross_entropy(const float* logits, const int* labels, __nv_bfloat16* dlogits,
                           float* loss_rows, int T, int V, float inv_n, cudaStream_t st);
 cudaError_t sum_scaled(const float* v, long long n, float scale, float* out, cudaStream_t st);
+// The step counter lives on the device (`step`, incremented by the launch
+// itself) so a captured CUDA graph replays the optimizer correctly; `c12`
+// (float2) receives the bias corrections 1/(1-b1^t), 1/(1-b2^t).
 cudaError_t adamw(float* master, __nv_bfloat16* w, const float* grad, float* m, float* v,
-                  long long n, float lr, float b1, float b2, float eps, float wd, int step,
-                  cudaStream_t st);
+                  long long n, float lr, float b1, float b2, float eps, float wd, int* step,
+                  float2* c12, cudaStream_t st);
 
 // Tensor-parallel helpers.
 cudaError_t init_sliced(__nv_bfloat16* w, float* master, long long R, long long C,

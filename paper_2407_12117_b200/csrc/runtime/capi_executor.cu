@@ -49,6 +49,7 @@ extern "C" int memo_exec_options_default(memo_exec_options* o) {
   o->alignment = d.alignment;
   o->dry_run = d.dry_run;
   o->op_timing = d.op_timing;
+  o->cuda_graph = d.cuda_graph;
   return MEMO_OK;
 }
 
@@ -163,6 +164,7 @@ memo::ExecOptions to_options(const memo_exec_options* o) {
     d.alignment = o->alignment;
     d.dry_run = o->dry_run != 0;
     d.op_timing = o->op_timing != 0;
+    d.cuda_graph = o->cuda_graph != 0;
     return d;
 }
 }  // namespace

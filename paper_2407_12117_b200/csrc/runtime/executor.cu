@@ -35,6 +35,7 @@
 #include "kernels/attention.h"
 #include "kernels/elementwise.h"
 #include "kernels/gemm_tc.h"
+#include "kernels/tma_util.h"
 
 namespace memo {
 namespace {
@@ -107,6 +108,8 @@ Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const Ex
   d_.n = static_cast<int>(cfg_.n_layers);
   d_.t = static_cast<int>(cfg_.tp_degree);
   d_.r = comm_ ? comm_->rank() : 0;
+  if (opt_.cuda_graph && d_.t > 1)
+    throw ConfigError("cuda_graph: the SP+TP communicators synchronise on the host; capture needs tp_degree 1");
   if (d_.t > 1 && (!comm_ || comm_->size() != d_.t) && !opt_.dry_run)
     throw ConfigError("tp_degree > 1 needs a communicator of that size");
   if (d_.h % d_.H || (d_.D != 64 && d_.D != 128)) throw ConfigError("head_dim must be 64 or 128");
@@ -452,6 +455,9 @@ void Executor::allocate() {
   csr_pos_ = reinterpret_cast<int*>(q); q += S * 4;
   csr_off_ = reinterpret_cast<int*>(q); q += (V + 1) * 4;
   loss_dev_ = reinterpret_cast<float*>(up(reinterpret_cast<uintptr_t>(q), 256));
+  adam_ctr_ = reinterpret_cast<int*>(loss_dev_ + 16);
+  adam_c12_ = reinterpret_cast<float2*>(loss_dev_ + 32);
+  ck(cudaMemset(adam_ctr_, 0, sizeof(int)), "memset(adam step)");
 
   if (pinned_bytes_ > 0) {
     void* hp = nullptr;
@@ -481,6 +487,8 @@ void Executor::allocate() {
   mk(ev_pre_mand_);
   mk(ev_pre_done_);
   ck(cudaEventCreate(&ev_start_), "event");
+  for (cudaEvent_t* e : {&ev_fork_, &ev_join_os_, &ev_join_ps_})
+    ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
   if (comm_ && d_.t > 1) {
     comm_->attach(dev_, dev_bytes_);  // peer backends: the single allocation is the symmetric heap
     ck(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking), "stream");
@@ -560,6 +568,10 @@ Executor::~Executor() {
     if (e) cudaEventDestroy(e);
   if (xs_) cudaStreamDestroy(xs_);
   if (ev_start_) cudaEventDestroy(ev_start_);
+  for (cudaEvent_t e : {ev_fork_, ev_join_os_, ev_join_ps_})
+    if (e) cudaEventDestroy(e);
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
   if (cs_) cudaStreamDestroy(cs_);
   if (os_) cudaStreamDestroy(os_);
   if (ps_) cudaStreamDestroy(ps_);
@@ -582,12 +594,12 @@ void Executor::gemm(const GemmDesc& g) {
   if (opt_.op_timing) {
     a = take_event();
     b = take_event();
-    ck(cudaEventRecord(a, cs_), "record");
+    ck(record_timing_event(a, cs_), "record");
   }
   ck(gemm_tc(g, cs_), "gemm_tc");
   stats_.kernel_launches += 1;
   if (opt_.op_timing) {
-    ck(cudaEventRecord(b, cs_), "record");
+    ck(record_timing_event(b, cs_), "record");
     ops_.push_back({OP_GEMM, a, b, 2.0 * g.M * static_cast<double>(g.N) * g.K});
   }
 }
@@ -621,7 +633,7 @@ void Executor::attention_bwd(AttnBwdArgs a) {
 void Executor::mark(int stream, int kind, int layer, bool begin) {
   cudaStream_t s = stream == 0 ? cs_ : (stream == 1 ? os_ : ps_);
   cudaEvent_t e = take_event();
-  ck(cudaEventRecord(e, s), "eventRecord");
+  ck(record_timing_event(e, s), "eventRecord");
   if (begin) {
     marks_.push_back({stream, kind, layer, e, nullptr});
   } else {
@@ -1314,17 +1326,53 @@ void Executor::sync_replicated_grads() {
   sum("gf", -1);
 }
 
+// With ExecOptions::cuda_graph the first step runs eagerly (kernel attributes,
+// lazy module loading and TMA-descriptor caches settle), the second is
+// captured from cs_ -- the copy streams join through ev_fork_ and rejoin at the
+// end -- and every step after replays the instantiated graph with one launch.
+// The timeline, op timings and launch counts of the captured step stay valid:
+// their events are external record nodes of the graph (record_timing_event).
 void Executor::step_resident() {
+  if (!opt_.cuda_graph) {
+    record_step();
+    return;
+  }
+  if (!graph_exec_ && eager_done_) {
+    G(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
+    capturing_ = true;
+    try {
+      record_step();
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(cs_, &g);
+      if (g) cudaGraphDestroy(g);
+      capturing_ = false;
+      throw;
+    }
+    G(cudaStreamEndCapture(cs_, &graph_));
+    capturing_ = false;
+    G(cudaGraphInstantiate(&graph_exec_, graph_, 0));
+  }
+  if (graph_exec_) {
+    G(cudaGraphLaunch(graph_exec_, cs_));
+    return;
+  }
+  record_step();
+  eager_done_ = true;
+}
+
+void Executor::record_step() {
   const int n = d_.n;
   marks_.clear();
   ops_.clear();
   ev_used_ = 0;
   stats_.offload_bytes = stats_.prefetch_bytes = 0;
   stats_.kernel_launches = 0;
-  G(cudaEventRecord(ev_start_, cs_));
+  G(record_timing_event(ev_start_, cs_));
   // copy streams must not run ahead of this step's start
-  G(cudaStreamWaitEvent(os_, ev_start_, 0));
-  G(cudaStreamWaitEvent(ps_, ev_start_, 0));
+  G(cudaEventRecord(ev_fork_, cs_));
+  G(cudaStreamWaitEvent(os_, ev_fork_, 0));
+  G(cudaStreamWaitEvent(ps_, ev_fork_, 0));
   mark(0, static_cast<int>(Kind::EmbFwd), -1, true);
   G(embed_fwd(tok_ + d_.r * d_.Sl, params_ + ptab_.at({"embedding", -1}).first,
               reinterpret_cast<float*>(comp(0, C_X)), d_.Sl, d_.h, cs_));
@@ -1343,11 +1391,16 @@ void Executor::step_resident() {
   mark(0, static_cast<int>(Kind::EmbBwd), -1, false);
   stats_.kernel_launches += 2;
   if (opt_.optimizer) {
-    ++adam_step_;
     G(adamw(master_, params_, grads_, adam_m_, adam_v_, n_params_, opt_.lr, opt_.beta1, opt_.beta2,
-            opt_.adam_eps, opt_.weight_decay, adam_step_, cs_));
-    stats_.kernel_launches += 1;
+            opt_.adam_eps, opt_.weight_decay, adam_ctr_, adam_c12_, cs_));
+    stats_.kernel_launches += 2;
   }
+  // rejoin the copy streams (all their work is already ordered before this
+  // point by F3 / B3; the join makes it explicit for graph capture)
+  G(cudaEventRecord(ev_join_os_, os_));
+  G(cudaEventRecord(ev_join_ps_, ps_));
+  G(cudaStreamWaitEvent(cs_, ev_join_os_, 0));
+  G(cudaStreamWaitEvent(cs_, ev_join_ps_, 0));
   mark(0, 99, -1, true);  // step end marker
 }
 

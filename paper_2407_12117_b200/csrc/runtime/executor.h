@@ -39,6 +39,7 @@ struct ExecOptions {
   Bytes alignment = 512;
   bool op_timing = false;  // record per-kernel-class CUDA events inside the step
   bool dry_run = false;  // plan only (trace, arena plan, alpha, sizes); no CUDA calls
+  bool cuda_graph = false;  // capture the step once (after one eager step) and replay it (t == 1)
 };
 
 // Llama dimensions derived from the reference ModelConfig: intermediate size
@@ -79,6 +80,7 @@ class Executor {
   void load_batch(const int* tokens, const int* labels);
   // One training step on the resident batch; loss stays on device.
   void step_resident();
+  bool graph_ready() const { return graph_exec_ != nullptr; }
   // End to end: load_batch + step + D2H of the loss.
   float step(const int* tokens, const int* labels);
   float last_loss();  // synchronises
@@ -185,7 +187,8 @@ class Executor {
   int *tok_ = nullptr, *lab_ = nullptr, *csr_off_ = nullptr, *csr_pos_ = nullptr;
   float* loss_dev_ = nullptr;
   int n_labeled_ = 0;
-  int adam_step_ = 0;
+  int* adam_ctr_ = nullptr;   // device AdamW step counter (graph-replay safe)
+  float2* adam_c12_ = nullptr;  // device bias corrections of the current step
 
   // host
   char* pinned_ = nullptr;
@@ -199,7 +202,12 @@ class Executor {
   cudaStream_t xs_ = nullptr;  // peer-collective stream (pulls overlapped with the GEMMs on cs_)
   std::vector<cudaEvent_t> ev_blk_;  // per row block landed (xs_ -> cs_)
   cudaEvent_t ev_cs2xs_ = nullptr, ev_xs2cs_ = nullptr;
-  cudaEvent_t ev_start_ = nullptr;
+  cudaEvent_t ev_start_ = nullptr, ev_fork_ = nullptr, ev_join_os_ = nullptr, ev_join_ps_ = nullptr;
+  // CUDA graph of one step (ExecOptions::cuda_graph): captured on the second call
+  void record_step();
+  bool eager_done_ = false, capturing_ = false;
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
   std::vector<cudaEvent_t> ev_fwd_done_, ev_bwd_done_, ev_off_done_, ev_off_x_, ev_pre_mand_, ev_pre_done_;
   struct Mark {
     int stream, kind, layer;

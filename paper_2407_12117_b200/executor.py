@@ -26,7 +26,7 @@ class ExecOptionsC(C.Structure):
                 ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
                 ("weight_decay", C.c_float), ("t_layer", C.c_double),
                 ("plan_time_budget", C.c_double), ("alignment", C.c_uint64),
-                ("op_timing", C.c_int32), ("dry_run", C.c_int32)]
+                ("op_timing", C.c_int32), ("dry_run", C.c_int32), ("cuda_graph", C.c_int32)]
 
 
 class ExecInfoC(C.Structure):

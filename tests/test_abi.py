@@ -37,6 +37,6 @@ def test_struct_sizes_match_header():
     assert C.sizeof(_abi.HardwareConfigC) == 40
     assert C.sizeof(_abi.ScheduleEventC) == 32
     assert C.sizeof(_abi.SwapPlanC) == 56
-    assert C.sizeof(E.ExecOptionsC) == 96
+    assert C.sizeof(E.ExecOptionsC) == 104
     o = E.default_options()
     assert o.token_granularity == 128 and o.swap_enabled == 1 and o.alignment == 512

@@ -169,3 +169,27 @@ def test_training_trajectory_across_alpha_matches_fp32():
     # Adam's normalised update turns bf16-vs-fp32 gradient noise on near-zero
     # gradients into full-size steps, so weights drift more than losses (1.6e-2 seen)
     assert _rel(base_w, master) < 3e-2
+
+
+def test_cuda_graph_replay_bitwise_equals_eager():
+    """ExecOptions::cuda_graph: step 1 eager, step 2 captured (swap copies on
+    the offload/prefetch streams, recompute, AdamW with its device step
+    counter), steps 3+ one graph launch each -- every loss, the weights and the
+    measured timeline equal the eager executor's."""
+    n, h, H, F, V, S = 4, 256, 2, 768, 512, 1024
+    cfg = model(n, h, H, F, V, S)
+    toks, labels = O.tokens(21, V, S)
+    runs = {}
+    for graph in (0, 1):
+        with Executor(cfg, HW, seed=4, alpha=0.5, optimizer=1, lr=1e-3, ce_chunk=512, cuda_graph=graph) as ex:
+            losses = [ex.step(toks, labels) for _ in range(4)]
+            tl = ex.timeline()
+            info = ex.info()
+            runs[graph] = (losses, ex.read("master/all"), ex.read("grad/all"), tl, info)
+    (l0, w0, g0, _, _), (l1, w1, g1, tl1, info1) = runs[0], runs[1]
+    assert l0 == l1
+    assert np.array_equal(w0, w1)
+    assert np.array_equal(g0, g1)
+    assert P.validate_schedule(tl1, n, info1["swap"]) == []
+    assert sum(e.kind == "recompute" for e in tl1) == 2
+    assert info1["last_step_ms"] > 0
