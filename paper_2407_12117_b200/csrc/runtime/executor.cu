@@ -492,6 +492,8 @@ void Executor::allocate() {
   if (comm_ && d_.t > 1) {
     comm_->attach(dev_, dev_bytes_);  // peer backends: the single allocation is the symmetric heap
     ck(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking), "stream");
+    xcs_.resize(d_.t - 1);  // one pull stream per peer block: the copy engines work in parallel
+    for (auto& st : xcs_) ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
     ev_blk_.resize(d_.t);
     for (auto& e : ev_blk_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ev_cs2xs_, cudaEventDisableTiming), "event");
@@ -567,6 +569,10 @@ Executor::~Executor() {
   for (auto e : {ev_cs2xs_, ev_xs2cs_})
     if (e) cudaEventDestroy(e);
   if (xs_) cudaStreamDestroy(xs_);
+  for (auto st : xcs_) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
   if (ev_start_) cudaEventDestroy(ev_start_);
   for (cudaEvent_t e : {ev_fork_, ev_join_os_, ev_join_ps_})
     if (e) cudaEventDestroy(e);
@@ -1067,14 +1073,19 @@ void Executor::gather_gemm(const __nv_bfloat16* shard, __nv_bfloat16* full, Gemm
   ck(cudaEventRecord(ev_cs2xs_, cs_), "record");
   ck(cudaStreamWaitEvent(xs_, ev_cs2xs_, 0), "wait");  // own shard written, `full` free
   const Bytes blk = shard_elems * 2;
-  for (int j = 0; j < t; ++j) {
+  for (int j = 0; j < t; ++j) {  // block j = 0 is the own shard (local copy on xs_)
     const int k = (r + j) % t;
-    if (k != r) comm_->wait(k, CH_AG_READY, xs_);
+    cudaStream_t st = j == 0 ? xs_ : xcs_[j - 1];
+    if (j > 0) {
+      ck(cudaStreamWaitEvent(st, ev_cs2xs_, 0), "wait");
+      comm_->wait(k, CH_AG_READY, st);
+    }
     const void* src = k == r ? static_cast<const void*>(shard) : comm_->peer_ptr(k, shard);
-    ck(cudaMemcpyAsync(reinterpret_cast<char*>(full) + k * blk, src, blk, cudaMemcpyDeviceToDevice, xs_),
+    ck(cudaMemcpyAsync(reinterpret_cast<char*>(full) + k * blk, src, blk, cudaMemcpyDeviceToDevice, st),
        "peer gather copy");
-    ck(cudaEventRecord(ev_blk_[j], xs_), "record");
+    ck(cudaEventRecord(ev_blk_[j], st), "record");
   }
+  for (int j = 1; j < t; ++j) ck(cudaStreamWaitEvent(xs_, ev_blk_[j], 0), "wait");  // all pulls done
   for (int k = 0; k < t; ++k)
     if (k != r) comm_->signal(k, CH_AG_DONE, xs_);
   for (int j = 0; j < t; ++j) {

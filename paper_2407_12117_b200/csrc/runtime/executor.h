@@ -200,6 +200,7 @@ class Executor {
   // streams / events
   cudaStream_t cs_ = nullptr, os_ = nullptr, ps_ = nullptr;
   cudaStream_t xs_ = nullptr;  // peer-collective stream (pulls overlapped with the GEMMs on cs_)
+  std::vector<cudaStream_t> xcs_;  // per-peer pull streams of the all-gather (parallel copy engines)
   std::vector<cudaEvent_t> ev_blk_;  // per row block landed (xs_ -> cs_)
   cudaEvent_t ev_cs2xs_ = nullptr, ev_xs2cs_ = nullptr;
   cudaEvent_t ev_start_ = nullptr, ev_fork_ = nullptr, ev_join_os_ = nullptr, ev_join_ps_ = nullptr;
