@@ -64,9 +64,11 @@ def ocfg_of(cfg):
                       cfg.seq_len)
 
 
-@pytest.mark.parametrize("t,kind", [(2, KIND_LOOPBACK), (2, KIND_PEER_LOCAL), (4, KIND_PEER_LOCAL)])
-def test_tp_matches_oracle(t, kind):
-    n, h, H, F, V, S = 4, 256, 4, 768, 512, 1024
+@pytest.mark.parametrize("t,kind,dims", [(2, KIND_LOOPBACK, None), (2, KIND_PEER_LOCAL, None),
+                                         (4, KIND_PEER_LOCAL, None),
+                                         (8, KIND_PEER_LOCAL, (4, 512, 8, 768, 512, 2048))])
+def test_tp_matches_oracle(t, kind, dims):
+    n, h, H, F, V, S = dims or (4, 256, 4, 768, 512, 1024)
     cfg = model(n, h, H, F, V, S, t)
     ocfg = ocfg_of(cfg)
     params = O.init_params(ocfg, 1234)
