@@ -89,9 +89,9 @@ std::unique_ptr<Comm> make_loopback_comm(std::shared_ptr<LoopbackGroup> g, int r
 // signals instead of NCCL:
 //   IPC    one process per GPU; the attached allocation and a 512-byte flag
 //          page are exported with cudaIpcGetMemHandle and mapped by every
-//          peer; signals are cuStreamWriteValue64 (release) into the peer's
-//          flag page and cuStreamWaitValue64 (>=) on the local one, so no SM
-//          spins and the host never blocks.
+//          peer; a signal is a one-thread kernel storing (st.release.sys)
+//          into the peer's flag page, a wait is cuStreamWaitValue64 (>=) on
+//          the local one, so no SM spins and the host never blocks.
 //   local  t ranks as threads of one process on one GPU (testing the same
 //          algorithms on one B200): pointers are exchanged in-process and a
 //          signal is an event the receiver's stream waits on.

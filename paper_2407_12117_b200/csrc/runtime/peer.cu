@@ -86,6 +86,12 @@ __global__ void peer_acc4_kernel(const float4* __restrict__ remote, float4* __re
   }
 }
 
+// One flag store into a peer's page, ordered after everything the stream did
+// before (kernel boundary) and released at system scope for the other GPU.
+__global__ void peer_signal_kernel(unsigned long long* flag, unsigned long long v) {
+  asm volatile("fence.acq_rel.sys;\n\tst.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
+}
+
 int grid_for(size_t n) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -181,7 +187,7 @@ class PeerComm : public Comm {
 // ------------------------------------------------------------------ IPC (multi-process)
 typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 struct StreamMemOps {
-  StreamValueFn write = nullptr, wait = nullptr;
+  StreamValueFn wait = nullptr;
 };
 const StreamMemOps& mem_ops() {
   static StreamMemOps ops;
@@ -189,9 +195,6 @@ const StreamMemOps& mem_ops() {
   std::call_once(once, [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      ops.write = reinterpret_cast<StreamValueFn>(p);
     if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       ops.wait = reinterpret_cast<StreamValueFn>(p);
@@ -210,7 +213,7 @@ struct IpcHandle {
 class IpcComm final : public PeerComm {
  public:
   IpcComm(int rank, int size) : PeerComm(rank, size) {
-    if (!mem_ops().write || !mem_ops().wait) throw std::runtime_error("cuStreamWriteValue64/WaitValue64 unavailable");
+    if (!mem_ops().wait) throw std::runtime_error("cuStreamWaitValue64 unavailable");
   }
   ~IpcComm() override {
     for (int k = 0; k < size_; ++k) {
@@ -262,9 +265,9 @@ class IpcComm final : public PeerComm {
   // flag page layout: uint64 [channel][source rank]
   void signal(int dst, int ch, cudaStream_t st) override {
     const uint64_t v = ++sent_[ch][dst];
-    const auto addr = reinterpret_cast<CUdeviceptr>(peer_flags_[dst] + (ch * kMaxPeers + rank_) * 8);
-    if (mem_ops().write(reinterpret_cast<CUstream>(st), addr, v, 0) != CUDA_SUCCESS)  // release (fenced)
-      throw std::runtime_error("cuStreamWriteValue64 failed");
+    auto* addr = reinterpret_cast<unsigned long long*>(peer_flags_[dst] + (ch * kMaxPeers + rank_) * 8);
+    peer_signal_kernel<<<1, 1, 0, st>>>(addr, v);
+    cuda_ck(cudaGetLastError(), "peer signal");
   }
   void wait(int src, int ch, cudaStream_t st) override {
     const uint64_t v = ++expect_[ch][src];
