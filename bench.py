@@ -234,6 +234,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step kernel by kernel (no CUDA graph)")
+    ap.add_argument("--watchdog", type=float, default=1800.0, help="abort the run after this many seconds")
     ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                     help="SP+TP collectives: peer memory over CUDA IPC (fused AG->GEMM / GEMM->RS) or NCCL")
     ap.add_argument("--parallel", default="tp", choices=["tp", "replicas"],
@@ -249,6 +250,17 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+
+    # A collective that never completes (e.g. a peer that died) must not hang the
+    # driver: after --watchdog seconds the process reports and exits.
+    import threading
+
+    def _watchdog():
+        print(f"[bench] rank {rank}: watchdog fired after {args.watchdog} s; aborting", file=sys.stderr, flush=True)
+        os._exit(3)
+    wd = threading.Timer(args.watchdog, _watchdog)
+    wd.daemon = True
+    wd.start()
 
     import numpy as np
     import torch
@@ -490,6 +502,7 @@ def main():
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+    wd.cancel()
 
 
 if __name__ == "__main__":
