@@ -51,3 +51,33 @@ def test_cfg2_full_size_swap_bitwise_equals_no_swap():
     assert np.isfinite(g1).all()
     assert l1 == l0
     assert np.array_equal(g1, g0)
+
+
+def test_cfg2_full_size_tp2_peer_paths_bitwise_equal_loopback():
+    """The same full-size step split over t = 2 SP+TP ranks sharing the B200:
+    the peer-memory backend (fused all-gather->GEMM by row block, staggered
+    GEMM->reduce-scatter with the own block accumulated in the epilogue) gives
+    the loopback backend's loss and gradients bitwise, with swap + recompute on
+    and a valid measured timeline on both ranks."""
+    from paper_2407_12117_b200.executor import KIND_LOOPBACK, KIND_PEER_LOCAL, LoopbackGroup, run_ranks
+    n, h, H, F, V, S, t = 4, 4096, 32, 11008, 32000, 131072, 2
+    cfg = P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=F * 3 // 2, n_heads=H, vocab=V, batch=1,
+                        seq_len=S, dtype_bytes=2, tp_degree=t, untied_classifier=True)
+    toks, labels = O.tokens(1234, V, S)
+    out = {}
+    for kind in (KIND_PEER_LOCAL, KIND_LOOPBACK):
+        g = LoopbackGroup(t)
+
+        def rank(r):
+            with Executor(cfg, HW, tp=(kind, g, r), seed=1234, alpha=0.5, optimizer=0, ce_chunk=8192) as ex:
+                loss = ex.step(toks, labels)
+                tl, info = ex.timeline(), ex.info()
+                assert P.validate_schedule(tl, n, info["swap"]) == []
+                return loss, ex.read("grad/all")
+        out[kind] = run_ranks(t, rank)
+    for r in range(t):
+        lp, gp = out[KIND_PEER_LOCAL][r]
+        ll, gl = out[KIND_LOOPBACK][r]
+        assert math.isfinite(lp) and lp == ll
+        assert np.isfinite(gp).all()
+        assert np.array_equal(gp, gl)
