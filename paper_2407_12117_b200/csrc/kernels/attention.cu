@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* s_full = v_empty + NS;    // [2]
   uint64_t* p_full = s_full + 2;      // [2]
   uint64_t* o_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* o_final = o_done + 1;  // committed once, after the last PV (unambiguous epilogue wait)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
 
   const int n_tiles = S / TILE;
   const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(256, 1)
       dev::mbar_init(&p_full[s], 128);
     }
     dev::mbar_init(o_done, 1);
+    dev::mbar_init(o_final, 1);
     dev::fence_barrier_init();
   }
   if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
@@ -230,7 +232,11 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
           dev::mma_bf16_ts_w(t_o, t_s[j & 1] + kk * 8, mnmajor_step(vd, kk), idesc_o, (j | kk) != 0);
-        dev::mma_commit_w(o_done);
+        // o_done phase j = PV(j) complete (the lazy rescale of tile j+1 waits it:
+        // at that point PV(j-1) is done and PV(j+1) not issued, so its parity
+        // is unambiguous); the epilogue waits o_final instead, because there
+        // the barrier may be one or two phases behind.
+        dev::mma_commit_w(j + 1 < n_kv ? o_done : o_final);
         dev::mma_commit_w(&v_empty[st]);
       }
     }
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(256, 1)
       dev::mbar_arrive(&p_full[st]);
     }
     // epilogue
-    dev::mbar_wait(o_done, (n_kv - 1) & 1);
+    dev::mbar_wait(o_final, 0);
     dev::tc_fence_after();
     const float inv = 1.f / l;
     __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D;
@@ -437,7 +443,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* s_full = v_empty + NS;    // [2]
   uint64_t* p_full = s_full + 2;      // [2]
   uint64_t* o_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* o_final = o_done + 1;  // committed once, after the last PV (unambiguous epilogue wait)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
   const uint32_t xchg_s = dev::smem_u32(smem + L::X_OFF);
 
   const int n_tiles = S / TILE;
@@ -462,6 +469,7 @@ __global__ void __launch_bounds__(384, 1)
       dev::mbar_init(&p_full[s], 256);
     }
     dev::mbar_init(o_done, 1);
+    dev::mbar_init(o_final, 1);
     dev::fence_barrier_init();
   }
   if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
@@ -520,7 +528,11 @@ __global__ void __launch_bounds__(384, 1)
         for (int kk = 0; kk < TILE / 16; ++kk)
           dev::mma_bf16_ts_w(t_o, t_s(j & 1) + 8 * kk + 32 * (kk >> 2), mnmajor_step(vd, kk), idesc_o,
                              (j | kk) != 0);
-        dev::mma_commit_w(o_done);
+        // o_done phase j = PV(j) complete (the lazy rescale of tile j+1 waits it:
+        // at that point PV(j-1) is done and PV(j+1) not issued, so its parity
+        // is unambiguous); the epilogue waits o_final instead, because there
+        // the barrier may be one or two phases behind.
+        dev::mma_commit_w(j + 1 < n_kv ? o_done : o_final);
         dev::mma_commit_w(&v_empty[st]);
       }
     }
@@ -647,7 +659,7 @@ __global__ void __launch_bounds__(384, 1)
     float l_other;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(l_other) : "r"(xp + ((hf ^ 1) * 128 + row) * 4) : "memory");
     const float lt = l + l_other;
-    dev::mbar_wait(o_done, (n_kv - 1) & 1);
+    dev::mbar_wait(o_final, 0);
     dev::tc_fence_after();
     const float inv = 1.f / lt;
     __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D + 64 * hf;

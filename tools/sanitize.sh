@@ -16,4 +16,17 @@ for tool in memcheck synccheck racecheck; do
   timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 \
       python tools/stress_attn.py 512 2 64 2 > $OUT/attn64_$tool.txt 2>&1
   echo "attn D=64 $tool rc=$?" | tee -a $OUT/summary.txt
+  timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 \
+      python tools/tp_peer_smoke.py 3 2 > $OUT/tp2_peer_$tool.txt 2>&1
+  echo "SP+TP t=2 peer-memory step $tool rc=$?" | tee -a $OUT/summary.txt
+done
+# Perturbation check: outputs computed under racecheck (which reorders and slows
+# execution) must equal a normal run bitwise.  This caught an ambiguous mbarrier
+# parity wait in the non-default forward kernels (attn_fwd_kernel at D=64,
+# attn_fwd_2w_kernel), invisible to racecheck itself (tcgen05 / async proxy).
+for D in 64 128; do
+  python tools/attn_golden_probe.py save 1024 2 $D /tmp/golden_$D.pt
+  timeout 600 $CS --tool racecheck python tools/attn_golden_probe.py check 1024 2 $D /tmp/golden_$D.pt \
+      > $OUT/perturb_attn$D.txt 2>&1
+  echo "attn D=$D under racecheck vs normal: $(grep -c DIFFERS $OUT/perturb_attn$D.txt) differing outputs" | tee -a $OUT/summary.txt
 done
