@@ -418,6 +418,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms.append(a.elapsed_time(b))
     e2e = statistics.mean(e2e_ms)
+    info_e2e = ex.info()  # byte counts of the last end-to-end step (H2D batch, D2H loss)
     if dist:
         t = torch.tensor([e2e], device=ddev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -471,7 +472,7 @@ def main():
         # and gate/up GEMMs (the attention output itself is swapped, not recomputed)
         "hfu": (seqs * flops + seqs * recompute_flops) / (t_max * 1e-3) / (world * B200_SPEC_BF16),
         "e2e": {"value": seqs * S / (e2e * 1e-3), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(info["h2d_bytes"]), "d2h_bytes_per_step": int(info["d2h_bytes"])},
+                "h2d_bytes_per_step": int(info_e2e["h2d_bytes"]), "d2h_bytes_per_step": int(info_e2e["d2h_bytes"])},
         "roofline": {"kernel": "attn_bwd_dkdv (causal FlashAttention dK/dV, tcgen05)",
                      "bound": "tensor", "achieved": achieved, "peak": sustained,
                      "unit": "TFLOP/s", "frac": (achieved / sustained) if achieved else None,

@@ -232,10 +232,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk)
           dev::mma_bf16_ts_w(t_o, t_s[j & 1] + kk * 8, mnmajor_step(vd, kk), idesc_o, (j | kk) != 0);
-        // o_done phase j = PV(j) complete (the lazy rescale of tile j+1 waits it:
-        // at that point PV(j-1) is done and PV(j+1) not issued, so its parity
-        // is unambiguous); the epilogue waits o_final instead, because there
-        // the barrier may be one or two phases behind.
+        // o_done phase j = PV(j) complete, consumed in order by the softmax
+        // warps at tile j+1; the last PV commits o_final for the epilogue.
         dev::mma_commit_w(j + 1 < n_kv ? o_done : o_final);
         dev::mma_commit_w(&v_empty[st]);
       }
@@ -322,9 +320,11 @@ __global__ void __launch_bounds__(256, 1)
         dev::tmem_st32(t_s[st] + lane_off, p0);
         dev::tmem_st32(t_s[st] + lane_off + 32, p1);
       }
+      // Every phase of o_done (PV(j-1) complete) is consumed, in order, so the
+      // parity wait is never ambiguous and no commit goes unwaited.
+      if (j > 0) dev::mbar_wait(o_done, (j - 1) & 1);
       if (any && j > 0) {
         // O must hold P(j-1)V(j-1) before it is rescaled.
-        dev::mbar_wait(o_done, (j - 1) & 1);
         dev::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
@@ -528,10 +528,8 @@ __global__ void __launch_bounds__(384, 1)
         for (int kk = 0; kk < TILE / 16; ++kk)
           dev::mma_bf16_ts_w(t_o, t_s(j & 1) + 8 * kk + 32 * (kk >> 2), mnmajor_step(vd, kk), idesc_o,
                              (j | kk) != 0);
-        // o_done phase j = PV(j) complete (the lazy rescale of tile j+1 waits it:
-        // at that point PV(j-1) is done and PV(j+1) not issued, so its parity
-        // is unambiguous); the epilogue waits o_final instead, because there
-        // the barrier may be one or two phases behind.
+        // o_done phase j = PV(j) complete, consumed in order by the softmax
+        // warps at tile j+1; the last PV commits o_final for the epilogue.
         dev::mma_commit_w(j + 1 < n_kv ? o_done : o_final);
         dev::mma_commit_w(&v_empty[st]);
       }
@@ -634,9 +632,9 @@ __global__ void __launch_bounds__(384, 1)
       else
         tile(std::false_type{});
       dev::tmem_st32(t_s(st) + lane_off + 64 * hf, p);  // inside this warp's own columns
+      if (j > 0) dev::mbar_wait(o_done, (j - 1) & 1);  // every phase consumed in order
       if (any && j > 0) {
         // O must hold P(j-1)V(j-1) before it is rescaled; this warp owns D cols [64hf, 64hf+64)
-        dev::mbar_wait(o_done, (j - 1) & 1);
         dev::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 2; ++c) {

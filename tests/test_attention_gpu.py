@@ -1,11 +1,14 @@
 """tcgen05 causal FlashAttention (csrc/kernels/attention.cu) vs a PyTorch fp32 reference."""
 import ctypes as C
 import math
+import os
 
 import pytest
 import torch
 
 from paper_2407_12117_b200 import _abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -177,3 +180,24 @@ def test_attn_bwd_fused_ablation():
     out = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT.format(root=root)], env=env,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "fused ok" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_attention_bitwise_under_sanitizer_timing(D, tmp_path):
+    """Outputs computed under compute-sanitizer racecheck (which slows and
+    reorders execution) equal a normal run bitwise.  Guards the mbarrier
+    protocols racecheck cannot see (tcgen05 / TMA async proxy): a forward
+    epilogue that waited a barrier by parity while it could be a phase behind
+    produced a wrong O at D=64 under exactly this perturbation."""
+    import shutil
+    import subprocess
+    import sys
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    probe = os.path.join(ROOT, "tools", "attn_golden_probe.py")
+    ref = str(tmp_path / "ref.pt")
+    subprocess.check_call([sys.executable, probe, "save", "1024", "2", str(D), ref], timeout=300)
+    out = subprocess.run([cs, "--tool", "racecheck", sys.executable, probe, "check", "1024", "2", str(D), ref],
+                         capture_output=True, text=True, timeout=600).stdout
+    assert "DIFFERS" not in out and out.count("equal") == 3, out[-2000:]

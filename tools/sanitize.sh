@@ -30,3 +30,11 @@ for D in 64 128; do
       > $OUT/perturb_attn$D.txt 2>&1
   echo "attn D=$D under racecheck vs normal: $(grep -c DIFFERS $OUT/perturb_attn$D.txt) differing outputs" | tee -a $OUT/summary.txt
 done
+# The same check for whole training steps: single GPU (D=64 and D=128) and the
+# SP+TP t=2 peer-memory path.
+for args in "0 1 4" "0 1 2" "3 2 4"; do
+  a=$(python tools/tp_peer_smoke.py $args | tail -1)
+  b=$(timeout 900 $CS --tool racecheck python tools/tp_peer_smoke.py $args 2>/dev/null | grep "losses+grad")
+  [ "$a" == "$b" ] && r=equal || r=DIFFERS
+  echo "step (kind t heads = $args) under racecheck vs normal: $r" | tee -a $OUT/summary.txt
+done
