@@ -41,6 +41,9 @@ CONFIGS = {
              "Llama-7B arch, 4 layers, seq 131072, 1xB200, alpha tuned by planner"),
     "cfg1p": (4, 256, 4, 768, 512, 4096, "tiny 4-layer (h256, 4 heads, seq 4096), alpha=0.5"),
     "cfg5": (32, 4096, 32, 11008, 32000, 262144, "Llama-7B arch, 32 layers, seq 262144, 1xB200"),
+    # the model family of BASELINE configs[3] (13B, 40 heads), sliced to 4 layers on one GPU
+    "cfg4s": (4, 5120, 40, 13824, 32000, 131072,
+              "Llama-13B arch, 4 layers, seq 131072, 1xB200, alpha tuned by planner"),
 }
 
 
@@ -458,7 +461,7 @@ def main():
         "higher_is_better": True, "scaling": "strong" if mode == "tp" else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (splitmix64 tokens, counter-hash random-init weights)",
-        "config": {"workload": desc, "model": "llama-7b-arch", "n_layers": n, "global_batch": world,
+        "config": {"workload": desc, "model": "llama-13b-arch" if h == 5120 else "llama-7b-arch", "n_layers": n, "global_batch": world,
                    "seq_len": S, "parallelism": {"single": "single", "tp": f"sp+tp{world} ({comm})",
                                                  "replicas": f"replicas{world}"}[mode],
                    "l2": "working set (GB of activations) >> 126 MB L2; no flush needed",
