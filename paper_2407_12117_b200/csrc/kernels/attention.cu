@@ -1243,6 +1243,17 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 }
 
+// Optional stall accounting of the dK/dV kernel (build with -DMEMO_DKDV_PROF):
+// [0] MMA warp waiting for Q/dO tiles, [1] MMA warp waiting for P/dS (compute),
+// [2] compute warp 4 waiting for S/dP (tensor), [3] compute warp 4 busy per step,
+// [4] steps (MMA warp), [5] total kernel cycles of the MMA warp.
+#ifdef MEMO_DKDV_PROF
+__device__ unsigned long long g_dkdv_prof[8];
+#define MEMO_PROF(x) x
+#else
+#define MEMO_PROF(x)
+#endif
+
 // ------------------------------------------------------------ dK/dV, K/V in TMEM
 // Same math as attn_bwd_dkdv_kernel, but K and V (fixed for the CTA) sit in
 // TMEM as the A operands of S^T = K Q^T and dP^T = V dO^T, so those MMAs read
@@ -1267,8 +1278,11 @@ struct DkdvTmSmem {
 };
 
 // WPQ: softmax-gradient warps per TMEM lane quarter (2: 16 query columns each;
-// 4: 8 columns each, compacted P/dS write-back behind a per-quarter named barrier)
-template <int D, int WPQ>
+// 4: 8 columns each, compacted P/dS write-back behind a per-quarter named barrier).
+// EMU: every EMU-th column pair's exponentials run on the FMA pipe (exp2_fma)
+// instead of MUFU.EX2 (0: none).  The MUFU is the largest single item of the
+// compute warps' per-step critical path (tools/dkdv_prof.py).
+template <int D, int WPQ, int EMU = 0, bool SPLIT = false>
 __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     attn_bwd_dkdv_tm_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
                             const __grid_constant__ CUtensorMap map_q,
@@ -1287,9 +1301,10 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   uint64_t* in_full = bars + 1;        // [NS]
   uint64_t* in_empty = in_full + NS;   // [NS]
   uint64_t* s_full = in_empty + NS;    // [2]
-  uint64_t* p_ready = s_full + 2;      // [2]
+  uint64_t* p_ready = s_full + 2;      // [2]  (SPLIT: P^T written; else P^T and dS^T)
   uint64_t* fin = p_ready + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+  uint64_t* ds_ready = fin + 1;        // [2]  SPLIT: dS^T written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ds_ready + 2);
   constexpr int CW = 32 * 4 * WPQ;
   constexpr int COLS = QSTEP / WPQ;  // query columns per compute warp per step
 
@@ -1312,6 +1327,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     for (int s2 = 0; s2 < 2; ++s2) {
       dev::mbar_init(&s_full[s2], 1);
       dev::mbar_init(&p_ready[s2], CW);
+      dev::mbar_init(&ds_ready[s2], CW);
     }
     dev::mbar_init(fin, 1);
     dev::fence_barrier_init();
@@ -1351,7 +1367,9 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       auto issue_sd = [&](int g) {
         const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
         if (qq == 0) {
+          MEMO_PROF(long long prof_b = clock64();)
           dev::mbar_wait_w(&in_full[st], (i / NS) & 1);
+          MEMO_PROF(if (lane == 0) atomicAdd(&g_dkdv_prof[0], static_cast<unsigned long long>(clock64() - prof_b));)
           dev::tc_fence_after();
         }
         const uint32_t roff = qq * QSTEP * 128;  // 32 rows of 128 B inside every 64-col chunk
@@ -1365,11 +1383,14 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
           dev::mma_bf16_ts_w(buf(b) + 32, t_v + kk * 8, kmajor_step(dod, kk), idesc_s, kk > 0);
         dev::mma_commit_w(&s_full[b]);
       };
+      MEMO_PROF(long long prof_s = clock64();)
       issue_sd(0);
       for (int g = 0; g < n_g; ++g) {
         if (g + 1 < n_g) issue_sd(g + 1);
         const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+        MEMO_PROF(long long prof_a = clock64();)
         dev::mbar_wait_w(&p_ready[b], (g >> 1) & 1);
+        MEMO_PROF(if (lane == 0) atomicAdd(&g_dkdv_prof[1], static_cast<unsigned long long>(clock64() - prof_a));)
         dev::tc_fence_after();
         const uint32_t roff = qq * QSTEP * 128;
         const uint64_t qm = mnmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
@@ -1377,6 +1398,10 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
 #pragma unroll
         for (int kk = 0; kk < QSTEP / 16; ++kk)
           dev::mma_bf16_ts_w(t_dv, buf(b) + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
+        if constexpr (SPLIT) {  // dV(g) above overlaps the dS^T math of the compute warps
+          dev::mbar_wait_w(&ds_ready[b], (g >> 1) & 1);
+          dev::tc_fence_after();
+        }
 #pragma unroll
         for (int kk = 0; kk < QSTEP / 16; ++kk)
           dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(qm, kk), idesc_g,
@@ -1384,6 +1409,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         if (qq == 3) dev::mma_commit_w(&in_empty[st]);
       }
       dev::mma_commit_w(fin);
+      MEMO_PROF(if (lane == 0) { atomicAdd(&g_dkdv_prof[5], static_cast<unsigned long long>(clock64() - prof_s)); atomicAdd(&g_dkdv_prof[4], static_cast<unsigned long long>(n_g)); })
     }
   } else if (warp >= 4) {
     const uint32_t q4 = warp & 3;
@@ -1403,7 +1429,9 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       if (qq == 0) dev::mbar_wait(&in_full[st], (i / NS) & 1);
       const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + COLS * ch) * 4;
       const uint32_t dl = l2 + 512;
+      MEMO_PROF(long long prof_t0 = clock64();)
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
+      MEMO_PROF(long long prof_t1 = clock64(); if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[2], static_cast<unsigned long long>(prof_t1 - prof_t0));)
       dev::tc_fence_after();
       uint32_t sr[COLS], dr[COLS];
       if constexpr (COLS == 16) {
@@ -1414,6 +1442,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         dev::tmem_ld8(buf(b) + lane_off + 32 + 8 * ch, dr);
       }
       dev::tmem_ld_wait_regs(sr, dr);
+      MEMO_PROF(if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[6], static_cast<unsigned long long>(clock64() - prof_t1));)
       uint32_t pp[COLS / 2], dd[COLS / 2];
       auto body = [&](auto diag_tag) {
         constexpr bool DIAG = decltype(diag_tag)::value;
@@ -1428,7 +1457,14 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
           for (int e = 0; e < 4; e += 2) {  // column pairs: FFMA2 / FADD2 / FMUL2
             const uint64_t x2 = ffma2_v(f2_pack(__uint_as_float(sr[4 * j4 + e]), __uint_as_float(sr[4 * j4 + e + 1])),
                                         scale_log2, f2_pack(lq[e], lq[e + 1]));
-            float pa = dev::ex2(f2_lo(x2)), pb = dev::ex2(f2_hi(x2));
+            float pa, pb;
+            if (EMU && ((2 * j4 + (e >> 1)) % (EMU ? EMU : 1)) == EMU - 1) {
+              pa = exp2_fma(f2_lo(x2));
+              pb = exp2_fma(f2_hi(x2));
+            } else {
+              pa = dev::ex2(f2_lo(x2));
+              pb = dev::ex2(f2_hi(x2));
+            }
             if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e < r) pa = 0.f;
             if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e + 1 < r) pb = 0.f;
             const uint64_t d2 = fmul2(f2_pack(pa, pb),
@@ -1445,6 +1481,66 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
           dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
         }
       };
+      if constexpr (SPLIT && COLS == 16) {
+        // P^T first (its own barrier, so dV(g) can start), then dS^T.
+        float pf[COLS];
+        auto pbody = [&](auto diag_tag) {
+          constexpr bool DIAG = decltype(diag_tag)::value;
+#pragma unroll
+          for (int j4 = 0; j4 < COLS / 4; ++j4) {
+            const float4 lv = dev::lds_f4(l2 + 16 * j4);
+            const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const uint64_t x2 = ffma2_v(f2_pack(__uint_as_float(sr[4 * j4 + e]), __uint_as_float(sr[4 * j4 + e + 1])),
+                                          scale_log2, f2_pack(lq[e], lq[e + 1]));
+              float pa, pb;
+              if (EMU && ((2 * j4 + (e >> 1)) % (EMU ? EMU : 1)) == EMU - 1) {
+                pa = exp2_fma(f2_lo(x2));
+                pb = exp2_fma(f2_hi(x2));
+              } else {
+                pa = dev::ex2(f2_lo(x2));
+                pb = dev::ex2(f2_hi(x2));
+              }
+              if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e < r) pa = 0.f;
+              if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e + 1 < r) pb = 0.f;
+              pf[4 * j4 + e] = pa;
+              pf[4 * j4 + e + 1] = pb;
+            }
+            pp[2 * j4] = dev::pack_bf16(pf[4 * j4], pf[4 * j4 + 1]);
+            pp[2 * j4 + 1] = dev::pack_bf16(pf[4 * j4 + 2], pf[4 * j4 + 3]);
+          }
+        };
+        if (diag)
+          pbody(std::true_type{});
+        else
+          pbody(std::false_type{});
+        dev::tmem_st8(buf(b) + lane_off + 16 * ch, pp);
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&p_ready[b]);
+#pragma unroll
+        for (int j4 = 0; j4 < COLS / 4; ++j4) {
+          const float4 dv4 = dev::lds_f4(dl + 16 * j4);
+          const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+          float d4[4];
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const uint64_t d2 = fmul2(f2_pack(pf[4 * j4 + e], pf[4 * j4 + e + 1]),
+                                      fadd2(f2_pack(__uint_as_float(dr[4 * j4 + e]), __uint_as_float(dr[4 * j4 + e + 1])),
+                                            f2_pack(dq4[e], dq4[e + 1])));
+            d4[e] = f2_lo(d2);
+            d4[e + 1] = f2_hi(d2);
+          }
+          dd[2 * j4] = dev::pack_bf16(d4[0], d4[1]);
+          dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
+        }
+        dev::tmem_st8(buf(b) + lane_off + 32 + 16 * ch, dd);
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&ds_ready[b]);
+        continue;
+      }
       if (diag)
         body(std::true_type{});
       else
@@ -1461,9 +1557,12 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         dev::tmem_st4(buf(b) + lane_off + 4 * ch, pp);
         dev::tmem_st4(buf(b) + lane_off + 32 + 4 * ch, dd);
       }
+      MEMO_PROF(long long prof_t2 = clock64();)
       dev::tmem_st_wait();
+      MEMO_PROF(if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[7], static_cast<unsigned long long>(clock64() - prof_t2));)
       dev::tc_fence_before();
       dev::mbar_arrive(&p_ready[b]);
+      MEMO_PROF(if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[3], static_cast<unsigned long long>(clock64() - prof_t1));)
     }
     dev::mbar_wait(fin, 0);
     dev::tc_fence_after();
@@ -2124,6 +2223,23 @@ int dkdv_wpq() {  // MEMO_ATTN_DKDV_WPQ: softmax-gradient warps per lane quarter
   return v;
 }
 
+bool dkdv_split() {  // MEMO_ATTN_DKDV_SPLIT=1: P^T and dS^T behind separate barriers
+  static const bool v = [] {
+    const char* e = getenv("MEMO_ATTN_DKDV_SPLIT");
+    return e && atoi(e) == 1;
+  }();
+  return v;
+}
+
+int dkdv_emu() {  // MEMO_ATTN_DKDV_EMU: every n-th column pair's exps on the FMA pipe (0, 2, 4)
+  static const int v = [] {
+    const char* e = getenv("MEMO_ATTN_DKDV_EMU");
+    const int x = e ? atoi(e) : 0;
+    return x == 2 || x == 4 ? x : 0;
+  }();
+  return v;
+}
+
 bool bwd_fused() {
   static const bool v = [] {
     const char* e = getenv("MEMO_ATTN_BWD");
@@ -2204,6 +2320,12 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
                          BwdSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2231,6 +2353,18 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
         scale_log2);
   else if (dkdv_wpq() == 4)
     attn_bwd_dkdv_tm_kernel<D, 4><<<grid, 32 * (4 + 16), DkdvTmSmem<D>::BYTES, stream>>>(
+        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+        scale_log2);
+  else if (dkdv_split())
+    attn_bwd_dkdv_tm_kernel<D, 2, 0, true><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+        scale_log2);
+  else if (dkdv_emu() == 2)
+    attn_bwd_dkdv_tm_kernel<D, 2, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+        scale_log2);
+  else if (dkdv_emu() == 4)
+    attn_bwd_dkdv_tm_kernel<D, 2, 4><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
         a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
         scale_log2);
   else
@@ -2349,4 +2483,15 @@ cudaError_t attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   if (a.D == 64) return launch_bwd<64>(a, stream);
   return cudaErrorInvalidValue;
 }
+#ifdef MEMO_DKDV_PROF
+extern "C" int memo_debug_dkdv_prof(unsigned long long* out8, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_dkdv_prof, 8 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_dkdv_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 }  // namespace memo
