@@ -301,7 +301,9 @@ int memo_comm_unique_id(uint8_t out[128]);
  * kind 2: peer memory over CUDA IPC, one process per GPU (handle unused; call
  *         memo_exec_peer_handle on every rank, exchange the bytes, then
  *         memo_exec_peer_connect with all of them in rank order before the first step),
- * kind 3: peer memory between t threads on one GPU (handle = memo_loopback_group*).
+ * kind 3: peer memory between t threads on one GPU (handle = memo_loopback_group*),
+ * kind 4: one rank measured alone (handle unused): collectives become local copies of
+ *         the same size -- projecting a t-GPU config's per-rank step on one GPU, not numerics.
  * Peer kinds run the fused all-gather->GEMM and GEMM->reduce-scatter paths. */
 int memo_exec_create_tp(const memo_model_config* cfg, const memo_hardware_config* hw,
                         const memo_exec_options* opt, int32_t kind, const void* handle,

@@ -81,7 +81,7 @@ extern "C" int memo_exec_create_tp(const memo_model_config* cfg, const memo_hard
                                    const memo_exec_options* o, int32_t kind, const void* handle,
                                    int32_t rank, memo_exec** out) {
   return guard([&] {
-    if (!cfg || !hw || !o || !out || (!handle && kind != 2)) throw memo::ConfigError("null argument");
+    if (!cfg || !hw || !o || !out || (!handle && kind != 2 && kind != 4)) throw memo::ConfigError("null argument");
     const int t = static_cast<int>(cfg->tp_degree);
     std::unique_ptr<memo::Comm> comm;
     if (kind == 0)
@@ -92,6 +92,8 @@ extern "C" int memo_exec_create_tp(const memo_model_config* cfg, const memo_hard
       comm = memo::make_ipc_comm(rank, t);
     else if (kind == 3)
       comm = memo::make_peer_local_comm(static_cast<const memo_loopback_group*>(handle)->g, rank);
+    else if (kind == 4)
+      comm = memo::make_solo_comm(rank, t);
     else
       throw memo::ConfigError("unknown communicator kind");
     auto* ctx = new memo_exec{nullptr};

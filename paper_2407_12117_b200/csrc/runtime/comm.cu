@@ -191,6 +191,41 @@ class LoopbackComm final : public Comm {
 
 }  // namespace
 
+namespace {
+// One rank of a t-rank group measured in isolation (communicator kind 4): every
+// collective is replaced by a local copy of the same size (a gather replicates
+// the own shard, a reduction keeps the own partial), so the rank's compute,
+// memory plan and swap traffic are those of the real group while no data
+// moves between GPUs.  For projecting multi-GPU configs from one GPU only --
+// the numerics are not those of the group.
+class SoloComm final : public Comm {
+ public:
+  SoloComm(int rank, int size) : rank_(rank), size_(size) {}
+  int rank() const override { return rank_; }
+  int size() const override { return size_; }
+  void all_gather(const void* send, void* recv, size_t count, CommDtype dt, cudaStream_t st) override {
+    const size_t b = count * esize(dt);
+    for (int k = 0; k < size_; ++k)
+      cudaMemcpyAsync(static_cast<char*>(recv) + k * b, send, b, cudaMemcpyDeviceToDevice, st);
+  }
+  void reduce_scatter(const void* send, void* recv, size_t count, CommDtype dt, cudaStream_t st) override {
+    const size_t b = count * esize(dt);
+    cudaMemcpyAsync(recv, static_cast<const char*>(send) + rank_ * b, b, cudaMemcpyDeviceToDevice, st);
+  }
+  void all_reduce(const void* send, void* recv, size_t count, CommDtype dt, CommOp, cudaStream_t st) override {
+    if (send != recv) cudaMemcpyAsync(recv, send, count * esize(dt), cudaMemcpyDeviceToDevice, st);
+  }
+  void reduce(const void* send, void* recv, size_t count, CommDtype dt, int root, cudaStream_t st) override {
+    if (root == rank_ && send != recv) cudaMemcpyAsync(recv, send, count * esize(dt), cudaMemcpyDeviceToDevice, st);
+  }
+
+ private:
+  int rank_, size_;
+};
+}  // namespace
+
+std::unique_ptr<Comm> make_solo_comm(int rank, int size) { return std::make_unique<SoloComm>(rank, size); }
+
 std::unique_ptr<Comm> make_nccl_comm(const void* unique_id, int rank, int size) {
   return std::make_unique<NcclComm>(unique_id, rank, size);
 }

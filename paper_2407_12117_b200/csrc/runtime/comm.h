@@ -98,6 +98,10 @@ std::unique_ptr<Comm> make_loopback_comm(std::shared_ptr<LoopbackGroup> g, int r
 std::unique_ptr<Comm> make_ipc_comm(int rank, int size);
 std::unique_ptr<Comm> make_peer_local_comm(std::shared_ptr<LoopbackGroup> g, int rank);
 
+// One rank of a t-rank group in isolation: collectives become local copies of
+// the same size.  Projection of multi-GPU configs on one GPU; not numerics.
+std::unique_ptr<Comm> make_solo_comm(int rank, int size);
+
 // acc = first ? remote : acc + remote  (f32, count % 4 == 0, 16-byte aligned);
 // one pull step of the executor's staggered reduce-scatter.
 cudaError_t peer_accumulate(const float* remote, float* acc, size_t count, bool first, cudaStream_t st);

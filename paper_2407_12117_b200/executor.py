@@ -199,7 +199,7 @@ class Executor:
         return out
 
 
-KIND_LOOPBACK, KIND_NCCL, KIND_IPC, KIND_PEER_LOCAL = 0, 1, 2, 3
+KIND_LOOPBACK, KIND_NCCL, KIND_IPC, KIND_PEER_LOCAL, KIND_SOLO = 0, 1, 2, 3, 4
 
 
 class LoopbackGroup:
