@@ -58,8 +58,8 @@ def main():
         ms = []
         for _ in range(args.steps):
             ex.step(toks, labels)
+            tl = ex.timeline()  # also computes the step's device time
             ms.append(ex.info()["last_step_ms"])
-        tl = ex.timeline()
         info = ex.info()
     step_s = float(np.median(ms)) * 1e-3
     swap = info0["swap"]
