@@ -131,3 +131,23 @@ def test_multi_gpu_configs_fit_one_b200_per_rank(name, t):
     assert info["pinned_bytes"] <= sw.cpu_footprint <= hw.cpu_mem
     if os.path.exists(PROBE):
         assert _ref_plan(ex.trace_text()) == ex.plan_json()
+
+
+def test_solo_rank_plan_equals_group_rank_plan_and_option_checks():
+    """Communicator kind 4 (one rank measured alone, tools/project_rank.py)
+    plans exactly what a rank of the real group plans; the C ABI refuses the
+    combinations it cannot honour (CUDA graphs with a multi-rank group, IPC
+    handles from a non-IPC communicator) with status 2."""
+    from paper_2407_12117_b200.executor import KIND_SOLO
+    cfg = llama(4, 4096, 32, 11008, 32000, 131072)
+    cfg.tp_degree = 4
+    group_rank = Executor(cfg, HW, alpha=0.5, dry_run=1)
+    solo = Executor(cfg, HW, alpha=0.5, dry_run=1, tp=(KIND_SOLO, None, 0))
+    assert solo.plan_json() == group_rank.plan_json()
+    assert solo.info()["device_bytes"] == group_rank.info()["device_bytes"]
+    with pytest.raises(MemoError) as e:
+        solo.peer_handle()
+    assert e.value.code == 2
+    with pytest.raises(MemoError) as e:
+        Executor(cfg, HW, alpha=0.5, dry_run=1, tp=(KIND_SOLO, None, 0), cuda_graph=1)
+    assert e.value.code == 2
