@@ -418,6 +418,33 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
 }
 __device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
 __device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {  // a * b + c
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// max(a, b, c) in one FMNMX3 (sm_100)
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// exp2_fma on a column pair with the paired FP32 instructions: bitwise the
+// scalar exp2_fma of each half (same operations, same rounding), in ~10
+// instructions per pair instead of ~18.
+__device__ __forceinline__ uint64_t exp2_fma2(uint64_t x2) {
+  const uint64_t x = f2_pack(fmaxf(f2_lo(x2), -126.f), fmaxf(f2_hi(x2), -126.f));
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
+  const uint64_t j = fadd2(x, magic);                                        // low bits = round(x)
+  const uint64_t t = fadd2(j, f2_pack(-12582912.f, -12582912.f));            // round(x) as float
+  const uint64_t f = fma2(t, f2_pack(-1.f, -1.f), x);                         // x - round(x), exact sub
+  uint64_t p = fma2(f, f2_pack(0.05517027f, 0.05517027f), f2_pack(0.24260795f, 0.24260795f));
+  p = fma2(p, f, f2_pack(0.6932609f, 0.6932609f));
+  p = fma2(p, f, f2_pack(0.9999283f, 0.9999283f));
+  const uint32_t lo = static_cast<uint32_t>(p) + (static_cast<uint32_t>(j) << 23);
+  const uint32_t hi = static_cast<uint32_t>(p >> 32) + (static_cast<uint32_t>(j >> 32) << 23);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -863,18 +890,19 @@ __global__ void __launch_bounds__(384, 1)
           for (int i = 0; i < 128; ++i)
             if (i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
         }
+        // row max: 8 independent chains of 3-input FMNMX3 (68 instructions, not 134)
+        auto rv = [&](int i) { return __uint_as_float(r[i >> 5][i & 31]); };
         float mx8[8];
 #pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = __uint_as_float(r[0][k2]);
+        for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(rv(k2), rv(8 + k2));
 #pragma unroll
-        for (int i = 8; i < 128; i += 8)
+        for (int i = 16; i < 128; i += 16)
 #pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(mx8[k2], __uint_as_float(r[i >> 5][(i & 31) + k2]));
-#pragma unroll
-        for (int k2 = 4; k2 > 0; k2 >>= 1)
-#pragma unroll
-          for (int q2 = 0; q2 < k2; ++q2) mx8[q2] = fmaxf(mx8[q2], mx8[q2 + k2]);
-        const float cand = fmaxf(m, mx8[0] * scale_log2);
+          for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmax3f(mx8[k2], rv(i + k2), rv(i + 8 + k2));
+        const float mxa = fmax3f(mx8[0], mx8[1], mx8[2]);
+        const float mxb = fmax3f(mx8[3], mx8[4], mx8[5]);
+        const float mxr = fmax3f(mxa, mxb, fmaxf(mx8[6], mx8[7]));
+        const float cand = fmaxf(m, mxr * scale_log2);
         const bool need = j == 0 || cand > m + kRescaleThreshold;
         any = __any_sync(0xffffffffu, need);
         float m_new = m;
@@ -890,8 +918,9 @@ __global__ void __launch_bounds__(384, 1)
                                     scale_log2, -m_new);
           float a, b;
           if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
-            a = exp2_fma(f2_lo(x2));
-            b = exp2_fma(f2_hi(x2));
+            const uint64_t e2 = exp2_fma2(x2);
+            a = f2_lo(e2);
+            b = f2_hi(e2);
           } else {
             a = dev::ex2(f2_lo(x2));
             b = dev::ex2(f2_hi(x2));
@@ -2430,14 +2459,21 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   // 8-10: ping-pong two Q tiles (default 8)
   const int v = fwd_variant();
   if (v >= 8 && a.D == 128 && a.S % (2 * TILE) == 0) {  // ping-pong (two Q tiles, setmaxnreg)
-    // FMA-pipe exp2 share: 8 -> 1/4, 9 -> none, 10 -> 1/8
+    // FMA-pipe exp2 share (paired exp2_fma2): 8 -> 1/3 (default), 9 -> none, 10 -> 1/8,
+    // 11 -> 1/4, 12 -> 1/2
     static std::once_flag f8;
     std::call_once(f8, [] {
       cudaFuncSetAttribute(attn_fwd_pp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
       cudaFuncSetAttribute(attn_fwd_pp_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
       cudaFuncSetAttribute(attn_fwd_pp_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_pp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+      cudaFuncSetAttribute(attn_fwd_pp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
     });
-    auto kern = v == 9 ? attn_fwd_pp_kernel<0> : v == 10 ? attn_fwd_pp_kernel<8> : attn_fwd_pp_kernel<4>;
+    auto kern = v == 9    ? attn_fwd_pp_kernel<0>
+                : v == 10 ? attn_fwd_pp_kernel<8>
+                : v == 11 ? attn_fwd_pp_kernel<4>
+                : v == 12 ? attn_fwd_pp_kernel<2>
+                          : attn_fwd_pp_kernel<3>;
     kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
                                                                         scale_log2);
   } else if (v >= 5 && a.D != 128) {
