@@ -1488,8 +1488,9 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
                                         scale_log2, f2_pack(lq[e], lq[e + 1]));
             float pa, pb;
             if (EMU && ((2 * j4 + (e >> 1)) % (EMU ? EMU : 1)) == EMU - 1) {
-              pa = exp2_fma(f2_lo(x2));
-              pb = exp2_fma(f2_hi(x2));
+              const uint64_t e2 = exp2_fma2(x2);
+              pa = f2_lo(e2);
+              pb = f2_hi(e2);
             } else {
               pa = dev::ex2(f2_lo(x2));
               pb = dev::ex2(f2_hi(x2));
@@ -1525,8 +1526,9 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
                                           scale_log2, f2_pack(lq[e], lq[e + 1]));
               float pa, pb;
               if (EMU && ((2 * j4 + (e >> 1)) % (EMU ? EMU : 1)) == EMU - 1) {
-                pa = exp2_fma(f2_lo(x2));
-                pb = exp2_fma(f2_hi(x2));
+                const uint64_t e2 = exp2_fma2(x2);
+                pa = f2_lo(e2);
+                pb = f2_hi(e2);
               } else {
                 pa = dev::ex2(f2_lo(x2));
                 pb = dev::ex2(f2_hi(x2));
