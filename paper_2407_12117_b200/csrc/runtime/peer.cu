@@ -20,6 +20,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "runtime/comm.h"
 #include "runtime/loopback_group.h"
@@ -135,12 +136,30 @@ class PeerComm : public Comm {
   void all_gather(const void* send, void* recv, size_t count, CommDtype dt, cudaStream_t st) override {
     const size_t b = count * esz(dt);
     barrier_all(CH_READY, st);
-    for (int j = 0; j < size_; ++j) {  // start at the own index: every link busy at once
+    // One stream per peer block, so the pulls run on parallel copy engines; each
+    // rank starts at its own index, so every link is busy at once.
+    ensure_streams();
+    cuda_ck(cudaEventRecord(fork_, st), "record");
+    for (int j = 0; j < size_; ++j) {
       const int k = (rank_ + j) % size_;
-      cuda_ck(cudaMemcpyAsync(static_cast<char*>(recv) + k * b, peer_ptr(k, send), b, cudaMemcpyDeviceToDevice, st),
+      cudaStream_t s = j == 0 ? st : xst_[j - 1];
+      if (j > 0) cuda_ck(cudaStreamWaitEvent(s, fork_, 0), "wait");
+      cuda_ck(cudaMemcpyAsync(static_cast<char*>(recv) + k * b, peer_ptr(k, send), b, cudaMemcpyDeviceToDevice, s),
               "peer all_gather copy");
+      if (j > 0) {
+        cuda_ck(cudaEventRecord(join_[j - 1], s), "record");
+        cuda_ck(cudaStreamWaitEvent(st, join_[j - 1], 0), "wait");
+      }
     }
     barrier_all(CH_DONE, st);
+  }
+  ~PeerComm() override {
+    for (auto s : xst_) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    for (auto e : join_) cudaEventDestroy(e);
+    if (fork_) cudaEventDestroy(fork_);
   }
   void reduce_scatter(const void* send, void* recv, size_t count, CommDtype dt, cudaStream_t st) override {
     barrier_all(CH_READY, st);
@@ -172,6 +191,19 @@ class PeerComm : public Comm {
     for (int k = 0; k < size_; ++k)
       if (k != rank_) wait(k, ch, st);
   }
+  void ensure_streams() {
+    if (fork_) return;
+    cuda_ck(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "event");
+    xst_.resize(size_ - 1);
+    join_.resize(size_ - 1);
+    for (int i = 0; i < size_ - 1; ++i) {
+      cuda_ck(cudaStreamCreateWithFlags(&xst_[i], cudaStreamNonBlocking), "stream");
+      cuda_ck(cudaEventCreateWithFlags(&join_[i], cudaEventDisableTiming), "event");
+    }
+  }
+  std::vector<cudaStream_t> xst_;
+  std::vector<cudaEvent_t> join_;
+  cudaEvent_t fork_ = nullptr;
   PtrTab table(const void* local) const {
     PtrTab t{};
     for (int k = 0; k < size_; ++k) t.p[k] = peer_ptr(k, local);
