@@ -148,7 +148,7 @@ template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, int M, int N, int K,
-                   EpiParams ep) {
+                   EpiParams ep, int group_m) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -186,10 +186,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto tile_coords = [&](int t, int& mb, int& nb) {
-    const int group_size = GROUP_M * n_tiles;
+    const int group_size = group_m * n_tiles;
     const int g = t / group_size;
-    const int first_m = g * GROUP_M;
-    const int gm = min(GROUP_M, m_tiles - first_m);
+    const int first_m = g * group_m;
+    const int gm = min(group_m, m_tiles - first_m);
     const int local = t - g * group_size;
     mb = first_m + local % gm;
     nb = local / gm;
@@ -526,8 +526,13 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   }
   const int tiles = ((d.M + BM - 1) / BM) * ((d.N + BN - 1) / BN);
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  static const int env_group_m = [] {  // MEMO_GEMM_GROUP_M: raster band override (experiments)
+    const char* e = getenv("MEMO_GEMM_GROUP_M");
+    return e ? atoi(e) : 0;
+  }();
+  const int group_m = env_group_m > 0 ? env_group_m : GROUP_M;
   gemm_tc_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, d.M, d.N,
-                                                                       d.K, ep);
+                                                                       d.K, ep, group_m);
   return cudaGetLastError();
 }
 
