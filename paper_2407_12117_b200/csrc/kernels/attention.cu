@@ -1458,6 +1458,14 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       if (qq == 0) dev::mbar_wait(&in_full[st], (i / NS) & 1);
       const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + COLS * ch) * 4;
       const uint32_t dl = l2 + 512;
+      // lse2 / delta of this step's columns, loaded before the S/dP wait so the
+      // shared-memory latency is off the critical path
+      float4 lvv[COLS / 4], dvv[COLS / 4];
+#pragma unroll
+      for (int j4 = 0; j4 < COLS / 4; ++j4) {
+        lvv[j4] = dev::lds_f4(l2 + 16 * j4);
+        dvv[j4] = dev::lds_f4(dl + 16 * j4);
+      }
       MEMO_PROF(long long prof_t0 = clock64();)
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       MEMO_PROF(long long prof_t1 = clock64(); if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[2], static_cast<unsigned long long>(prof_t1 - prof_t0));)
@@ -1477,8 +1485,8 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
         for (int j4 = 0; j4 < COLS / 4; ++j4) {
-          const float4 lv = dev::lds_f4(l2 + 16 * j4);
-          const float4 dv4 = dev::lds_f4(dl + 16 * j4);
+          const float4 lv = lvv[j4];
+          const float4 dv4 = dvv[j4];
           const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
           const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
           float p4[4], d4[4];
@@ -1518,7 +1526,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
           constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
           for (int j4 = 0; j4 < COLS / 4; ++j4) {
-            const float4 lv = dev::lds_f4(l2 + 16 * j4);
+            const float4 lv = lvv[j4];
             const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
 #pragma unroll
             for (int e = 0; e < 4; e += 2) {
@@ -1552,7 +1560,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         dev::mbar_arrive(&p_ready[b]);
 #pragma unroll
         for (int j4 = 0; j4 < COLS / 4; ++j4) {
-          const float4 dv4 = dev::lds_f4(dl + 16 * j4);
+          const float4 dv4 = dvv[j4];
           const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
           float d4[4];
 #pragma unroll
