@@ -209,11 +209,9 @@ def run_reference(args, rank):
     if rank != 0:
         return
     n_cfg = CONFIGS[args.config]
-    vals = []
-    for _ in range(max(1, args.warmup and 0) + args.steps):
-        vals.append(cpu_baseline(n_cfg)["value"])
-    base = cpu_baseline(n_cfg)
-    v = statistics.median(vals)
+    samples = [cpu_baseline(n_cfg) for _ in range(max(1, args.steps))]
+    base = samples[-1]
+    v = statistics.median(x["value"] for x in samples)
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             # one full workload step at the sampled rate (extrapolated from the bounded sample)
