@@ -115,3 +115,20 @@ def test_tp2_peer_paths_bitwise_equal_loopback():
         assert a[r][0] == b[r][0]
         for k in a[r][2]:
             assert np.array_equal(a[r][2][k], b[r][2][k]), (r, k)
+
+
+def test_solo_rank_step_runs_with_valid_timeline():
+    """Communicator kind 4 (tools/project_rank.py): one rank of a t = 4 group
+    runs its whole step alone -- finite loss, a timeline that passes the
+    reference validator, and the device allocation of the group rank's plan."""
+    from paper_2407_12117_b200.executor import KIND_SOLO
+    n, h, H, F, V, S, t = 4, 256, 4, 768, 512, 1024, 4
+    cfg = model(n, h, H, F, V, S, t)
+    toks, labels = O.tokens(5, V, S)
+    planned = Executor(cfg, HW, alpha=0.5, dry_run=1, ce_chunk=512).info()["device_bytes"]
+    with Executor(cfg, HW, tp=(KIND_SOLO, None, 0), seed=3, alpha=0.5, optimizer=1, ce_chunk=512) as ex:
+        losses = [ex.step(toks, labels) for _ in range(2)]
+        tl, info = ex.timeline(), ex.info()
+    assert all(np.isfinite(losses))
+    assert P.validate_schedule(tl, n, info["swap"]) == []
+    assert info["device_bytes"] == planned
