@@ -484,13 +484,18 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
     ok = make_tma_2d_bf16(&ma, d.a, d.K, d.M, d.lda, BK, BM);
   else
     ok = make_tma_2d_bf16(&ma, d.a, d.M, d.K, d.lda, 64, BK);
-  // MEMO_GEMM_PAIR=1: CTA-pair 256x256 tiles (ablation).  Correct (same per-row
-  // K order, bitwise swap parity holds) but not faster under the power cap on
-  // the 7B layer shapes: +6 % on QKV, -3..-13 % on the others (profiles/README.md).
-  static const bool pair = [] {
+  // CTA-pair 256x256 tiles (cta_group::2) where they measured faster: forward-
+  // layout GEMMs (both operands K-major) with a short K and a wide N -- the QKV,
+  // gate/up and classifier-logit projections (7 % / 6 % at 128K, interleaved
+  // A/B, profiles/README.md); the single-CTA kernel everywhere else.  The choice
+  // depends on (layout, N, K) only, never on M, so a recomputed row block runs
+  // the same kernel as the forward and stays bitwise equal to it.
+  // MEMO_GEMM_PAIR=0/1 forces one kernel for every GEMM.
+  static const int pair_env = [] {
     const char* e = getenv("MEMO_GEMM_PAIR");
-    return e && atoi(e) != 0;
+    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
   }();
+  const bool pair = pair_env >= 0 ? pair_env == 1 : (!A_MN && !B_MN && d.K <= 4096 && d.N >= 8192);
   if (!B_MN)
     ok = ok && make_tma_2d_bf16(&mb, d.b, d.K, d.N, d.ldb, BK, pair ? P_BN / 2 : BN);
   else
