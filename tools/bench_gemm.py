@@ -61,9 +61,11 @@ def run(M, N, K, layout, iters=10):
 if __name__ == "__main__":
     S = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
     only = os.environ.get("GEMM_ONLY")  # comma-separated shape indices
-    shapes = [(S, 12288, 4096, "fwd"), (S, 22016, 4096, "fwd"), (S, 4096, 11008, "fwd"),
-              (S, 4096, 12288, "dgrad"), (S, 4096, 22016, "dgrad"),
-              (4096, 11008, S, "wgrad"), (12288, 4096, S, "wgrad")]
+    # GEMM_MODEL=13b: the Llama-13B layer shapes (h 5120, f 13824) instead of 7B's
+    h, f = (5120, 13824) if os.environ.get("GEMM_MODEL") == "13b" else (4096, 11008)
+    shapes = [(S, 3 * h, h, "fwd"), (S, 2 * f, h, "fwd"), (S, h, f, "fwd"),
+              (S, h, 3 * h, "dgrad"), (S, h, 2 * f, "dgrad"),
+              (h, f, S, "wgrad"), (3 * h, h, S, "wgrad")]
     for i, (M, N, K, lay) in enumerate(shapes):
         if only and str(i) not in only.split(","):
             continue
