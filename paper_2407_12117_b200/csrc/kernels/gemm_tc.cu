@@ -41,7 +41,8 @@ constexpr int STAGE_BYTES = A_TILE_BYTES + B_TILE_BYTES;
 constexpr int NUM_THREADS = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int GROUP_M = 16;  // rasterisation: 16 M-tiles share a B panel in L2
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int SLAB_BYTES = 4 * 32 * 128;  // epilogue: one 32-row x 128 B slab per epilogue warp
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + SLAB_BYTES;
 
 struct EpiParams {
   int kind;
@@ -57,6 +58,7 @@ struct EpiParams {
   int head_dim;
   const float2* rope;
   long long pos0;
+  int staged;  // BF16/F32 stores through the shared-memory slab (MEMO_GEMM_EPI_STAGE)
 };
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* x) {
@@ -144,6 +146,90 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int m, int n
   }
 }
 
+// Staged row stores for the plain BF16 / F32 epilogues.  tcgen05.ld gives each
+// lane one accumulator row, so a direct store puts 32 rows x 16 B into every
+// warp store instruction, each half-filling a 32-byte L2 sector.  Here the
+// warp's 32 rows x 128 B go through an XOR-swizzled 4 KiB shared-memory slab
+// (conflict-free on both sides) and leave as 4 full 128-byte row segments per
+// store instruction.  Same values, same bytes, same addresses.
+__device__ __forceinline__ void slab_store(uint4* slab, const uint4 (&v)[8], uint32_t lane, uint8_t* row0,
+                                           long long ld_bytes, int rows_valid, int bytes_valid) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) slab[lane * 8 + (i ^ (lane & 7))] = v[i];
+  __syncwarp();
+  const int u = lane & 7;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int r = it * 4 + static_cast<int>(lane >> 3);
+    const uint4 w = slab[r * 8 + (u ^ (r & 7))];
+    if (r < rows_valid && u * 16 < bytes_valid)
+      *reinterpret_cast<uint4*>(row0 + r * ld_bytes + u * 16) = w;
+  }
+  __syncwarp();
+}
+
+// One epilogue warp's 32 rows x NCOLS columns of an accumulator buffer.
+// t_row: TMEM address of the warp's lane quarter at the tile's column 0;
+// m0: output row of lane 0; n_base: output column of the tile's column 0.
+template <int NCOLS>
+__device__ __forceinline__ void epilogue_rows(const EpiParams& ep, uint4* slab, uint32_t t_row, int m0,
+                                              int M, int n_base, int N, uint32_t lane) {
+  if (ep.staged && ep.kind == GEMM_EPI_BF16) {
+#pragma unroll 1
+    for (int c = 0; c < NCOLS / 64; ++c) {
+      const int n0 = n_base + c * 64;
+      if (n0 >= N) break;
+      uint32_t r0[32], r1[32];
+      dev::tmem_ld32(t_row + c * 64, r0);
+      dev::tmem_ld32(t_row + c * 64 + 32, r1);
+      dev::tmem_ld_wait_regs(r0, r1);
+      uint4 v[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[i] = make_uint4(dev::pack_bf16(__uint_as_float(r0[8 * i + 0]), __uint_as_float(r0[8 * i + 1])),
+                          dev::pack_bf16(__uint_as_float(r0[8 * i + 2]), __uint_as_float(r0[8 * i + 3])),
+                          dev::pack_bf16(__uint_as_float(r0[8 * i + 4]), __uint_as_float(r0[8 * i + 5])),
+                          dev::pack_bf16(__uint_as_float(r0[8 * i + 6]), __uint_as_float(r0[8 * i + 7])));
+        v[4 + i] = make_uint4(dev::pack_bf16(__uint_as_float(r1[8 * i + 0]), __uint_as_float(r1[8 * i + 1])),
+                              dev::pack_bf16(__uint_as_float(r1[8 * i + 2]), __uint_as_float(r1[8 * i + 3])),
+                              dev::pack_bf16(__uint_as_float(r1[8 * i + 4]), __uint_as_float(r1[8 * i + 5])),
+                              dev::pack_bf16(__uint_as_float(r1[8 * i + 6]), __uint_as_float(r1[8 * i + 7])));
+      }
+      slab_store(slab, v, lane,
+                 reinterpret_cast<uint8_t*>(reinterpret_cast<__nv_bfloat16*>(ep.c) + m0 * ep.ldc + n0),
+                 ep.ldc * 2, M - m0, (N - n0) * 2);
+    }
+    return;
+  }
+  if (ep.staged && ep.kind == GEMM_EPI_F32) {
+#pragma unroll 1
+    for (int c = 0; c < NCOLS / 32; ++c) {
+      const int n0 = n_base + c * 32;
+      if (n0 >= N) break;
+      uint32_t r[32];
+      dev::tmem_ld32(t_row + c * 32, r);
+      dev::tmem_ld_wait_regs(r);
+      uint4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = make_uint4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+      slab_store(slab, v, lane, reinterpret_cast<uint8_t*>(reinterpret_cast<float*>(ep.c) + m0 * ep.ldc + n0),
+                 ep.ldc * 4, M - m0, (N - n0) * 4);
+    }
+    return;
+  }
+  const int m = m0 + static_cast<int>(lane);
+#pragma unroll 1
+  for (int c = 0; c < NCOLS / 32; ++c) {
+    uint32_t r[32];
+    dev::tmem_ld32(t_row + c * 32, r);
+    dev::tmem_ld_wait_regs(r);
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
+    if (m < M) epilogue_chunk(ep, m, n_base + c * 32, N, x);
+  }
+}
+
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -157,6 +243,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint4* slab = reinterpret_cast<uint4*>(smem + STAGES * STAGE_BYTES + 256);
 
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
@@ -278,17 +365,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       dev::mbar_wait(&tfull_bar[buf], acc_phase);
       dev::tc_fence_after();
-      const int m = mb * BM + q * 32 + lane;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        dev::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * BN + c * 32, r);
-        dev::tmem_ld_wait_regs(r);
-        float x[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
-        if (m < M) epilogue_chunk(ep, m, nb * BN + c * 32, N, x);
-      }
+      epilogue_rows<BN>(ep, slab + q * 256, tmem_base + ((q * 32) << 16) + buf * BN, mb * BM + q * 32, M,
+                        nb * BN, N, lane);
       dev::tc_fence_before();
       dev::mbar_arrive(&tempty_bar[buf]);
     }
@@ -315,7 +393,7 @@ constexpr int P_STAGES = 6;
 constexpr int P_A_BYTES = P_BM * BK * 2;         // 16 KiB
 constexpr int P_B_BYTES = (P_BN / 2) * BK * 2;   // 16 KiB
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256 + SLAB_BYTES;
 constexpr int P_GROUP_M = 16;  // raster band of pair tiles (8 measured slower)
 
 template <bool A_MN, bool B_MN>
@@ -330,6 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + P_STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint4* slab = reinterpret_cast<uint4*>(smem + P_STAGES * P_STAGE_BYTES + 256);
 
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
@@ -452,17 +531,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       dev::mbar_wait(&tfull_bar[buf], acc_phase);
       dev::tc_fence_after();
-      const int m = mb * 2 * P_BM + rank * P_BM + q * 32 + lane;
-#pragma unroll 1
-      for (int c = 0; c < P_BN / 32; ++c) {
-        uint32_t r[32];
-        dev::tmem_ld32(tmem_base + ((q * 32) << 16) + buf * P_BN + c * 32, r);
-        dev::tmem_ld_wait_regs(r);
-        float x[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(r[i]);
-        if (m < M) epilogue_chunk(ep, m, nb * P_BN + c * 32, N, x);
-      }
+      epilogue_rows<P_BN>(ep, slab + q * 256, tmem_base + ((q * 32) << 16) + buf * P_BN,
+                          mb * 2 * P_BM + rank * P_BM + q * 32, M, nb * P_BN, N, lane);
       dev::tc_fence_before();
       dev::mbar_arrive_cluster(dev::mapa(dev::smem_u32(&tempty_bar[buf]), 0));
     }
@@ -515,6 +585,11 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   ep.head_dim = d.head_dim;
   ep.rope = reinterpret_cast<const float2*>(d.rope);
   ep.pos0 = d.pos0;
+  static const int staged = [] {  // MEMO_GEMM_EPI_STAGE=0: direct row-per-thread stores (ablation)
+    const char* e = getenv("MEMO_GEMM_EPI_STAGE");
+    return e ? (atoi(e) != 0 ? 1 : 0) : 1;
+  }();
+  ep.staged = staged;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN>,
