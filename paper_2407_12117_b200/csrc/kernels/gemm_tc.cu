@@ -11,7 +11,9 @@
 // ring; one thread issues tcgen05.mma (M=128, N=256, K=16) into a
 // double-buffered TMEM accumulator so the epilogue of tile i overlaps the
 // main loop of tile i+1.  Epilogues are fused: bf16/f32 store, f32
-// accumulate, residual add, and the RoPE-rotating Q/K/V split.
+// accumulate, residual add, and the RoPE-rotating Q/K/V split.  The plain
+// bf16/f32 epilogues turn their row-per-lane TMEM values around in a
+// shared-memory slab so global stores leave as full 128-byte row segments.
 //
 // The K loop order is the same for every output row, so recomputing a token
 // suffix reproduces the full-pass rows bit for bit (MEMO's recompute must be
