@@ -327,6 +327,27 @@ __device__ __forceinline__ void mma2_bf16_ss_w(uint32_t d_tmem, uint64_t a_desc,
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// 2-D tile load multicast to the same shared-memory offset in every CTA of
+// `mask`; each destination CTA's barrier at `bar`'s offset gets the tx bytes.
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+// Single-CTA MMAs: arrive on the barrier at `bar`'s offset in every CTA of
+// `mask` once this thread's prior tcgen05 ops complete.
+__device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 // Arrive (once each) on the barrier at the same offset in every CTA of `mask`
 // when the leader's prior pair MMAs complete.
 __device__ __forceinline__ void mma2_commit_mc_w(uint64_t* bar, uint16_t mask) {

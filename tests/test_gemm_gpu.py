@@ -114,3 +114,41 @@ def test_gemm_cta_pair_ablation():
     env = dict(os.environ, MEMO_GEMM_PAIR="1")
     out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "pair ok" in out.stdout, out.stdout + out.stderr
+
+
+def test_gemm_b_multicast_cluster_bitwise():
+    """MEMO_GEMM_MC=1 (single-CTA tiles in 2-CTA clusters, B shared by TMA
+    multicast): bitwise equal to the plain single-CTA kernel on all three
+    layouts, with odd M-tile counts (the partner of the last tile is empty)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys, torch; sys.path.insert(0, %r)\n"
+        "from tests.test_gemm_gpu import _gemm, _rand\n"
+        "outs = []\n"
+        "for (M, N, K) in [(128, 256, 64), (200, 512, 192), (384, 768, 4096), (1152, 2048, 1024), (640, 288, 512)]:\n"
+        "    torch.manual_seed(M + N + K)\n"
+        "    a, b = _rand(M, K), _rand(N, K)\n"
+        "    c = torch.empty(M, N, device='cuda', dtype=torch.bfloat16)\n"
+        "    _gemm(M, N, K, a, K, 0, b, K, 0, 0, c, N); outs.append(c.cpu())\n"
+        "    bt = b.t().contiguous()\n"
+        "    c2 = torch.empty(M, N, device='cuda', dtype=torch.float32)\n"
+        "    _gemm(M, N, K, a, K, 0, bt, N, 1, 1, c2, N); outs.append(c2.cpu())\n"
+        "    at = a.t().contiguous()\n"
+        "    c3 = torch.empty(M, N, device='cuda', dtype=torch.float32)\n"
+        "    _gemm(M, N, K, at, M, 1, bt, N, 1, 1, c3, N); outs.append(c3.cpu())\n"
+        "torch.save(outs, sys.argv[1])\n" % root)
+    res = []
+    with tempfile.TemporaryDirectory() as d:
+        for mc in ("0", "1"):
+            path = os.path.join(d, f"mc{mc}.pt")
+            env = dict(os.environ, MEMO_GEMM_PAIR="0", MEMO_GEMM_MC=mc)
+            out = subprocess.run([sys.executable, "-c", script, path], env=env, capture_output=True, text=True,
+                                 timeout=300)
+            assert out.returncode == 0, out.stdout + out.stderr
+            res.append(torch.load(path))
+    for x, y in zip(*res):
+        assert torch.equal(x, y)
