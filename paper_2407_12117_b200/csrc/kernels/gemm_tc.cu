@@ -234,7 +234,7 @@ __device__ __forceinline__ void epilogue_rows(const EpiParams& ep, uint4* slab, 
   }
 }
 
-template <bool A_MN, bool B_MN, bool MC>
+template <bool A_MN, bool B_MN, int CL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b, int M, int N, int K,
@@ -254,14 +254,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int m_tiles = (M + BM - 1) / BM;
   const int n_tiles = (N + BN - 1) / BN;
-  // MC: a 2-CTA cluster takes M-tiles 2u and 2u+1 of one N column; each CTA
-  // loads its own A and half of the shared B tile, multicast to both.  The
-  // per-row K order is unchanged, so results equal the plain kernel's bitwise.
+  // CL = 2: a 2-CTA cluster takes M-tiles 2u and 2u+1 of one N column; each
+  // CTA loads its own A and half of the shared B tile, multicast to both.
+  // CL = 4: a 2x2 cluster takes M-tiles 2u+rm and N-tiles 2v+rn; A is shared
+  // by the two CTAs of one rm and B by the two of one rn, each loaded half by
+  // each sharer.  The per-row K order is unchanged, so results equal the
+  // unclustered kernel's bitwise.
+  constexpr bool MC = CL > 1;
   const uint32_t rank = MC ? dev::cluster_ctarank() : 0;
-  const int first = MC ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-  const int stride = MC ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  const uint32_t rm = CL == 4 ? (rank & 1) : rank;  // M position in the cluster; also B's half
+  const uint32_t rn = CL == 4 ? (rank >> 1) : 0;    // N position in the cluster; also A's half
+  const int first = static_cast<int>(blockIdx.x) / CL;
+  const int stride = static_cast<int>(gridDim.x) / CL;
   const int m_units = MC ? (m_tiles + 1) / 2 : m_tiles;
-  const int num_tiles = m_units * n_tiles;
+  const int n_units = CL == 4 ? (n_tiles + 1) / 2 : n_tiles;
+  const int num_tiles = m_units * n_units;
   const int group_u = MC ? max(1, group_m / 2) : group_m;
   const int num_kb = (K + BK - 1) / BK;
 
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     dev::tma_prefetch_desc(&map_b);
     for (int s = 0; s < STAGES; ++s) {
       dev::mbar_init(&full_bar[s], 1);
-      dev::mbar_init(&empty_bar[s], MC ? 2 : 1);
+      dev::mbar_init(&empty_bar[s], CL);
     }
     for (int b = 0; b < 2; ++b) {
       dev::mbar_init(&tfull_bar[b], 1);
@@ -286,14 +293,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto tile_coords = [&](int t, int& mb, int& nb) {
-    const int group_size = group_u * n_tiles;
+    const int group_size = group_u * n_units;
     const int g = t / group_size;
     const int first_m = g * group_u;
     const int gm = min(group_u, m_units - first_m);
     const int local = t - g * group_size;
     mb = first_m + local % gm;
     nb = local / gm;
-    if (MC) mb = 2 * mb + static_cast<int>(rank);
+    if (MC) mb = 2 * mb + static_cast<int>(rm);
+    if (CL == 4) nb = 2 * nb + static_cast<int>(rn);
   };
 
   if (warp == 0) {
@@ -309,7 +317,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_TILE_BYTES;
           dev::mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
-          if (!A_MN) {
+          if (CL == 4) {
+            const uint16_t mask_a = static_cast<uint16_t>((1u << rm) | (1u << (rm + 2)));
+            if (!A_MN)
+              dev::tma_load_2d_mc(sa + rn * (A_TILE_BYTES / 2), &map_a, &full_bar[stage], kb * BK,
+                                  mb * BM + static_cast<int>(rn) * (BM / 2), mask_a);
+            else
+              dev::tma_load_2d_mc(sa + rn * 8192, &map_a, &full_bar[stage], mb * BM + static_cast<int>(rn) * 64,
+                                  kb * BK, mask_a);
+          } else if (!A_MN) {
             dev::tma_load_2d(sa, &map_a, &full_bar[stage], kb * BK, mb * BM);
           } else {
 #pragma unroll
@@ -318,14 +334,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                kb * BK);
           }
           if (MC) {
+            const uint16_t mask_b = static_cast<uint16_t>(CL == 4 ? (3u << (2 * rn)) : 3u);
             if (!B_MN) {
-              dev::tma_load_2d_mc(sb + rank * (B_TILE_BYTES / 2), &map_b, &full_bar[stage], kb * BK,
-                                  nb * BN + static_cast<int>(rank) * (BN / 2), 0x3);
+              dev::tma_load_2d_mc(sb + rm * (B_TILE_BYTES / 2), &map_b, &full_bar[stage], kb * BK,
+                                  nb * BN + static_cast<int>(rm) * (BN / 2), mask_b);
             } else {
 #pragma unroll
               for (int j = 0; j < BN / 128; ++j) {
-                const int jj = static_cast<int>(rank) * (BN / 128) + j;
-                dev::tma_load_2d_mc(sb + jj * 8192, &map_b, &full_bar[stage], nb * BN + jj * 64, kb * BK, 0x3);
+                const int jj = static_cast<int>(rm) * (BN / 128) + j;
+                dev::tma_load_2d_mc(sb + jj * 8192, &map_b, &full_bar[stage], nb * BN + jj * 64, kb * BK, mask_b);
               }
             }
           } else if (!B_MN) {
@@ -371,7 +388,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             dev::mma_bf16_ss_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
           if (MC)
-            dev::mma_commit_mc_w(&empty_bar[stage], 0x3);  // both CTAs wrote this stage's B
+            dev::mma_commit_mc_w(&empty_bar[stage], CL == 4 ? 0xF : 0x3);  // the sharers wrote this stage
           else
             dev::mma_commit_w(&empty_bar[stage]);
           if (++stage == STAGES) {
@@ -579,10 +596,6 @@ template <bool A_MN, bool B_MN>
 cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   CUtensorMap ma, mb;
   bool ok;
-  if (!A_MN)
-    ok = make_tma_2d_bf16(&ma, d.a, d.K, d.M, d.lda, BK, BM);
-  else
-    ok = make_tma_2d_bf16(&ma, d.a, d.M, d.K, d.lda, 64, BK);
   // CTA-pair 256x256 tiles (cta_group::2) where they measured faster: forward-
   // layout GEMMs (both operands K-major) with a short K and a wide N -- the QKV,
   // gate/up and classifier-logit projections (7 % / 6 % at 128K, interleaved
@@ -598,11 +611,18 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   // Single-CTA tiles run in 2-CTA clusters that share each B tile by TMA
   // multicast (half the B bytes per CTA; bitwise equal to unclustered tiles):
   // 3 % less GEMM time per cfg2 step.  MEMO_GEMM_MC=0 launches them unclustered.
-  static const bool mc_env = [] {
+  // MEMO_GEMM_MC=4: 2x2 clusters that also share A (experiment).
+  static const int mc_env = [] {
     const char* e = getenv("MEMO_GEMM_MC");
-    return !e || atoi(e) != 0;
+    const int v = e ? atoi(e) : 2;
+    return v == 4 ? 4 : (v != 0 ? 2 : 1);
   }();
-  const bool mc = !pair && mc_env;
+  const int cl = pair ? 1 : mc_env;
+  const bool mc = cl > 1;
+  if (!A_MN)
+    ok = make_tma_2d_bf16(&ma, d.a, d.K, d.M, d.lda, BK, cl == 4 ? BM / 2 : BM);
+  else
+    ok = make_tma_2d_bf16(&ma, d.a, d.M, d.K, d.lda, 64, BK);
   if (!B_MN)
     ok = ok && make_tma_2d_bf16(&mb, d.b, d.K, d.N, d.ldb, BK, (pair || mc) ? BN / 2 : BN);
   else
@@ -629,9 +649,11 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   ep.staged = staged;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN, false>,
+    cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN, 1>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN, true>,
+    cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN, 2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN, 4>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(gemm_tc2_kernel<A_MN, B_MN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
@@ -651,23 +673,36 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   }();
   const int group_m = env_group_m > 0 ? env_group_m : GROUP_M;
   if (mc) {
-    const int units = ((d.M + 2 * BM - 1) / (2 * BM)) * ((d.N + BN - 1) / BN);
-    const int clusters = units < g_num_sms / 2 ? units : g_num_sms / 2;
+    const int units = ((d.M + 2 * BM - 1) / (2 * BM)) * ((d.N + (cl == 4 ? 2 : 1) * BN - 1) / ((cl == 4 ? 2 : 1) * BN));
+    auto kern = cl == 4 ? gemm_tc_kernel<A_MN, B_MN, 4> : gemm_tc_kernel<A_MN, B_MN, 2>;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<A_MN, B_MN, true>, ma, mb, d.M, d.N, d.K, ep, group_m);
+    // Persistent clusters: no more than can be co-resident (GPCs need not hold
+    // a whole number of clusters), else the surplus would run as a second wave.
+    static int resident[5] = {0, 0, 0, 0, 0};
+    if (resident[cl] == 0) {
+      cfg.gridDim = dim3(cl * (g_num_sms / cl));
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = g_num_sms / cl;
+      }
+      resident[cl] = n;
+    }
+    const int clusters = units < resident[cl] ? units : resident[cl];
+    cfg.gridDim = dim3(cl * clusters);
+    return cudaLaunchKernelEx(&cfg, kern, ma, mb, d.M, d.N, d.K, ep, group_m);
   }
-  gemm_tc_kernel<A_MN, B_MN, false><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, d.M, d.N,
+  gemm_tc_kernel<A_MN, B_MN, 1><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, d.M, d.N,
                                                                               d.K, ep, group_m);
   return cudaGetLastError();
 }

@@ -117,9 +117,10 @@ def test_gemm_cta_pair_ablation():
 
 
 def test_gemm_b_multicast_cluster_bitwise():
-    """MEMO_GEMM_MC=1 (single-CTA tiles in 2-CTA clusters, B shared by TMA
-    multicast): bitwise equal to the plain single-CTA kernel on all three
-    layouts, with odd M-tile counts (the partner of the last tile is empty)."""
+    """MEMO_GEMM_MC=1 (default: single-CTA tiles in 2-CTA clusters, B shared by
+    TMA multicast) and MEMO_GEMM_MC=4 (2x2 clusters sharing A and B): bitwise
+    equal to the unclustered kernel on all three layouts, with odd M- and
+    N-tile counts (a cluster's last tiles are empty)."""
     import os
     import subprocess
     import sys
@@ -143,12 +144,13 @@ def test_gemm_b_multicast_cluster_bitwise():
         "torch.save(outs, sys.argv[1])\n" % root)
     res = []
     with tempfile.TemporaryDirectory() as d:
-        for mc in ("0", "1"):
+        for mc in ("0", "1", "4"):
             path = os.path.join(d, f"mc{mc}.pt")
             env = dict(os.environ, MEMO_GEMM_PAIR="0", MEMO_GEMM_MC=mc)
             out = subprocess.run([sys.executable, "-c", script, path], env=env, capture_output=True, text=True,
                                  timeout=300)
             assert out.returncode == 0, out.stdout + out.stderr
             res.append(torch.load(path))
-    for x, y in zip(*res):
-        assert torch.equal(x, y)
+    for other in res[1:]:
+        for x, y in zip(res[0], other):
+            assert torch.equal(x, y)
