@@ -185,6 +185,9 @@ typedef struct memo_gemm_args {
   int32_t hidden, head_dim;
   const void* rope;
   int64_t pos0;
+  /* 0 = the product's kernel choice; 1 single-CTA, 2 2-CTA B-multicast cluster,
+   * 3 2x2 cluster, 4 CTA pair (cta_group::2): forced, for equivalence tests */
+  int32_t variant;
 } memo_gemm_args;
 int memo_gemm(const memo_gemm_args* args, void* stream);
 

@@ -437,12 +437,16 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu,
 // ------------------------------------------------------------------ cross-entropy
 // One block per token row of f32 logits: loss_row = lse - logit[label];
 // dlogits = bf16((softmax - onehot) * inv_n); rows with label < 0 give zeros.
+// inv_n = 1 / (labeled tokens of the batch) is read from device memory: it is
+// written with each batch's H2D, so a captured CUDA graph replays the current
+// batch's scale, not the capture-time one.
 __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits,
                                                  const int* __restrict__ labels,
                                                  __nv_bfloat16* __restrict__ dlogits,
                                                  float* __restrict__ loss_rows, int V,
-                                                 float inv_n) {
+                                                 const float* __restrict__ inv_n_dev) {
   const int row = blockIdx.x;
+  const float inv_n = *inv_n_dev;
   const float* lr = logits + static_cast<long long>(row) * V;
   __nv_bfloat16* dr = dlogits + static_cast<long long>(row) * V;
   const int label = labels[row];
@@ -490,8 +494,8 @@ __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logit
 }
 
 // Deterministic single-block sum of n floats into out[0], times `scale`.
-__global__ void sum_kernel(const float* __restrict__ v, long long n, float scale,
-                           float* __restrict__ out) {
+__global__ void sum_kernel(const float* __restrict__ v, long long n,
+                           const float* __restrict__ scale, float* __restrict__ out) {
   __shared__ double sh[1024];
   double s = 0.0;
   for (long long i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
@@ -501,7 +505,7 @@ __global__ void sum_kernel(const float* __restrict__ v, long long n, float scale
     if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[0] = static_cast<float>(sh[0] * scale);
+  if (threadIdx.x == 0) out[0] = static_cast<float>(sh[0] * *scale);
 }
 
 // ------------------------------------------------------------------ optimizer
@@ -639,8 +643,9 @@ __global__ void __launch_bounds__(256) ce_vp_grad_kernel(const float* __restrict
                                                          const int* __restrict__ labels, int v0,
                                                          __nv_bfloat16* __restrict__ dlogits,
                                                          float* __restrict__ loss_rows, int T, int V,
-                                                         float inv_n) {
+                                                         const float* __restrict__ inv_n_dev) {
   const int row = blockIdx.x;
+  const float inv_n = *inv_n_dev;
   const float* lr = logits + static_cast<long long>(row) * V;
   __nv_bfloat16* dr = dlogits + static_cast<long long>(row) * V;
   const int label = labels[row];
@@ -705,7 +710,7 @@ cudaError_t ce_vp_sum(const float* logits, const float* gmax, const int* labels,
 }
 cudaError_t ce_vp_grad(const float* logits, const float* gmax, const float* gstats,
                        const int* labels, int v0, __nv_bfloat16* dlogits, float* loss_rows, int T,
-                       int V, float inv_n, cudaStream_t st) {
+                       int V, const float* inv_n, cudaStream_t st) {
   ce_vp_grad_kernel<<<T, 256, 0, st>>>(logits, gmax, gstats, labels, v0, dlogits, loss_rows, T, V, inv_n);
   return cudaGetLastError();
 }
@@ -803,13 +808,13 @@ cudaError_t swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_
 }
 
 cudaError_t cross_entropy(const float* logits, const int* labels, __nv_bfloat16* dlogits,
-                          float* loss_rows, int T, int V, float inv_n, cudaStream_t st) {
+                          float* loss_rows, int T, int V, const float* inv_n, cudaStream_t st) {
   if (V % 4) return cudaErrorInvalidValue;
   ce_kernel<<<T, 256, 0, st>>>(logits, labels, dlogits, loss_rows, V, inv_n);
   return cudaGetLastError();
 }
 
-cudaError_t sum_scaled(const float* v, long long n, float scale, float* out, cudaStream_t st) {
+cudaError_t sum_scaled(const float* v, long long n, const float* scale, float* out, cudaStream_t st) {
   sum_kernel<<<1, 1024, 0, st>>>(v, n, scale, out);
   return cudaGetLastError();
 }

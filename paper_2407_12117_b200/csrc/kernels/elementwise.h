@@ -29,8 +29,8 @@ cudaError_t swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* act, long long S,
 cudaError_t swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* dact, __nv_bfloat16* dgu,
                        long long S, int F, cudaStream_t st);
 cudaError_t cross_entropy(const float* logits, const int* labels, __nv_bfloat16* dlogits,
-                          float* loss_rows, int T, int V, float inv_n, cudaStream_t st);
-cudaError_t sum_scaled(const float* v, long long n, float scale, float* out, cudaStream_t st);
+                          float* loss_rows, int T, int V, const float* inv_n, cudaStream_t st);
+cudaError_t sum_scaled(const float* v, long long n, const float* scale, float* out, cudaStream_t st);
 // The step counter lives on the device (`step`, incremented by the launch
 // itself) so a captured CUDA graph replays the optimizer correctly; `c12`
 // (float2) receives the bias corrections 1/(1-b1^t), 1/(1-b2^t).
@@ -50,6 +50,6 @@ cudaError_t ce_vp_sum(const float* logits, const float* gmax, const int* labels,
                       float* stats, int T, int V, cudaStream_t st);
 cudaError_t ce_vp_grad(const float* logits, const float* gmax, const float* gstats,
                        const int* labels, int v0, __nv_bfloat16* dlogits, float* loss_rows, int T,
-                       int V, float inv_n, cudaStream_t st);
+                       int V, const float* inv_n, cudaStream_t st);
 
 }  // namespace memo

@@ -24,6 +24,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -31,6 +32,10 @@
 #include "gemm_tc.h"
 #include "sm100.cuh"
 #include "tma_util.h"
+
+namespace {
+constexpr int MAX_DEVICES = 64;
+}
 
 namespace memo {
 namespace {
@@ -359,6 +364,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      // Producer tail: wait for every stage's last release.  With multicast the
+      // releases are tcgen05.commit arrivals from the peer CTAs' MMA warps, and
+      // the closing cluster_sync does not order those async arrivals: without
+      // this wait a CTA could exit while one is still landing in its smem.
+      for (int s = 0; s < STAGES; ++s) {
+        dev::mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     {
@@ -530,6 +546,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      // Producer tail: the leader's multicast commits release both CTAs'
+      // stages; wait for the last of them before teardown (see gemm_tc_kernel).
+      for (int s = 0; s < P_STAGES; ++s) {
+        dev::mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (++stage == P_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
     }
   } else if (warp == 1) {
     if (rank == 0) {
@@ -602,22 +627,22 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   // A/B, profiles/README.md); the single-CTA kernel everywhere else.  The choice
   // depends on (layout, N, K) only, never on M, so a recomputed row block runs
   // the same kernel as the forward and stays bitwise equal to it.
-  // MEMO_GEMM_PAIR=0/1 forces one kernel for every GEMM.
-  static const int pair_env = [] {
-    const char* e = getenv("MEMO_GEMM_PAIR");
-    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
-  }();
-  const bool pair = pair_env >= 0 ? pair_env == 1 : (!A_MN && !B_MN && d.K <= 4096 && d.N >= 8192);
   // Single-CTA tiles run in 2-CTA clusters that share each B tile by TMA
   // multicast (half the B bytes per CTA; bitwise equal to unclustered tiles):
-  // 3 % less GEMM time per cfg2 step.  MEMO_GEMM_MC=0 launches them unclustered.
-  // MEMO_GEMM_MC=4: 2x2 clusters that also share A (experiment).
-  static const int mc_env = [] {
-    const char* e = getenv("MEMO_GEMM_MC");
-    const int v = e ? atoi(e) : 2;
-    return v == 4 ? 4 : (v != 0 ? 2 : 1);
-  }();
-  const int cl = pair ? 1 : mc_env;
+  // 3 % less GEMM time per cfg2 step.  d.variant (tests and A/B tools only)
+  // forces one kernel: GEMM_VARIANT_SINGLE / _MC2 / _MC4 (2x2 clusters that
+  // also share A) / _PAIR.
+  bool pair;
+  int cl;
+  switch (d.variant) {
+    case GEMM_VARIANT_SINGLE: pair = false; cl = 1; break;
+    case GEMM_VARIANT_MC2: pair = false; cl = 2; break;
+    case GEMM_VARIANT_MC4: pair = false; cl = 4; break;
+    case GEMM_VARIANT_PAIR: pair = true; cl = 1; break;
+    default:
+      pair = !A_MN && !B_MN && d.K <= 4096 && d.N >= 8192;
+      cl = pair ? 1 : 2;
+  }
   const bool mc = cl > 1;
   if (!A_MN)
     ok = make_tma_2d_bf16(&ma, d.a, d.K, d.M, d.lda, BK, cl == 4 ? BM / 2 : BM);
@@ -642,11 +667,7 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   ep.head_dim = d.head_dim;
   ep.rope = reinterpret_cast<const float2*>(d.rope);
   ep.pos0 = d.pos0;
-  static const int staged = [] {  // MEMO_GEMM_EPI_STAGE=0: direct row-per-thread stores (ablation)
-    const char* e = getenv("MEMO_GEMM_EPI_STAGE");
-    return e ? (atoi(e) != 0 ? 1 : 0) : 1;
-  }();
-  ep.staged = staged;
+  ep.staged = 1;  // swizzled shared-memory slab stores (the direct stores remain for the fused epilogues)
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN, 1>,
@@ -667,11 +688,7 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   }
   const int tiles = ((d.M + BM - 1) / BM) * ((d.N + BN - 1) / BN);
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  static const int env_group_m = [] {  // MEMO_GEMM_GROUP_M: raster band override (experiments)
-    const char* e = getenv("MEMO_GEMM_GROUP_M");
-    return e ? atoi(e) : 0;
-  }();
-  const int group_m = env_group_m > 0 ? env_group_m : GROUP_M;
+  const int group_m = GROUP_M;
   if (mc) {
     const int units = ((d.M + 2 * BM - 1) / (2 * BM)) * ((d.N + (cl == 4 ? 2 : 1) * BN - 1) / ((cl == 4 ? 2 : 1) * BN));
     auto kern = cl == 4 ? gemm_tc_kernel<A_MN, B_MN, 4> : gemm_tc_kernel<A_MN, B_MN, 2>;
@@ -688,17 +705,22 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
     cfg.numAttrs = 1;
     // Persistent clusters: no more than can be co-resident (GPCs need not hold
     // a whole number of clusters), else the surplus would run as a second wave.
-    static int resident[5] = {0, 0, 0, 0, 0};
-    if (resident[cl] == 0) {
+    // Cached per (device, cluster size); atomic because peer-local groups launch
+    // GEMMs from several host threads (all of them compute the same value).
+    static std::atomic<int> resident[MAX_DEVICES][5];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int>& slot = resident[dev < MAX_DEVICES ? dev : 0][cl];
+    int res = slot.load(std::memory_order_relaxed);
+    if (res == 0) {
       cfg.gridDim = dim3(cl * (g_num_sms / cl));
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      if (cudaOccupancyMaxActiveClusters(&res, kern, &cfg) != cudaSuccess || res <= 0) {
         cudaGetLastError();
-        n = g_num_sms / cl;
+        res = g_num_sms / cl;
       }
-      resident[cl] = n;
+      slot.store(res, std::memory_order_relaxed);
     }
-    const int clusters = units < resident[cl] ? units : resident[cl];
+    const int clusters = units < res ? units : res;
     cfg.gridDim = dim3(cl * clusters);
     return cudaLaunchKernelEx(&cfg, kern, ma, mb, d.M, d.N, d.K, ep, group_m);
   }

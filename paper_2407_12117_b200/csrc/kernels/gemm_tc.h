@@ -13,6 +13,16 @@ enum GemmEpilogue {
   GEMM_EPI_QKV_ROPE = 4,  // columns [0,h)->q (RoPE), [h,2h)->k (RoPE), [2h,3h)->v
 };
 
+// Kernel choice.  GEMM_VARIANT_AUTO is the product rule (gemm_tc.cu:launch);
+// the others force one kernel for the bitwise-equivalence tests and A/B tools.
+enum GemmVariant {
+  GEMM_VARIANT_AUTO = 0,
+  GEMM_VARIANT_SINGLE = 1,  // single-CTA 128x256 tiles, unclustered
+  GEMM_VARIANT_MC2 = 2,     // single-CTA tiles in 2-CTA clusters, B multicast
+  GEMM_VARIANT_MC4 = 3,     // 2x2 clusters, A and B multicast
+  GEMM_VARIANT_PAIR = 4,    // CTA-pair 256x256 tiles (cta_group::2)
+};
+
 // C = A . B^T with A logical [M, K], B logical [N, K].
 //   a_mn_major = 0: A stored [M][lda], K contiguous;  1: stored [K][lda], M contiguous.
 //   b_mn_major = 0: B stored [N][ldb], K contiguous;  1: stored [K][ldb], N contiguous.
@@ -37,6 +47,7 @@ struct GemmDesc {
   int head_dim = 0;
   const void* rope = nullptr;  // float2 [positions][head_dim/2] (cos, sin)
   long long pos0 = 0;          // absolute position of row 0
+  int variant = GEMM_VARIANT_AUTO;
 };
 
 cudaError_t gemm_tc(const GemmDesc& d, cudaStream_t stream);

@@ -36,6 +36,7 @@ extern "C" int memo_gemm(const memo_gemm_args* a, void* stream) {
   d.head_dim = a->head_dim;
   d.rope = a->rope;
   d.pos0 = a->pos0;
+  d.variant = a->variant;
   cudaError_t e = memo::gemm_tc(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess)
     return set_error(MEMO_ERR_INTERNAL, std::string("memo_gemm: ") + cudaGetErrorString(e));

@@ -454,6 +454,7 @@ void Executor::allocate() {
   lab_ = reinterpret_cast<int*>(q); q += S * 4;
   csr_pos_ = reinterpret_cast<int*>(q); q += S * 4;
   csr_off_ = reinterpret_cast<int*>(q); q += (V + 1) * 4;
+  inv_n_dev_ = reinterpret_cast<float*>(q); q += 4;
   loss_dev_ = reinterpret_cast<float*>(up(reinterpret_cast<uintptr_t>(q), 256));
   adam_ctr_ = reinterpret_cast<int*>(loss_dev_ + 16);
   adam_c12_ = reinterpret_cast<float2*>(loss_dev_ + 32);
@@ -469,9 +470,9 @@ void Executor::allocate() {
     pinned_ = static_cast<char*>(hp);
   }
   void* sp = nullptr;
-  ck(cudaHostAlloc(&sp, S * 4 * 3 + (V + 1) * 4 + 64, cudaHostAllocDefault), "cudaHostAlloc(staging)");
+  ck(cudaHostAlloc(&sp, S * 4 * 3 + (V + 1) * 4 + 4 + 64, cudaHostAllocDefault), "cudaHostAlloc(staging)");
   staging_ = static_cast<char*>(sp);
-  loss_host_ = reinterpret_cast<float*>(staging_ + S * 4 * 3 + (V + 1) * 4);
+  loss_host_ = reinterpret_cast<float*>(staging_ + S * 4 * 3 + (V + 1) * 4 + 4);
 
   ck(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&os_, cudaStreamNonBlocking), "stream");
@@ -487,6 +488,7 @@ void Executor::allocate() {
   mk(ev_pre_mand_);
   mk(ev_pre_done_);
   ck(cudaEventCreate(&ev_start_), "event");
+  ck(cudaEventCreateWithFlags(&ev_staging_, cudaEventDisableTiming), "event");
   for (cudaEvent_t* e : {&ev_fork_, &ev_join_os_, &ev_join_ps_})
     ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
   if (comm_ && d_.t > 1) {
@@ -574,6 +576,7 @@ Executor::~Executor() {
     cudaStreamDestroy(st);
   }
   if (ev_start_) cudaEventDestroy(ev_start_);
+  if (ev_staging_) cudaEventDestroy(ev_staging_);
   for (cudaEvent_t e : {ev_fork_, ev_join_os_, ev_join_ps_})
     if (e) cudaEventDestroy(e);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
@@ -709,6 +712,16 @@ GemmDesc gd(int M, int N, int K, const void* a, long long lda, int amn, const vo
 
 void Executor::load_batch(const int* tokens, const int* labels) {
   const int S = d_.S, V = d_.V;
+  for (int t = 0; t < S; ++t) {
+    if (tokens[t] < 0 || tokens[t] >= V) throw ConfigError("token id out of range");
+    if (labels[t] >= V) throw ConfigError("label out of range");
+  }
+  int nl = 0;
+  for (int t = 0; t < S; ++t) nl += labels[t] >= 0;
+  if (nl == 0) throw ConfigError("batch has no labeled tokens");
+  // The previous batch's H2D may still be queued on cs_ behind a running step:
+  // staging_ is rewritten only after it has left.
+  ck(cudaEventSynchronize(ev_staging_), "staging reuse");
   int* st = reinterpret_cast<int*>(staging_);
   std::memcpy(st, tokens, S * 4);
   std::memcpy(st + S, labels, S * 4);
@@ -716,21 +729,19 @@ void Executor::load_batch(const int* tokens, const int* labels) {
   int* pos = st + 2 * S;
   int* offs = st + 3 * S;
   std::fill(offs, offs + V + 1, 0);
-  for (int t = 0; t < S; ++t)
-    if (tokens[t] < 0 || tokens[t] >= V) throw ConfigError("token id out of range");
   // embedding-gradient CSR over this rank's token shard (positions are local rows)
   const int t0 = d_.r * d_.Sl, t1 = t0 + d_.Sl;
   for (int t = t0; t < t1; ++t) ++offs[tokens[t] + 1];
   for (int v = 0; v < V; ++v) offs[v + 1] += offs[v];
   std::vector<int> fillp(offs, offs + V);
   for (int t = t0; t < t1; ++t) pos[fillp[tokens[t]]++] = t - t0;
-  n_labeled_ = 0;
-  for (int t = 0; t < S; ++t) n_labeled_ += labels[t] >= 0;
-  if (n_labeled_ == 0) throw ConfigError("batch has no labeled tokens");
-  // tok | lab | csr_pos | csr_off are contiguous on both sides
-  ck(cudaMemcpyAsync(tok_, staging_, static_cast<size_t>(3 * S + V + 1) * 4, cudaMemcpyHostToDevice, cs_),
+  n_labeled_ = nl;
+  reinterpret_cast<float*>(offs + V + 1)[0] = 1.0f / static_cast<float>(nl);
+  // tok | lab | csr_pos | csr_off | inv_n are contiguous on both sides
+  ck(cudaMemcpyAsync(tok_, staging_, static_cast<size_t>(3 * S + V + 2) * 4, cudaMemcpyHostToDevice, cs_),
      "H2D batch");
-  stats_.h2d_bytes = static_cast<double>(3 * S + V + 1) * 4;
+  ck(cudaEventRecord(ev_staging_, cs_), "record");
+  stats_.h2d_bytes = static_cast<double>(3 * S + V + 2) * 4;
 }
 
 void Executor::offload(int i) {
@@ -940,7 +951,7 @@ void Executor::classifier() {
   float* logits = static_cast<float*>(arena_ptr(seg_cls_bwd_, "logits"));
   auto* dlog = static_cast<__nv_bfloat16*>(arena_ptr(seg_cls_bwd_, "dlogits"));
   float* part = static_cast<float*>(arena_ptr(seg_cls_bwd_, "cls_part"));
-  const float inv_n = 1.0f / static_cast<float>(n_labeled_);
+  const float* inv_n = inv_n_dev_;  // 1/n_labeled of the loaded batch (device, see load_batch)
   for (int c0 = 0; c0 < S; c0 += T) {
     const int t = std::min(T, S - c0);
     const __nv_bfloat16* xc = xf + static_cast<Bytes>(c0) * h;
@@ -1288,7 +1299,7 @@ void Executor::classifier_tp() {
   float* stats = static_cast<float*>(arena_ptr(sb, "ce_stats"));  // [lmax | gmax | lsum,ltgt | gsum,gtgt]
   const size_t shard = static_cast<size_t>(Sl) * h;
   ag(comm_.get(), xf, xf_full, shard, cs_);
-  const float inv_n = 1.0f / static_cast<float>(n_labeled_);
+  const float* inv_n = inv_n_dev_;  // 1/n_labeled of the loaded batch (device, see load_batch)
   const int v0 = d_.r * Vl;
   for (int c0 = 0; c0 < S; c0 += T) {
     const int t = std::min(T, S - c0);

@@ -186,6 +186,7 @@ class Executor {
   float2* rope_ = nullptr;
   int *tok_ = nullptr, *lab_ = nullptr, *csr_off_ = nullptr, *csr_pos_ = nullptr;
   float* loss_dev_ = nullptr;
+  float* inv_n_dev_ = nullptr;  // 1/n_labeled of the loaded batch, H2D with the batch
   int n_labeled_ = 0;
   int* adam_ctr_ = nullptr;   // device AdamW step counter (graph-replay safe)
   float2* adam_c12_ = nullptr;  // device bias corrections of the current step
@@ -203,6 +204,7 @@ class Executor {
   std::vector<cudaStream_t> xcs_;  // per-peer pull streams of the all-gather (parallel copy engines)
   std::vector<cudaEvent_t> ev_blk_;  // per row block landed (xs_ -> cs_)
   cudaEvent_t ev_cs2xs_ = nullptr, ev_xs2cs_ = nullptr;
+  cudaEvent_t ev_staging_ = nullptr;  // last batch H2D out of staging_ (staging reuse)
   cudaEvent_t ev_start_ = nullptr, ev_fork_ = nullptr, ev_join_os_ = nullptr, ev_join_ps_ = nullptr;
   // CUDA graph of one step (ExecOptions::cuda_graph): captured on the second call
   void record_step();

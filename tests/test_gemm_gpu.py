@@ -30,7 +30,7 @@ def _rand(*shape):
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (384, 768, 4096),
                                    (200, 256, 192), (1024, 2048, 1024)])
 @pytest.mark.parametrize("layout", ["fwd", "dgrad", "wgrad"])
-def test_gemm_layouts(M, N, K, layout):
+def test_gemm_layouts(M, N, K, layout, variant=0):
     torch.manual_seed(0)
     if layout == "fwd":      # A [M,K] K-major, B [N,K] K-major
         A = _rand(M, K); B = _rand(N, K)
@@ -45,11 +45,11 @@ def test_gemm_layouts(M, N, K, layout):
         ref = As.float().t() @ Bs.float()
         a, lda, amn, b, ldb, bmn = As, M, 1, Bs, N, 1
     out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
-    _gemm(M, N, K, a, lda, amn, b, ldb, bmn, 1, out, N)
+    _gemm(M, N, K, a, lda, amn, b, ldb, bmn, 1, out, N, variant=variant)
     err = (out - ref).abs().max().item()
     assert err <= 1e-3 * (1 + ref.abs().max().item()), err
     outb = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-    _gemm(M, N, K, a, lda, amn, b, ldb, bmn, 0, outb, N)
+    _gemm(M, N, K, a, lda, amn, b, ldb, bmn, 0, outb, N, variant=variant)
     torch.testing.assert_close(outb.float(), ref.to(torch.bfloat16).float(), rtol=1e-2, atol=1e-2)
 
 
@@ -97,60 +97,36 @@ def test_gemm_qkv_rope_epilogue():
     torch.testing.assert_close(v.float(), y[:, 2 * h:], rtol=1e-2, atol=1e-2)
 
 
-def test_gemm_cta_pair_ablation():
-    """MEMO_GEMM_PAIR=1 (CTA-pair 256x256 tiles, cta_group::2): all three layouts,
-    ragged M and N, against the fp32 reference in a fresh process."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    script = (
-        "import sys, torch; sys.path.insert(0, %r)\n"
-        "from tests.test_gemm_gpu import test_gemm_layouts\n"
-        "for shp in [(128, 256, 64), (200, 256, 192), (1024, 2048, 1024), (640, 288, 4096)]:\n"
-        "    for lay in ('fwd', 'dgrad', 'wgrad'):\n"
-        "        test_gemm_layouts(*shp, lay)\n"
-        "print('pair ok')\n" % root)
-    env = dict(os.environ, MEMO_GEMM_PAIR="1")
-    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0 and "pair ok" in out.stdout, out.stdout + out.stderr
+def test_gemm_cta_pair_variant():
+    """variant=4 (CTA-pair 256x256 tiles, cta_group::2) forced on all three
+    layouts, ragged M and N, against the fp32 reference."""
+    for shp in [(128, 256, 64), (200, 256, 192), (1024, 2048, 1024), (640, 288, 4096)]:
+        for lay in ("fwd", "dgrad", "wgrad"):
+            test_gemm_layouts(*shp, lay, variant=4)
 
 
 def test_gemm_b_multicast_cluster_bitwise():
-    """MEMO_GEMM_MC=1 (default: single-CTA tiles in 2-CTA clusters, B shared by
-    TMA multicast) and MEMO_GEMM_MC=4 (2x2 clusters sharing A and B): bitwise
-    equal to the unclustered kernel on all three layouts, with odd M- and
-    N-tile counts (a cluster's last tiles are empty)."""
-    import os
-    import subprocess
-    import sys
-    import tempfile
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    script = (
-        "import sys, torch; sys.path.insert(0, %r)\n"
-        "from tests.test_gemm_gpu import _gemm, _rand\n"
-        "outs = []\n"
-        "for (M, N, K) in [(128, 256, 64), (200, 512, 192), (384, 768, 4096), (1152, 2048, 1024), (640, 288, 512)]:\n"
-        "    torch.manual_seed(M + N + K)\n"
-        "    a, b = _rand(M, K), _rand(N, K)\n"
-        "    c = torch.empty(M, N, device='cuda', dtype=torch.bfloat16)\n"
-        "    _gemm(M, N, K, a, K, 0, b, K, 0, 0, c, N); outs.append(c.cpu())\n"
-        "    bt = b.t().contiguous()\n"
-        "    c2 = torch.empty(M, N, device='cuda', dtype=torch.float32)\n"
-        "    _gemm(M, N, K, a, K, 0, bt, N, 1, 1, c2, N); outs.append(c2.cpu())\n"
-        "    at = a.t().contiguous()\n"
-        "    c3 = torch.empty(M, N, device='cuda', dtype=torch.float32)\n"
-        "    _gemm(M, N, K, at, M, 1, bt, N, 1, 1, c3, N); outs.append(c3.cpu())\n"
-        "torch.save(outs, sys.argv[1])\n" % root)
+    """variant 2 (the default single-CTA kernel: 2-CTA clusters, B shared by TMA
+    multicast) and 3 (2x2 clusters sharing A and B): bitwise equal to the
+    unclustered kernel (variant 1) on all three layouts, with odd M- and N-tile
+    counts (a cluster's last tiles are empty)."""
     res = []
-    with tempfile.TemporaryDirectory() as d:
-        for mc in ("0", "1", "4"):
-            path = os.path.join(d, f"mc{mc}.pt")
-            env = dict(os.environ, MEMO_GEMM_PAIR="0", MEMO_GEMM_MC=mc)
-            out = subprocess.run([sys.executable, "-c", script, path], env=env, capture_output=True, text=True,
-                                 timeout=300)
-            assert out.returncode == 0, out.stdout + out.stderr
-            res.append(torch.load(path))
+    for var in (1, 2, 3):
+        outs = []
+        for (M, N, K) in [(128, 256, 64), (200, 512, 192), (384, 768, 4096), (1152, 2048, 1024), (640, 288, 512)]:
+            torch.manual_seed(M + N + K)
+            a, b = _rand(M, K), _rand(N, K)
+            c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            _gemm(M, N, K, a, K, 0, b, K, 0, 0, c, N, variant=var)
+            outs.append(c.clone())
+            bs = _rand(K, N)
+            c32 = torch.empty(M, N, device="cuda", dtype=torch.float32)
+            _gemm(M, N, K, a, K, 0, bs, N, 1, 1, c32, N, variant=var)
+            outs.append(c32.clone())
+            as_ = _rand(K, M)
+            _gemm(M, N, K, as_, M, 1, bs, N, 1, 1, c32, N, variant=var)
+            outs.append(c32.clone())
+        res.append(outs)
     for other in res[1:]:
         for x, y in zip(res[0], other):
             assert torch.equal(x, y)

@@ -193,3 +193,52 @@ def test_cuda_graph_replay_bitwise_equals_eager():
     assert P.validate_schedule(tl1, n, info1["swap"]) == []
     assert sum(e.kind == "recompute" for e in tl1) == 2
     assert info1["last_step_ms"] > 0
+
+
+def test_cuda_graph_replay_follows_each_batch_ignore_mask():
+    """The CE scale 1/n_labeled lives in device memory and travels with each
+    batch's H2D, so graph replays of batches with different ignore masks
+    (label < 0) give the eager executor's losses and gradients bit for bit
+    (a host-scalar scale would be frozen at capture)."""
+    n, h, H, F, V, S = 4, 256, 2, 768, 512, 1024
+    cfg = model(n, h, H, F, V, S)
+    toks, labels = O.tokens(22, V, S)
+    lab_a = labels.copy()
+    lab_b = labels.copy()
+    lab_b[: S // 3] = -1          # a third of the rows ignored
+    lab_c = labels.copy()
+    lab_c[::7] = -1
+    batches = [lab_a, lab_b, lab_a, lab_c, lab_b]
+    runs = {}
+    for graph in (0, 1):
+        with Executor(cfg, HW, seed=4, alpha=0.5, optimizer=0, ce_chunk=512, cuda_graph=graph) as ex:
+            out = []
+            for lab in batches:
+                out.append((ex.step(toks, lab), ex.read("grad/all")))
+            runs[graph] = out
+    for (l0, g0), (l1, g1) in zip(runs[0], runs[1]):
+        assert l0 == l1
+        assert np.array_equal(g0, g1)
+    # the losses differ across masks (the scale really changed)
+    assert runs[1][0][0] != runs[1][1][0]
+    ref_loss, _ = O.step(O.make_cfg(n, h, H, F, V, S), O.init_params(O.make_cfg(n, h, H, F, V, S), 4), toks, lab_b)
+    assert abs(runs[1][1][0] - ref_loss) <= 5e-3 * abs(ref_loss)
+
+
+def test_load_batch_rejects_out_of_range_ids():
+    """Token ids and labels >= V (and token ids < 0) are refused with
+    MEMO_ERR_INPUT before anything is copied; label -1 means ignore."""
+    from paper_2407_12117_b200 import _abi
+    n, h, H, F, V, S = 2, 256, 2, 768, 512, 512
+    cfg = model(n, h, H, F, V, S)
+    toks, labels = O.tokens(5, V, S)
+    with Executor(cfg, HW, seed=1, alpha=0.0, optimizer=0, ce_chunk=512) as ex:
+        good = ex.step(toks, labels)
+        for t, lab in ((toks, np.where(np.arange(S) == 7, V, labels)),
+                       (np.where(np.arange(S) == 3, V, toks), labels),
+                       (np.where(np.arange(S) == 3, -2, toks), labels),
+                       (toks, np.full(S, -1))):
+            with pytest.raises(_abi.MemoError) as e:
+                ex.step(t.astype(toks.dtype), lab.astype(labels.dtype))
+            assert e.value.code == _abi.MEMO_ERR_INPUT
+        assert ex.step(toks, labels) == good
