@@ -150,36 +150,63 @@ def host_link_bandwidth(torch, nbytes=1 << 31):
     return out
 
 
-def cpu_baseline(n_cfg, repeat=1):
-    """CPU oracle (oracle/llama_cpu.c, OpenMP on all host cores) on a bounded sample:
-    one layer of the workload's width at 256 tokens, full vocab; converted to the
-    workload's tokens/s through the reference FLOP model (schedule.hpp:57-61)."""
+def flop_terms(n, h, H, inter, V, S):
+    """The reference FLOP model in plain Python (schedule.hpp:44-61): params
+    P = V*h + n*(4h^2 + 2h*ffn + 4h) + 2h (+ V*h untied, ffn = the reference's
+    ffn_hidden = 3/2 of the SwiGLU width); FLOPs per sample = 6*s*P (dense)
+    + 6*n*h*s^2 (causal attention).  Returns (dense, attention)."""
+    ffn = inter * 3 // 2
+    p = V * h + n * (4 * h * h + 2 * h * ffn + 4 * h) + 2 * h + V * h
+    return 6.0 * S * p, 6.0 * n * h * float(S) * S
+
+
+def cpu_baseline(n_cfg, s_dense=128, v_dense=4096, s_attn=8192, h_attn=1):
+    """CPU oracle (oracle/llama_cpu.c, OpenMP on all host cores) on a bounded
+    sample, each FLOP term of the workload timed on its own:
+      * dense: one full-width layer (+ embedding/classifier over a `v_dense`
+        vocabulary) fwd+bwd at `s_dense` tokens, the sample's small attention
+        share removed with the attention rate below;
+      * attention: causal attention fwd+bwd of `h_attn` heads (D = the
+        workload's head dim) at `s_attn` tokens.
+    The workload step time is dense/rate_dense + attention/rate_attention
+    (reference FLOP model, flop_terms); value = tokens of the step / that time."""
+    import numpy as np
     from oracle import oracle as O
     n, h, H, inter, V, S, _ = n_cfg
-    s_sample = 256
-    ocfg = O.make_cfg(1, h, H, inter, V, s_sample)
-    params = O.init_params(ocfg, 1234)
-    toks, labels = synthetic_batch(1234, V, s_sample)
+    D = h // H
+    # attention rate
+    rng = np.random.default_rng(7)
+    qa, ka, va, da = (rng.standard_normal((s_attn, h_attn * D), dtype=np.float32) for _ in range(4))
     t0 = time.perf_counter()
-    for _ in range(repeat):
-        O.step(ocfg, params, toks, labels)
-    dt = (time.perf_counter() - t0) / repeat
-    from paper_2407_12117_b200 import planner as P
-    sample_cfg = P.ModelConfig(n_layers=1, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
-                               seq_len=s_sample, untied_classifier=True)
-    work_cfg = P.ModelConfig(n_layers=n, hidden=h, ffn_hidden=inter * 3 // 2, n_heads=H, vocab=V,
-                             seq_len=S, untied_classifier=True)
-    f_sample = P.estimate_flops_per_sample(sample_cfg, P.count_params(sample_cfg)["total"])
-    f_work = P.estimate_flops_per_sample(work_cfg, P.count_params(work_cfg)["total"])
-    cpu_flops = f_sample / dt
-    tokens_per_s = cpu_flops / (f_work / S)
+    O.attention(qa, ka, va, da, h_attn)
+    t_attn = time.perf_counter() - t0
+    _, f_attn_sample = flop_terms(1, h_attn * D, h_attn, 0, 0, s_attn)
+    rate_attn = f_attn_sample / t_attn
+    # dense rate
+    vs = min(V, v_dense)
+    ocfg = O.make_cfg(1, h, H, inter, vs, s_dense)
+    params = O.init_params(ocfg, 1234)
+    toks, labels = synthetic_batch(1234, vs, s_dense)
+    t0 = time.perf_counter()
+    O.step(ocfg, params, toks, labels)
+    t_dense_all = time.perf_counter() - t0
+    f_dense_s, f_attn_s = flop_terms(1, h, H, inter, vs, s_dense)
+    t_dense = max(t_dense_all - f_attn_s / rate_attn, 1e-9)
+    rate_dense = f_dense_s / t_dense
+    f_dense_w, f_attn_w = flop_terms(n, h, H, inter, V, S)
+    t_work = f_dense_w / rate_dense + f_attn_w / rate_attn
     cores = os.cpu_count()
-    return {"value": tokens_per_s, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": (f"oracle/llama_cpu.c fwd+bwd of 1 layer (h={h}, heads={H}, f={inter}, V={V}) at "
-                       f"{s_sample} tokens on {cores} OpenMP threads took {dt:.2f} s = "
-                       f"{cpu_flops / 1e9:.1f} GFLOP/s (reference FLOP model); value = that rate / "
-                       f"FLOPs-per-token of the workload"),
-            "sample_seconds": dt}
+    return {"value": S / t_work, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": (f"oracle/llama_cpu.c on {cores} OpenMP threads: dense part = 1 layer (h={h}, heads={H}, "
+                       f"f={inter}, V={vs}) fwd+bwd at {s_dense} tokens, {t_dense_all:.2f} s "
+                       f"({rate_dense / 1e9:.1f} GFLOP/s); attention part = causal attention fwd+bwd of "
+                       f"{h_attn} heads (D={D}) at {s_attn} tokens, {t_attn:.2f} s ({rate_attn / 1e9:.1f} "
+                       f"GFLOP/s); workload step = dense {f_dense_w:.3e} / dense rate + attention "
+                       f"{f_attn_w:.3e} / attention rate (reference FLOP model, schedule.hpp:57-61) = "
+                       f"{t_work:.0f} s"),
+            "sample_seconds": t_dense_all + t_attn,
+            "workload_step_s_extrapolated": t_work,
+            "dense_gflops": rate_dense / 1e9, "attention_gflops": rate_attn / 1e9}
 
 
 def reference_planner_ms(name):
@@ -205,19 +232,36 @@ def reference_planner_ms(name):
         os.unlink(f.name)
 
 
+def workload_config(name):
+    """The config keys both arms report for a workload (no run-dependent keys)."""
+    n, h, H, inter, V, S, desc = CONFIGS[name]
+    return {"workload": desc, "model": "llama-13b-arch" if h == 5120 else "llama-7b-arch", "n_layers": n,
+            "global_batch": 1, "seq_len": S}
+
+
 def run_reference(args, rank):
+    """The reference's CPU implementation of the step (the oracle port; the
+    reference itself has no model math) on this box's host cores.  Each step is
+    one bounded sample (cpu_baseline); the workload's tokens/s is extrapolated
+    per FLOP term.  Imports nothing from the product package."""
     if rank != 0:
         return
     n_cfg = CONFIGS[args.config]
+    for _ in range(min(args.warmup, 1)):
+        cpu_baseline(n_cfg)
+    t0 = time.perf_counter()
     samples = [cpu_baseline(n_cfg) for _ in range(max(1, args.steps))]
+    wall = time.perf_counter() - t0
     base = samples[-1]
     v = statistics.median(x["value"] for x in samples)
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            # one full workload step at the sampled rate (extrapolated from the bounded sample)
-            "ms_per_step": n_cfg[5] / v * 1e3 if v else None, "ms_per_step_extrapolated": True,
+            # measured wall of one step (= one bounded sample); the workload step it
+            # stands for is reported separately, extrapolated
+            "ms_per_step": wall / len(samples) * 1e3,
+            "workload_ms_per_step_extrapolated": n_cfg[5] / v * 1e3 if v else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": n_cfg[6], "cpu": "oracle port"},
+            "data": "synthetic", "config": {**workload_config(args.config), "parallelism": "cpu"},
             "cpu_baseline": {**base, "value": v},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     rp = reference_planner_ms(args.config)
@@ -235,6 +279,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step kernel by kernel (no CUDA graph)")
+    ap.add_argument("--no-swap-delta", action="store_true", help="skip the swap-disabled reference step")
     ap.add_argument("--watchdog", type=float, default=1800.0, help="abort the run after this many seconds")
     ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                     help="SP+TP collectives: peer memory over CUDA IPC (fused AG->GEMM / GEMM->RS) or NCCL")
@@ -389,6 +434,7 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    free_before, _ = torch.cuda.mem_get_info()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
@@ -398,6 +444,9 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    # MEMO's planned allocator never reorganises (allocator.hpp:264-285): device
+    # memory is the same before and after the timed steps
+    free_after, _ = torch.cuda.mem_get_info()
     tl = ex.timeline()  # last step
     info = ex.info()
     launches = info["kernel_launches"] * args.steps
@@ -424,6 +473,33 @@ def main():
         t = torch.tensor([e2e], device=ddev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = t.item()
+
+    # ---- the same step with swapping disabled (one rounding buffer per layer),
+    # when it fits: exposed swap as a step-time difference, T(swap) - T(no swap)
+    nosw_ms = None
+    if world == 1 and not args.no_swap_delta:
+        ex.close()
+        try:
+            exn = Executor(cfg, hw, alpha=forced_alpha, t_layer=t_layer, op_timing=0, cuda_graph=use_graph,
+                           swap_enabled=0)
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] no-swap reference step does not fit ({e})", file=sys.stderr)
+            exn = None
+        if exn is not None:
+            with exn:
+                sn = torch.cuda.ExternalStream(exn.stream)
+                exn.load_batch(toks, labels)
+                for _ in range(3):
+                    exn.step_resident()
+                torch.cuda.synchronize()
+                k = max(1, min(args.steps, 5))
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(sn)
+                for _ in range(k):
+                    exn.step_resident()
+                b.record(sn)
+                torch.cuda.synchronize()
+                nosw_ms = a.elapsed_time(b) / k
 
     # ---- MEMO report on the measured timeline (reference validator + simulator)
     swap = info0["swap"]
@@ -459,8 +535,8 @@ def main():
         "higher_is_better": True, "scaling": "strong" if mode == "tp" else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (splitmix64 tokens, counter-hash random-init weights)",
-        "config": {"workload": desc, "model": "llama-13b-arch" if h == 5120 else "llama-7b-arch", "n_layers": n, "global_batch": world,
-                   "seq_len": S, "parallelism": {"single": "single", "tp": f"sp+tp{world} ({comm})",
+        "config": {**workload_config(args.config), "global_batch": world if mode == "replicas" else 1,
+                   "parallelism": {"single": "single", "tp": f"sp+tp{world} ({comm})",
                                                  "replicas": f"replicas{world}"}[mode],
                    "l2": "working set (GB of activations) >> 126 MB L2; no flush needed",
                    "alpha": swap.alpha, "swap_tokens": info0["split"][0],
@@ -481,8 +557,16 @@ def main():
                      "algorithmic_flops_per_launch": dk["flops"] / dk["count"] if dk["count"] else None},
         "kernels": kernels,
         "memo": {"schedule_violations": violations, "sim": sim,
-                 "exposed_swap_s": sim["compute_blocked"],
-                 "exposed_swap_frac": sim["compute_blocked"] / sim["iteration_time"] if sim["iteration_time"] else None,
+                 # compute-stream gaps waiting on copy events (simulate, schedule.hpp:250-297)
+                 # + stalls on the copy event waited inside a layer (copy_wait_ms)
+                 "exposed_swap_s": sim["compute_blocked"] + info["copy_wait_ms"] * 1e-3,
+                 "exposed_swap_frac": ((sim["compute_blocked"] + info["copy_wait_ms"] * 1e-3) / sim["iteration_time"]
+                                       if sim["iteration_time"] else None),
+                 "in_layer_copy_wait_s": info["copy_wait_ms"] * 1e-3,
+                 "no_swap_ms_per_step": nosw_ms,
+                 "exposed_swap_delta_s": (t_max - nosw_ms) * 1e-3 if nosw_ms else None,
+                 "hbm_free_before_timed_steps": free_before, "hbm_free_after_timed_steps": free_after,
+                 "hbm_unchanged_over_timed_steps": free_before == free_after,
                  "forward_blocked_s": sim["forward_blocked"],
                  "offload_GBps": info["offload_bytes"] / off_s / 1e9 if off_s else None,
                  "prefetch_GBps": info["prefetch_bytes"] / pre_s / 1e9 if pre_s else None,

@@ -262,6 +262,10 @@ typedef struct memo_exec_info {
    * 2 attn_bwd_dkdv, 3 attn_bwd_dq, 4 gemm — device ms, algorithmic FLOPs, launches */
   double op_ms[5], op_flops[5];
   int32_t op_count[5];
+  /* compute-stream stall (ms) of the last step on copy events waited INSIDE a
+   * layer (layer i's down projection waits for the layer_input rows of layer
+   * i-1's offload); not visible as a timeline gap, so reported here */
+  double copy_wait_ms;
 } memo_exec_info;
 
 int memo_exec_options_default(memo_exec_options* opt);
@@ -286,6 +290,14 @@ int memo_exec_get_info(memo_exec* ctx, memo_exec_info* info);
  * (json_io.hpp:189 to_json(GlobalPlan).dump()). */
 int memo_exec_trace(memo_exec* ctx, char** text);
 int memo_exec_plan(memo_exec* ctx, char** json);
+/* Replay an externally computed plan instead of the executor's own (SURVEY
+ * §8b memo_bind_plan).  plan_json = to_json(GlobalPlan).dump() (json_io.hpp:
+ * 189-202) of a plan of memo_exec_trace()'s trace, e.g. from the reference's
+ * actmem::plan_model.  Status 2 if it does not place exactly this trace's
+ * transient requests or places two live-together requests on shared bytes;
+ * 3 if its total_peak exceeds the arena reserved at creation.  Call before
+ * the first step. */
+int memo_exec_bind_plan(memo_exec* ctx, const char* plan_json);
 /* Device pointer of a named tensor: "<param>", "grad/<param>", "master/<param>"
  * with param in {embedding, g1, wqkv, wo, g2, wgu, wd, gf, wcls, all}
  * (layer = -1 for non-layer params), or "act/<skeletal component>". */

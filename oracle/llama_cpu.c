@@ -328,6 +328,16 @@ static void attn_bwd(const float* q, const float* k, const float* v, const float
   }
 }
 
+/* Attention alone (forward + backward of one causal multi-head attention over
+ * [S, H*D] f32 inputs), for the CPU baseline's per-part timing (bench.py). */
+int oc_attention(int S, int H, int D, const float* q, const float* k, const float* v,
+                 const float* dout, float* o, float* lse, float* dq, float* dk, float* dv) {
+  if (S <= 0 || H <= 0 || D <= 0 || D > 256) return 1;
+  attn_fwd(q, k, v, o, lse, S, H, D);
+  attn_bwd(q, k, v, o, lse, dout, dq, dk, dv, S, H, D);
+  return 0;
+}
+
 /* ------------------------------------------------------------ step */
 typedef struct {
   float *x, *xn, *rstd1, *q, *k, *v, *o, *lse, *a, *x1, *xn2, *rstd2, *gu, *act;

@@ -73,6 +73,21 @@ def step(cfg: OcCfg, params: np.ndarray, toks: np.ndarray, labels: np.ndarray):
     return loss.value, g
 
 
+def attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, dout: np.ndarray, H: int):
+    """Causal attention forward + backward of [S, H*D] f32 arrays on the CPU;
+    returns (o, lse, dq, dk, dv).  bench.py times it for the CPU baseline."""
+    q, k, v, dout = (np.ascontiguousarray(a, np.float32) for a in (q, k, v, dout))
+    S, h = q.shape
+    D = h // H
+    o, dq, dk, dv = (np.empty_like(q) for _ in range(4))
+    lse = np.empty((H, S), np.float32)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    rc = lib().oc_attention(S, H, D, ptr(q), ptr(k), ptr(v), ptr(dout), ptr(o), ptr(lse), ptr(dq), ptr(dk),
+                            ptr(dv))
+    assert rc == 0
+    return o, lse, dq, dk, dv
+
+
 def layout(cfg: OcCfg):
     """[(name, layer, offset, count)] in the shared parameter layout."""
     h, F, V = cfg.hidden, cfg.ffn, cfg.vocab

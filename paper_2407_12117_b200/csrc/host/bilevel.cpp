@@ -178,4 +178,28 @@ std::string plan_to_json(const ModelPlan& p) {
   return j.dump();
 }
 
+std::string parse_plan_json(const std::string& text, Bytes* total_peak,
+                            std::map<std::pair<std::size_t, TensorId>, Bytes>* absolute) {
+  nlohmann::json j;
+  try {
+    j = nlohmann::json::parse(text);
+  } catch (const nlohmann::json::exception& e) {
+    throw ConfigError(std::string("plan: invalid JSON: ") + e.what());
+  }
+  if (!j.is_object() || !j.contains("absolute") || !j.contains("total_peak") || !j["absolute"].is_array())
+    throw ConfigError("plan: not a GlobalPlan (needs 'absolute' and 'total_peak')");
+  try {
+    *total_peak = j["total_peak"].get<Bytes>();
+    absolute->clear();
+    for (const auto& a : j["absolute"]) {
+      const auto key = std::make_pair(a.at("segment").get<std::size_t>(), a.at("tensor").get<TensorId>());
+      if (!absolute->emplace(key, a.at("offset").get<Bytes>()).second)
+        throw ConfigError("plan: tensor " + std::to_string(key.second) + " placed twice");
+    }
+  } catch (const nlohmann::json::exception& e) {
+    throw ConfigError(std::string("plan: bad value: ") + e.what());
+  }
+  return j.dump();
+}
+
 }  // namespace memo

@@ -180,6 +180,10 @@ LayerLayout plan_one_layer(const Segment& fwd, const Segment& bwd, Bytes cap, Se
                            Bytes alignment);                                  // bilevel.hpp:66
 ModelPlan plan_iteration(const Trace& t, Bytes cap, Seconds budget, Bytes alignment);  // :189
 std::string plan_to_json(const ModelPlan& p);  // json_io.hpp:189 to_json(GlobalPlan).dump()
+// The placement of a to_json(GlobalPlan) text: total_peak and (segment, tensor)
+// -> absolute offset; returns the canonical dump.  ConfigError on bad input.
+std::string parse_plan_json(const std::string& text, Bytes* total_peak,
+                            std::map<std::pair<std::size_t, TensorId>, Bytes>* absolute);
 
 // ---------------------------------------------------------------- skeletal / alpha
 struct Skeletal {  // swap.hpp:67-89

@@ -240,6 +240,7 @@ extern "C" int memo_exec_get_info(memo_exec* ctx, memo_exec_info* info) {
     info->offload_bytes = st.offload_bytes;
     info->prefetch_bytes = st.prefetch_bytes;
     info->kernel_launches = st.kernel_launches;
+    info->copy_wait_ms = st.copy_wait_ms;
     for (int c = 0; c < 5; ++c) {
       info->op_ms[c] = st.op_ms[c];
       info->op_flops[c] = st.op_flops[c];
@@ -254,6 +255,13 @@ extern "C" int memo_exec_trace(memo_exec* ctx, char** text) {
 
 extern "C" int memo_exec_plan(memo_exec* ctx, char** json) {
   return guard([&] { *json = memo::dup_string(ctx->ex->plan_json()); });
+}
+
+extern "C" int memo_exec_bind_plan(memo_exec* ctx, const char* plan_json) {
+  return guard([&] {
+    if (!ctx || !plan_json) throw memo::ConfigError("memo_exec_bind_plan: null argument");
+    ctx->ex->bind_plan(plan_json);
+  });
 }
 
 extern "C" int memo_exec_tensor(memo_exec* ctx, const char* name, int32_t layer, void** ptr,

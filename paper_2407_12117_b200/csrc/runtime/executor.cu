@@ -251,7 +251,63 @@ void Executor::build_trace_and_plan() {
   for (const AbsAddr& a : mp.absolute) {
     const auto& nm = tb.names().at(a.id);
     arena_off_[{a.segment, nm.second}] = a.offset;
+    req_name_[{a.segment, a.id}] = nm.second;
   }
+}
+
+// Replay an externally computed plan (SURVEY §8b memo_bind_plan): the text is
+// to_json(GlobalPlan).dump() (json_io.hpp:189-202) of a plan of THIS executor's
+// trace, e.g. the reference's own actmem::plan_model(parse_trace(trace_text())).
+// Refused (status 2) unless it places exactly the executor's transient requests
+// (same (segment, tensor) set), at offsets that are multiples of the alignment, with
+// no two requests whose lifespans overlap (trace.hpp:146 lifespans over the
+// whole iteration) sharing bytes; status 3 if its total_peak exceeds the arena
+// reserved at creation (allocator.hpp:264-285: the plan never grows the
+// reservation).  On success every arena pointer of later steps follows the
+// bound offsets.  Must precede the first step (a captured graph bakes pointers).
+void Executor::bind_plan(const std::string& text) {
+  if (eager_done_ || graph_exec_) throw ConfigError("bind_plan: bind the plan before the first step");
+  Bytes peak = 0;
+  std::map<std::pair<std::size_t, TensorId>, Bytes> off;
+  std::string canonical = parse_plan_json(text, &peak, &off);
+  if (off.size() != req_name_.size())
+    throw ConfigError("bind_plan: plan places " + std::to_string(off.size()) + " tensors, the executor's trace has " +
+                      std::to_string(req_name_.size()) + " transient requests");
+  for (const auto& kv : off)
+    if (!req_name_.count(kv.first))
+      throw ConfigError("bind_plan: tensor " + std::to_string(kv.first.second) + " of segment " +
+                        std::to_string(kv.first.first) + " is not a transient request of this executor");
+  if (peak > arena_bytes_)
+    throw InfeasibleError("bind_plan: total_peak " + std::to_string(peak) + " exceeds the reserved arena " +
+                          std::to_string(arena_bytes_));
+  // lifespans over the whole iteration; every placed request checked
+  const Trace t = parse_trace_text(trace_text_);
+  std::vector<Lifespan> spans = lifespans_of(t.segs.data(), t.segs.size(), false);
+  std::map<TensorId, std::size_t> seg_of;
+  for (const auto& kv : req_name_) seg_of[kv.first.second] = kv.first.first;
+  struct Item {
+    Lifespan l;
+    Bytes lo, hi;
+  };
+  std::vector<Item> items;
+  const Bytes al = opt_.alignment ? opt_.alignment : 1;
+  for (const Lifespan& l : spans) {
+    auto it = seg_of.find(l.id);
+    if (it == seg_of.end()) continue;  // skeletal: rounding buffers, not the arena
+    const Bytes o = off.at({it->second, l.id});
+    const Bytes sz = (l.size + al - 1) / al * al;
+    if (o % al) throw ConfigError("bind_plan: offset of tensor " + std::to_string(l.id) + " not aligned");
+    if (o + sz > peak)
+      throw ConfigError("bind_plan: tensor " + std::to_string(l.id) + " ends past total_peak");
+    items.push_back({l, o, o + sz});
+  }
+  for (std::size_t a = 0; a < items.size(); ++a)
+    for (std::size_t b = a + 1; b < items.size() && items[b].l.first < items[a].l.last; ++b)
+      if (items[a].l.overlaps(items[b].l) && items[a].lo < items[b].hi && items[b].lo < items[a].hi)
+        throw ConfigError("bind_plan: tensors " + std::to_string(items[a].l.id) + " and " +
+                          std::to_string(items[b].l.id) + " are live together and share bytes");
+  for (const auto& kv : off) arena_off_[{kv.first.first, req_name_.at(kv.first)}] = kv.second;
+  plan_json_ = canonical;
 }
 
 // SP+TP request trace of one rank (same segment structure; every layer
@@ -598,6 +654,20 @@ cudaEvent_t Executor::take_event() {
   return ev_pool_[ev_used_++];
 }
 
+// A wait of the compute stream on a copy event INSIDE a layer (the layer_input
+// rows of the previous layer's offload, before the down projection writes the
+// next layer's input over them).  The measured timeline cannot see it (it sits
+// between a layer's begin/end marks), so it is bracketed by two timing events
+// on the compute stream; their distance is the stall, reported as copy_wait_ms
+// and added to the exposed swap time.
+void Executor::copy_wait(cudaEvent_t ev) {
+  cudaEvent_t a = take_event(), b = take_event();
+  ck(record_timing_event(a, cs_), "record");
+  ck(cudaStreamWaitEvent(cs_, ev, 0), "wait");
+  ck(record_timing_event(b, cs_), "record");
+  waits_.push_back({a, b});
+}
+
 void Executor::gemm(const GemmDesc& g) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (opt_.op_timing) {
@@ -831,7 +901,7 @@ void Executor::layer_fwd(int i) {
   // being offloaded from.  Only the layer_input rows must have left (they are
   // copied first); everything else of RB(i+1) is written by fwd(i+1), which F3
   // holds until offload(i-1) is complete.
-  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_x_[i - 1], 0));
+  if (i >= 1 && swaps(i - 1)) copy_wait(ev_off_x_[i - 1]);
   g = gd(S, h, F, ACT, F, 0, P("wd"), F, 0, GEMM_EPI_RESID, nullptr, 0);
   g.out_f32 = out; g.resid = x1; g.ld_f32 = h;
   gemm(g);
@@ -1154,7 +1224,7 @@ void Executor::layer_fwd_tp(int i) {
   // being offloaded from.  Only the layer_input rows must have left (they are
   // copied first); everything else of RB(i+1) is written by fwd(i+1), which F3
   // holds until offload(i-1) is complete.
-  if (i >= 1 && swaps(i - 1)) G(cudaStreamWaitEvent(cs_, ev_off_x_[i - 1], 0));
+  if (i >= 1 && swaps(i - 1)) copy_wait(ev_off_x_[i - 1]);
   G(resid_round(x1, d_red, nullptr, out, static_cast<long long>(shard), cs_));
   stats_.kernel_launches += 5;
   mark(0, static_cast<int>(Kind::LayerFwd), i, false);
@@ -1387,6 +1457,7 @@ void Executor::record_step() {
   const int n = d_.n;
   marks_.clear();
   ops_.clear();
+  waits_.clear();
   ev_used_ = 0;
   stats_.offload_bytes = stats_.prefetch_bytes = 0;
   stats_.kernel_launches = 0;
@@ -1470,6 +1541,12 @@ Timeline Executor::timeline() const {
     st.op_ms[c] = 0;
     st.op_flops[c] = 0;
     st.op_count[c] = 0;
+  }
+  st.copy_wait_ms = 0;
+  for (const auto& w : waits_) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, w.first, w.second), "elapsed");
+    st.copy_wait_ms += ms;
   }
   for (const OpMark& o : ops_) {
     float ms = 0;

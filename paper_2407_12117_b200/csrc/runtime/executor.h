@@ -66,6 +66,7 @@ struct StepStats {
   double op_ms[OP_NCLASS] = {0, 0, 0, 0, 0};
   double op_flops[OP_NCLASS] = {0, 0, 0, 0, 0};
   int op_count[OP_NCLASS] = {0, 0, 0, 0, 0};
+  double copy_wait_ms = 0;  // compute-stream stalls on in-layer copy waits (copy_wait)
 };
 
 class Executor {
@@ -87,6 +88,8 @@ class Executor {
 
   const std::string& trace_text() const { return trace_text_; }
   const std::string& plan_json() const { return plan_json_; }
+  // Replay an external to_json(GlobalPlan) of this executor's trace (validated).
+  void bind_plan(const std::string& plan_json);
   const ModelConfig& model() const { return cfg_; }
   const Dims& dims() const { return d_; }
   const SwapDecision& swap() const { return swap_; }
@@ -155,6 +158,8 @@ class Executor {
     double flops;
   };
   std::vector<OpMark> ops_;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> waits_;  // copy_wait brackets of the step
+  void copy_wait(cudaEvent_t ev);
 
   ModelConfig cfg_;
   HardwareConfig hw_;
@@ -168,6 +173,7 @@ class Executor {
   std::unique_ptr<Comm> comm_;
 
   std::string trace_text_, plan_json_;
+  std::map<std::pair<std::size_t, TensorId>, std::string> req_name_;  // planned (segment, tensor) -> slot
   std::map<std::pair<std::size_t, std::string>, Bytes> arena_off_;
   std::size_t seg_emb_fwd_ = 0, seg_cls_fwd_ = 0, seg_cls_bwd_ = 0, seg_emb_bwd_ = 0;
   std::vector<std::size_t> seg_fwd_, seg_bwd_;

@@ -37,7 +37,8 @@ class ExecInfoC(C.Structure):
         ("param_count", C.c_int64), ("swap_enabled", C.c_int32)] + [
         (n, C.c_double) for n in ("last_step_ms", "h2d_bytes", "d2h_bytes", "offload_bytes",
                                   "prefetch_bytes")] + [("kernel_launches", C.c_int32),
-        ("op_ms", C.c_double * 5), ("op_flops", C.c_double * 5), ("op_count", C.c_int32 * 5)]
+        ("op_ms", C.c_double * 5), ("op_flops", C.c_double * 5), ("op_count", C.c_int32 * 5),
+        ("copy_wait_ms", C.c_double)]
 
 
 lib.memo_comm_loopback_group.restype = C.c_void_p
@@ -179,6 +180,12 @@ class Executor:
         p = C.c_char_p()
         check(lib.memo_exec_plan(self._h, C.byref(p)))
         return take_string(p)
+
+    def bind_plan(self, plan_json: str) -> None:
+        """Replay an external to_json(GlobalPlan) of this executor's trace
+        (memo_exec_bind_plan): status 2 if it does not fit the trace, 3 if it
+        needs more than the reserved arena.  Before the first step."""
+        check(lib.memo_exec_bind_plan(self._h, plan_json.encode()))
 
     def tensor_ptr(self, name: str, layer: int = -1):
         ptr, n = C.c_void_p(), C.c_size_t()

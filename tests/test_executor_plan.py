@@ -151,3 +151,77 @@ def test_solo_rank_plan_equals_group_rank_plan_and_option_checks():
     with pytest.raises(MemoError) as e:
         Executor(cfg, HW, alpha=0.5, dry_run=1, tp=(KIND_SOLO, None, 0), cuda_graph=1)
     assert e.value.code == 2
+
+
+def _sizes_of_trace(trace: str):
+    sizes = {}
+    for line in trace.splitlines():
+        parts = line.split()
+        if len(parts) == 3 and parts[0] == "malloc":
+            sizes[int(parts[1])] = int(parts[2])
+    return sizes
+
+
+def mirror(plan_json: str, trace: str, alignment: int = 512) -> str:
+    """Another valid placement of the same trace: every tensor moved to
+    total_peak - offset - aligned size.  Disjointness is preserved, so it is a
+    legal plan with different addresses."""
+    j = json.loads(plan_json)
+    peak = j["total_peak"]
+    sizes = _sizes_of_trace(trace)
+    for a in j["absolute"]:
+        sz = -(-sizes[a["tensor"]] // alignment) * alignment
+        a["offset"] = peak - a["offset"] - sz
+    return json.dumps(j)
+
+
+def test_bind_plan_accepts_own_reference_and_mirrored_plans():
+    """memo_exec_bind_plan: the executor replays a GlobalPlan JSON
+    computed outside it -- its own, the reference planner's (oracle/_ref), and a
+    different valid placement (mirrored offsets) -- and refuses plans that do
+    not fit its trace."""
+    cfg, alpha = CONFIGS["cfg1p"]
+    ex = Executor(cfg, HW, alpha=alpha, dry_run=1)
+    trace, plan = ex.trace_text(), ex.plan_json()
+    ex.bind_plan(plan)
+    assert ex.plan_json() == plan
+    if os.path.exists(PROBE):
+        ex.bind_plan(_ref_plan(trace))
+        assert ex.plan_json() == plan
+    mp = mirror(plan, trace)
+    ex.bind_plan(mp)
+    assert ex.plan_json() == json.dumps(json.loads(mp), separators=(",", ":"))
+    assert ex.plan_json() != plan
+
+
+def test_bind_plan_refusals():
+    cfg, alpha = CONFIGS["cfg1p"]
+    ex = Executor(cfg, HW, alpha=alpha, dry_run=1)
+    trace, plan = ex.trace_text(), ex.plan_json()
+    j = json.loads(plan)
+
+    def code(pj):
+        with pytest.raises(MemoError) as e:
+            ex.bind_plan(json.dumps(pj) if not isinstance(pj, str) else pj)
+        return e.value.code
+
+    assert code("{not json") == 2
+    assert code({"total_peak": 0}) == 2
+    bad = json.loads(plan)
+    bad["absolute"] = bad["absolute"][1:]          # a request left unplaced
+    assert code(bad) == 2
+    bad = json.loads(plan)
+    bad["absolute"].append(dict(bad["absolute"][0], tensor=10 ** 9))   # not in the trace
+    assert code(bad) == 2
+    bad = json.loads(plan)
+    bad["total_peak"] = j["total_peak"] + 512      # more than the reserved arena
+    assert code(bad) == 3
+    bad = json.loads(plan)
+    bad["absolute"][0]["offset"] += 1              # misaligned
+    assert code(bad) == 2
+    # everything at offset 0: live-together tensors share bytes
+    bad = json.loads(plan)
+    for a in bad["absolute"]:
+        a["offset"] = 0
+    assert code(bad) == 2
+    ex.bind_plan(plan)                              # still bindable after refusals

@@ -242,3 +242,34 @@ def test_load_batch_rejects_out_of_range_ids():
                 ex.step(t.astype(toks.dtype), lab.astype(labels.dtype))
             assert e.value.code == _abi.MEMO_ERR_INPUT
         assert ex.step(toks, labels) == good
+
+
+def test_bound_external_plan_is_replayed():
+    """memo_exec_bind_plan: a different valid placement of the executor's trace
+    (every arena tensor mirrored inside total_peak) is replayed -- the step
+    computes on the new addresses, gives the default plan's loss and gradients
+    bit for bit, and device memory is unchanged across the steps."""
+    import json as _json
+
+    import torch
+    from tests.test_executor_plan import mirror
+    n, h, H, F, V, S = 4, 256, 2, 768, 512, 1024
+    cfg = model(n, h, H, F, V, S)
+    toks, labels = O.tokens(31, V, S)
+    out = {}
+    for bound in (False, True):
+        with Executor(cfg, HW, seed=2, alpha=0.5, optimizer=0, ce_chunk=512) as ex:
+            if bound:
+                mp = mirror(ex.plan_json(), ex.trace_text())
+                ex.bind_plan(mp)
+                assert _json.loads(ex.plan_json()) == _json.loads(mp)
+            loss = [ex.step(toks, labels)]
+            free0 = torch.cuda.mem_get_info()[0]  # after the first step (lazy module loading)
+            loss += [ex.step(toks, labels) for _ in range(2)]
+            assert torch.cuda.mem_get_info()[0] == free0
+            out[bound] = (loss, ex.read("grad/all"))
+            from paper_2407_12117_b200 import _abi
+            with pytest.raises(_abi.MemoError):
+                ex.bind_plan(ex.plan_json())  # after the first step: refused
+    assert out[False][0] == out[True][0]
+    assert np.array_equal(out[False][1], out[True][1])
