@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(256, 1)
 // each warp keeps its own partial row sum (combined once in the epilogue),
 // FFMA2/FADD2 process column pairs, and a quarter of the exponentials run on
 // the FMA pipe (exp2_fma) to keep MUFU below the MMA time.
+#ifdef MEMO_ATTN_ABLATIONS  // split-row forward layout (ablation build only)
 struct Fwd2wSmem {
   static constexpr int TILE_BYTES = 2 * CHUNK_BYTES;  // D = 128
   static constexpr int K_OFF = 0;
@@ -390,6 +391,8 @@ struct Fwd2wSmem {
   static constexpr int BAR_OFF = X_OFF + 2 * 2 * 128 * 4;
   static constexpr int BYTES = BAR_OFF + 256 + 1024;
 };
+#endif  // MEMO_ATTN_ABLATIONS
+
 
 __device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
   return (static_cast<uint64_t>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
@@ -449,6 +452,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+#ifdef MEMO_ATTN_ABLATIONS  // split-row forward (ablation build only)
 template <int EMU_EVERY>  // 0: all exps on MUFU; n: every n-th column pair on the FMA pipe
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_2w_kernel(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap map_k,
@@ -713,6 +717,7 @@ __global__ void __launch_bounds__(384, 1)
     dev::tmem_dealloc(tmem, 512);
   }
 }
+#endif  // MEMO_ATTN_ABLATIONS
 
 // ------------------------------------------------------------------ forward, ping-pong
 // Two adjacent query tiles (A = 2p, B = 2p+1) of one head per CTA, each with
@@ -1061,6 +1066,7 @@ __device__ __forceinline__ void store_grad32(__nv_bfloat16* dst, float (&x)[32],
   }
 }
 
+#ifdef MEMO_ATTN_ABLATIONS  // K/V-in-shared-memory dK/dV (ablation build only)
 template <int D>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap map_q,
@@ -1271,6 +1277,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     dev::tmem_dealloc(tmem, 512);
   }
 }
+#endif  // MEMO_ATTN_ABLATIONS
 
 // Optional stall accounting of the dK/dV kernel (build with -DMEMO_DKDV_PROF):
 // [0] MMA warp waiting for Q/dO tiles, [1] MMA warp waiting for P/dS (compute),
@@ -1641,7 +1648,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                        const __grid_constant__ CUtensorMap map_v, const float* __restrict__ lse2,
                        const float* __restrict__ delta, __nv_bfloat16* __restrict__ dq, long long ld,
                        const float2* __restrict__ rope, long long pos0, int S, int H, float scale,
-                       float scale_log2, int dbg) {
+                       float scale_log2) {
   using L = BwdSmem<D>;
   constexpr int NC = L::NC;
   // With Q/dO in TMEM the A0/A1 region joins the K/V ring as a third stage.
@@ -1727,7 +1734,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         const uint64_t kd = kmajor_base(dev::smem_u32(smem + k_off(st)) + half * HALF_BYTES);
         const uint64_t vd = kmajor_base(dev::smem_u32(smem + v_off(st)) + half * HALF_BYTES);
-        if (!(dbg & 2)) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           if (AT)
@@ -1743,7 +1749,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
             dev::mma_bf16_ss_w(tmem + b * 128 + 64, kmajor_step(doa0, kk), kmajor_step(vd, kk), idesc_s,
                              kk > 0);
         }
-        }
         dev::mma_commit_w(&s_full[b]);
       };
       issue_s(0);
@@ -1753,12 +1758,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         dev::mbar_wait_w(&ds_ready[b], (g >> 1) & 1);
         dev::tc_fence_after();
         const uint64_t km = mnmajor_base(dev::smem_u32(smem + k_off(st)) + half * HALF_BYTES);
-        if (!(dbg & 4)) {
 #pragma unroll
         for (int kk = 0; kk < HALF / 16; ++kk)
           dev::mma_bf16_ts_w(t_dq, tmem + b * 128 + 32 * (kk >> 1) + 8 * (kk & 1), mnmajor_step(km, kk),
                              idesc_g, (g | kk) != 0);
-        }
         if (half == 1) dev::mma_commit_w(&kv_empty[st]);
       }
       dev::mma_commit_w(fin);
@@ -1811,12 +1814,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           dev::tmem_st16(t_s + c * 32, dd);  // inside this warp's own slice
         }
       };
-      if (!(dbg & 1)) {
-        if (diag)
-          body(std::true_type{});
-        else
-          body(std::false_type{});
-      }
+      if (diag)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
       dev::tmem_st_wait();
       dev::tc_fence_before();
       dev::mbar_arrive(&ds_ready[b]);
@@ -1844,6 +1845,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
 }
 
+#ifdef MEMO_ATTN_ABLATIONS  // fused 5-unit backward (ablation build only)
 // ------------------------------------------------------------ fused backward
 // One CTA per (key tile kt, head): S^T, dP^T, dV += P^T dO, dK += dS^T Q and
 // dQ^T_partial = K^T dS^T for every 64-query half of the query tiles kt..n-1,
@@ -1891,7 +1893,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                           uint32_t* __restrict__ counters, uint32_t* __restrict__ ticket,
                           __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, long long ld,
                           const float2* __restrict__ rope, long long pos0, int S, int H, float scale,
-                          float scale_log2, int G, int dbg) {
+                          float scale_log2, int G) {
   static_assert(D == 128, "fused backward needs M = D = 128 for the dQ^T MMA");
   using L = FusedBwdSmem<D>;
   constexpr int NC = L::NC;
@@ -2069,17 +2071,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const int b = g & 1;
         const int ck = chunk_of(g);
         dev::mbar_wait(&staged[b], (g >> 1) & 1);
-        if (kt > 0 && !(dbg & 1)) {
+        if (kt > 0) {
           while (dev::ld_acquire_u32(ctr0 + ck) != static_cast<uint32_t>(kt)) __nanosleep(32);
         }
         dev::fence_proxy_async_global();
         const uint32_t stg = stg0 + (g % FB_NSTG) * L::STG_BYTES;
-        if (!(dbg & 2)) {
-          if (kt == 0)
-            dev::bulk_store(acc0 + static_cast<long long>(ck) * HALF * D, stg, L::STG_BYTES);
-          else
-            dev::bulk_reduce_add_f32(acc0 + static_cast<long long>(ck) * HALF * D, stg, L::STG_BYTES);
-        }
+        if (kt == 0)
+          dev::bulk_store(acc0 + static_cast<long long>(ck) * HALF * D, stg, L::STG_BYTES);
+        else
+          dev::bulk_reduce_add_f32(acc0 + static_cast<long long>(ck) * HALF * D, stg, L::STG_BYTES);
         dev::bulk_commit();
         dev::bulk_wait_read<0>();
         dev::mbar_arrive(&stg_free[b]);
@@ -2243,48 +2243,20 @@ __global__ void attn_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloa
     *reinterpret_cast<uint4*>(dq + t * ld + col) = o;
   }
 }
+#endif  // MEMO_ATTN_ABLATIONS
 
-int attn_debug() {
-  static const int v = [] {
-    const char* e = getenv("MEMO_ATTN_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
+#ifdef MEMO_ATTN_ABLATIONS
+// Ablation build only (make -C csrc ablations -> _lib_ablations/libmemo.so,
+// selected by tools through MEMO_LIB_PATH): environment-selected variants whose
+// measurements DESIGN §4 and profiles/README.md record.  The product library
+// contains none of these kernels and reads no environment variable here.
+int abl_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
-
-// MEMO_ATTN_BWD=fused selects the fused kernel (ablation; the split dK/dV +
-// dQ kernels measured faster at S=128K: 478 vs 498 ms, H=32, D=128).
-int dkdv_wpq() {  // MEMO_ATTN_DKDV_WPQ: softmax-gradient warps per lane quarter (2 or 4)
-  static const int v = [] {
-    const char* e = getenv("MEMO_ATTN_DKDV_WPQ");
-    return e && atoi(e) == 4 ? 4 : 2;
-  }();
-  return v;
-}
-
-bool dkdv_split() {  // MEMO_ATTN_DKDV_SPLIT=1: P^T and dS^T behind separate barriers
-  static const bool v = [] {
-    const char* e = getenv("MEMO_ATTN_DKDV_SPLIT");
-    return e && atoi(e) == 1;
-  }();
-  return v;
-}
-
-int dkdv_emu() {  // MEMO_ATTN_DKDV_EMU: every n-th column pair's exps on the FMA pipe (0, 2, 4)
-  static const int v = [] {
-    const char* e = getenv("MEMO_ATTN_DKDV_EMU");
-    const int x = e ? atoi(e) : 0;
-    return x == 2 || x == 4 ? x : 0;
-  }();
-  return v;
-}
-
 bool bwd_fused() {
-  static const bool v = [] {
-    const char* e = getenv("MEMO_ATTN_BWD");
-    return e && std::string(e) == "fused";
-  }();
-  return v;
+  const char* e = getenv("MEMO_ATTN_BWD");
+  return e && std::string(e) == "fused";
 }
 
 cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
@@ -2304,16 +2276,9 @@ cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
     cudaFuncSetAttribute(attn_bwd_fused_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
     cudaFuncSetAttribute(attn_bwd_fused_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
   });
-  static const int pend = [] {
-    const char* e = getenv("MEMO_FB_PEND");
-    return e ? atoi(e) : 0;
-  }();
-  static const int g_env = [] {
-    const char* e = getenv("MEMO_FB_GROUP");
-    return e ? atoi(e) : 0;
-  }();
+  const int pend = abl_env("MEMO_FB_PEND", 0);
   // heads per ticket group: the accumulator of a group should stay L2-resident
-  int G = g_env;
+  int G = abl_env("MEMO_FB_GROUP", 0);
   if (G <= 0) G = 4;
   while (G > 1 && a.H % G != 0) --G;
   const long long HS = static_cast<long long>(a.H) * a.S;
@@ -2334,7 +2299,7 @@ cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
                          : attn_bwd_fused_kernel<D, 0>;
   kern<<<(a.S / TILE) * a.H, BWD_THREADS, L::BYTES, stream>>>(
       mq, mk, mv, mdo, lse2, delta, acc, counters, ticket, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S,
-      a.H, a.softmax_scale, a.softmax_scale * kLog2e, G, attn_debug());
+      a.H, a.softmax_scale, a.softmax_scale * kLog2e, G);
   if (a.ev[2]) record_timing_event(a.ev[2], stream);
   const long long n8 = HS * D / 8;
   const int blocks = static_cast<int>(std::min<long long>((n8 + 255) / 256, 148LL * 16));
@@ -2343,7 +2308,11 @@ cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
   if (a.ev[3]) record_timing_event(a.ev[3], stream);
   return cudaGetLastError();
 }
+#endif  // MEMO_ATTN_ABLATIONS
 
+// Deterministic split backward: prep (delta, log2 LSE), dK/dV (K/V resident in
+// TMEM, one CTA per key tile) and dQ (Q/dO resident in TMEM, one CTA per query
+// tile); no atomics, so every output is bitwise repeatable.
 template <int D>
 cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   const int h = a.H * a.D;
@@ -2355,10 +2324,13 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   static std::once_flag f;
   std::call_once(f, [] {
-    cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         BwdSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         BwdSmem<D>::BYTES);
+#ifdef MEMO_ATTN_ABLATIONS
+    cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         BwdSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2367,10 +2339,9 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
-    cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         BwdSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
+#endif
   });
   float* delta = a.delta;
   float* lse2 = a.delta + static_cast<long long>(a.H) * a.S;
@@ -2382,51 +2353,54 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   dim3 grid(a.S / TILE, a.H);
   if (a.ev[1]) record_timing_event(a.ev[1], stream);
-  static const bool dkdv_smem = [] {  // MEMO_ATTN_DKDV=smem: K/V as shared-memory operands (ablation)
-    const char* e = getenv("MEMO_ATTN_DKDV");
-    return e && std::string(e) == "smem";
-  }();
-  if (dkdv_smem)
-    attn_bwd_dkdv_kernel<D><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
-        mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale,
-        scale_log2);
-  else if (dkdv_wpq() == 4)
-    attn_bwd_dkdv_tm_kernel<D, 4><<<grid, 32 * (4 + 16), DkdvTmSmem<D>::BYTES, stream>>>(
-        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
-        scale_log2);
-  else if (dkdv_split())
-    attn_bwd_dkdv_tm_kernel<D, 2, 0, true><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
-        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
-        scale_log2);
-  else if (dkdv_emu() == 2)
-    attn_bwd_dkdv_tm_kernel<D, 2, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
-        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
-        scale_log2);
-  else if (dkdv_emu() == 4)
-    attn_bwd_dkdv_tm_kernel<D, 2, 4><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
-        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
-        scale_log2);
-  else
-    attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
-        a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
-        scale_log2);
+#ifdef MEMO_ATTN_ABLATIONS
+  // MEMO_ATTN_DKDV_VARIANT: 1 K/V in shared memory, 2 four warps per lane
+  // quarter, 3 P^T/dS^T behind separate barriers, 4/5 every 2nd/4th column
+  // pair's exponentials on the FMA pipe
+  switch (abl_env("MEMO_ATTN_DKDV_VARIANT", 0)) {
+    case 1:
+      attn_bwd_dkdv_kernel<D><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
+          mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale, scale_log2);
+      break;
+    case 2:
+      attn_bwd_dkdv_tm_kernel<D, 4><<<grid, 32 * (4 + 16), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
+    case 3:
+      attn_bwd_dkdv_tm_kernel<D, 2, 0, true><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
+    case 4:
+      attn_bwd_dkdv_tm_kernel<D, 2, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
+    case 5:
+      attn_bwd_dkdv_tm_kernel<D, 2, 4><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
+    default:
+#endif
+      attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+#ifdef MEMO_ATTN_ABLATIONS
+  }
+#endif
   if (a.ev[2]) record_timing_event(a.ev[2], stream);
-  static const int dbg = [] {
-    const char* e = getenv("MEMO_ATTN_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  static const bool dq_at = [] {
-    const char* e = getenv("MEMO_ATTN_DQ_TMEM_A");
-    return e ? atoi(e) != 0 : true;
-  }();
-  if (dq_at)
-    attn_bwd_dq_kernel<D, true><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
-        a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
-        a.softmax_scale, scale_log2, dbg);
-  else
+#ifdef MEMO_ATTN_ABLATIONS
+  if (abl_env("MEMO_ATTN_DQ_TMEM_A", 1) == 0)  // Q/dO as shared-memory operands
     attn_bwd_dq_kernel<D, false><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
         a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
-        a.softmax_scale, scale_log2, dbg);
+        a.softmax_scale, scale_log2);
+  else
+#endif
+    attn_bwd_dq_kernel<D, true><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
+        a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
+        a.softmax_scale, scale_log2);
   if (a.ev[3]) record_timing_event(a.ev[3], stream);
   return cudaGetLastError();
 }
@@ -2447,14 +2421,6 @@ void launch_fwd(const AttnFwdArgs& a, const CUtensorMap& mq, const CUtensorMap& 
                                                                a.H, scale_log2);
 }
 
-int fwd_variant() {
-  static int v = [] {
-    const char* e = getenv("MEMO_ATTN_FWD_VARIANT");
-    return e ? atoi(e) : 8;
-  }();
-  return v;
-}
-
 cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   if (a.S % TILE != 0 || (a.D != 64 && a.D != 128)) return cudaErrorInvalidValue;
   const int h = a.H * a.D;
@@ -2465,45 +2431,55 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   const float scale_log2 = a.softmax_scale * kLog2e;
   if (a.ev[0]) record_timing_event(a.ev[0], stream);
-  // 0-3: one softmax warp per row (bit0 Q in TMEM, bit1 FMA exp2 share); 5-7: split rows;
-  // 8-10: ping-pong two Q tiles (default 8)
-  const int v = fwd_variant();
-  if (v >= 8 && a.D == 128 && a.S % (2 * TILE) == 0) {  // ping-pong (two Q tiles, setmaxnreg)
-    // FMA-pipe exp2 share (paired exp2_fma2): 8 -> 1/3 (default), 9 -> none, 10 -> 1/8,
-    // 11 -> 1/4, 12 -> 1/2
+#ifdef MEMO_ATTN_ABLATIONS
+  // MEMO_ATTN_FWD_VARIANT: 0-3 one softmax warp per row (bit0 Q in TMEM, bit1
+  // FMA exp2 share); 5-7 split rows (1/4, none, 1/8 FMA share); 8-12 ping-pong
+  // with FMA share 1/3 (product), none, 1/8, 1/4, 1/2
+  const int v = abl_env("MEMO_ATTN_FWD_VARIANT", 8);
+  if (v != 8) {
+    if (v >= 9 && a.D == 128 && a.S % (2 * TILE) == 0) {
+      static std::once_flag fa;
+      std::call_once(fa, [] {
+        for (auto k : {attn_fwd_pp_kernel<0>, attn_fwd_pp_kernel<8>, attn_fwd_pp_kernel<4>, attn_fwd_pp_kernel<2>})
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+      });
+      auto kern = v == 9 ? attn_fwd_pp_kernel<0> : v == 10 ? attn_fwd_pp_kernel<8>
+                : v == 11 ? attn_fwd_pp_kernel<4> : attn_fwd_pp_kernel<2>;
+      kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
+                                                                          scale_log2);
+    } else if ((v == 5 || v == 6 || v == 7) && a.D == 128) {
+      static std::once_flag fb;
+      std::call_once(fb, [] {
+        for (auto k : {attn_fwd_2w_kernel<4>, attn_fwd_2w_kernel<8>, attn_fwd_2w_kernel<0>})
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
+      });
+      auto kern = v == 5 ? attn_fwd_2w_kernel<4> : v == 7 ? attn_fwd_2w_kernel<8> : attn_fwd_2w_kernel<0>;
+      kern<<<dim3(a.S / TILE, a.H), 384, Fwd2wSmem::BYTES, stream>>>(a.q, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
+    } else if (a.D == 128) {
+      switch (v) {
+        case 0: launch_fwd<128, false, false>(a, mq, mk, mv, scale_log2, stream); break;
+        case 1: launch_fwd<128, true, false>(a, mq, mk, mv, scale_log2, stream); break;
+        case 2: launch_fwd<128, false, true>(a, mq, mk, mv, scale_log2, stream); break;
+        default: launch_fwd<128, true, true>(a, mq, mk, mv, scale_log2, stream); break;
+      }
+    } else {
+      launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
+    }
+    if (a.ev[1]) record_timing_event(a.ev[1], stream);
+    return cudaGetLastError();
+  }
+#endif
+  if (a.D == 128 && a.S % (2 * TILE) == 0) {
+    // ping-pong: two query tiles per CTA, setmaxnreg, 1/3 of the exponentials
+    // on the FMA pipe (paired exp2_fma2)
     static std::once_flag f8;
     std::call_once(f8, [] {
-      cudaFuncSetAttribute(attn_fwd_pp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
-      cudaFuncSetAttribute(attn_fwd_pp_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
-      cudaFuncSetAttribute(attn_fwd_pp_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
       cudaFuncSetAttribute(attn_fwd_pp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
-      cudaFuncSetAttribute(attn_fwd_pp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
     });
-    auto kern = v == 9    ? attn_fwd_pp_kernel<0>
-                : v == 10 ? attn_fwd_pp_kernel<8>
-                : v == 11 ? attn_fwd_pp_kernel<4>
-                : v == 12 ? attn_fwd_pp_kernel<2>
-                          : attn_fwd_pp_kernel<3>;
-    kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
-                                                                        scale_log2);
-  } else if (v >= 5 && a.D != 128) {
-    launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
-  } else if (v == 5 || v == 6 || v == 7) {  // FMA-pipe exp2 share: 5 -> 1/4, 7 -> 1/8, 6 -> none
-    static std::once_flag f5;
-    std::call_once(f5, [] {
-      cudaFuncSetAttribute(attn_fwd_2w_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
-      cudaFuncSetAttribute(attn_fwd_2w_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
-      cudaFuncSetAttribute(attn_fwd_2w_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2wSmem::BYTES);
-    });
-    auto kern = v == 5 ? attn_fwd_2w_kernel<4> : v == 7 ? attn_fwd_2w_kernel<8> : attn_fwd_2w_kernel<0>;
-    kern<<<dim3(a.S / TILE, a.H), 384, Fwd2wSmem::BYTES, stream>>>(a.q, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
-  } else if (a.D == 128) {
-    switch (v) {
-      case 0: launch_fwd<128, false, false>(a, mq, mk, mv, scale_log2, stream); break;
-      case 1: launch_fwd<128, true, false>(a, mq, mk, mv, scale_log2, stream); break;
-      case 2: launch_fwd<128, false, true>(a, mq, mk, mv, scale_log2, stream); break;
-      default: launch_fwd<128, true, true>(a, mq, mk, mv, scale_log2, stream); break;
-    }
+    attn_fwd_pp_kernel<3><<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse,
+                                                                                        a.S, a.H, scale_log2);
+  } else if (a.D == 128) {  // an odd number of query tiles: one tile per CTA
+    launch_fwd<128, true, true>(a, mq, mk, mv, scale_log2, stream);
   } else {
     launch_fwd<64, true, true>(a, mq, mk, mv, scale_log2, stream);
   }
@@ -2517,14 +2493,18 @@ namespace memo {
 size_t attn_bwd_workspace_bytes(int S, int H, int D) {
   const size_t HS = static_cast<size_t>(H) * S;
   size_t b = 2 * HS * sizeof(float);  // delta, lse2
+#ifdef MEMO_ATTN_ABLATIONS
   if (D == 128 && bwd_fused())  // f32 dQ accumulator, ordering counters, ticket
     b += HS * D * sizeof(float) + (HS / HALF + 4) * sizeof(uint32_t);
+#endif
   return b;
 }
 
 cudaError_t attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   if (a.S % TILE != 0) return cudaErrorInvalidValue;
+#ifdef MEMO_ATTN_ABLATIONS
   if (a.D == 128 && bwd_fused()) return launch_bwd_fused(a, stream);
+#endif
   if (a.D == 128) return launch_bwd<128>(a, stream);
   if (a.D == 64) return launch_bwd<64>(a, stream);
   return cudaErrorInvalidValue;

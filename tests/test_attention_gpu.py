@@ -169,14 +169,18 @@ print("fused ok")
 """
 
 
+ABLATION_LIB = os.path.join(ROOT, "paper_2407_12117_b200", "_lib_ablations", "libmemo.so")
+
+
+@pytest.mark.skipif(not os.path.exists(ABLATION_LIB), reason="ablation library not built")
 def test_attn_bwd_fused_ablation():
-    """MEMO_ATTN_BWD=fused: one kernel for dK/dV/dQ with dQ partials reduced
+    """The fused 5-unit backward of the ABLATION library (MEMO_ATTN_BWD=fused,
+    make -C csrc ablations): one kernel for dK/dV/dQ with dQ partials reduced
     at L2 in ticket order -- same parity bar and bitwise repeatable."""
-    import os
     import subprocess
     import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MEMO_ATTN_BWD="fused")
+    root = ROOT
+    env = dict(os.environ, MEMO_ATTN_BWD="fused", MEMO_LIB_PATH=ABLATION_LIB)
     out = subprocess.run([sys.executable, "-c", _FUSED_SCRIPT.format(root=root)], env=env,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "fused ok" in out.stdout, out.stdout + out.stderr

@@ -82,26 +82,21 @@ def bench(S, H, D, iters=5, bwd=False):
 if __name__ == "__main__":
     for S in [int(x) for x in (sys.argv[1:] or ["8192", "32768"])]:
         print(json.dumps(bench(S, 32, 128, bwd=True)), flush=True)
+    # variant sweeps run on the ablation library (make -C paper_2407_12117_b200/csrc ablations)
+    abl = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2407_12117_b200",
+                       "_lib_ablations", "libmemo.so")
     if os.environ.get("MEMO_FWD_SWEEP"):
         import subprocess
         for v in range(4):
-            env = dict(os.environ, MEMO_ATTN_FWD_VARIANT=str(v))
+            env = dict(os.environ, MEMO_ATTN_FWD_VARIANT=str(v), MEMO_LIB_PATH=abl)
             env.pop("MEMO_FWD_SWEEP")
             out = subprocess.check_output([sys.executable, __file__, sys.argv[-1]], env=env, text=True)
             r = json.loads(out.strip().splitlines()[0])
             print(json.dumps({"variant": v, "S": r["S"], "fwd_tflops": r["fwd_tflops"]}), flush=True)
-    if os.environ.get("MEMO_DBG_SWEEP"):
-        import subprocess
-        for v in [0, 1, 2, 4, 3, 5, 6, 7]:
-            env = dict(os.environ, MEMO_ATTN_DEBUG=str(v))
-            env.pop("MEMO_DBG_SWEEP")
-            out = subprocess.check_output([sys.executable, __file__, sys.argv[-1]], env=env, text=True)
-            r = json.loads(out.strip().splitlines()[0])
-            print(json.dumps({"dbg": v, "S": r["S"], "dq_ms": r["dq_ms"], "dkdv_ms": r["dkdv_ms"]}), flush=True)
     if os.environ.get("MEMO_DQ_SWEEP"):
         import subprocess
         for v in range(2):
-            env = dict(os.environ, MEMO_ATTN_DQ_TMEM_A=str(v))
+            env = dict(os.environ, MEMO_ATTN_DQ_TMEM_A=str(v), MEMO_LIB_PATH=abl)
             env.pop("MEMO_DQ_SWEEP")
             out = subprocess.check_output([sys.executable, __file__, sys.argv[-1]], env=env, text=True)
             r = json.loads(out.strip().splitlines()[0])

@@ -27,6 +27,9 @@ def run(M, N, K, layout, iters=10):
     args.b, args.ldb, args.b_mn_major = B.data_ptr(), ldb, bmn
     args.epilogue = 0 if layout != "wgrad" else 1
     args.c, args.ldc = out.data_ptr(), N
+    # GEMM_VARIANT (this tool's switch): 0 product choice, 1 single CTA, 2 B-multicast
+    # cluster, 3 2x2 cluster, 4 CTA pair (memo_gemm_args.variant)
+    args.variant = int(os.environ.get("GEMM_VARIANT", "0"))
     for _ in range(3):
         _abi.check(_abi.lib.memo_gemm(C.byref(args), None))
     torch.cuda.synchronize()

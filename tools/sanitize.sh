@@ -17,6 +17,9 @@ for tool in memcheck synccheck racecheck; do
       python tools/stress_attn.py 512 2 64 2 > $OUT/attn64_$tool.txt 2>&1
   echo "attn D=64 $tool rc=$?" | tee -a $OUT/summary.txt
   timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 \
+      python tools/gemm_variants_probe.py > $OUT/gemm_variants_$tool.txt 2>&1
+  echo "GEMM variants (single, B-multicast cluster, 2x2 cluster, CTA pair) $tool rc=$?" | tee -a $OUT/summary.txt
+  timeout 900 $CS --tool $tool --print-limit 20 --error-exitcode 9 \
       python tools/tp_peer_smoke.py 3 2 > $OUT/tp2_peer_$tool.txt 2>&1
   echo "SP+TP t=2 peer-memory step $tool rc=$?" | tee -a $OUT/summary.txt
 done
