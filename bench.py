@@ -508,6 +508,7 @@ def main():
     sim = P.simulate(tl, cfg, hw, p_total)
     flops = P.estimate_flops_per_sample(cfg, p_total)
     n_rec = sum(e.kind == "recompute" for e in tl)
+    rec_s = sum(e.end - e.start for e in tl if e.kind == "recompute")
     f_int = inter  # SwiGLU width
     recompute_flops = n_rec * 2.0 * info0["split"][1] * (4.0 * h * h + 2.0 * h * f_int)  # whole job
     mfu = seqs * flops / (t_max * 1e-3) / (world * B200_SPEC_BF16)
@@ -564,7 +565,11 @@ def main():
                                        if sim["iteration_time"] else None),
                  "in_layer_copy_wait_s": info["copy_wait_ms"] * 1e-3,
                  "no_swap_ms_per_step": nosw_ms,
-                 "exposed_swap_delta_s": (t_max - nosw_ms) * 1e-3 if nosw_ms else None,
+                 # T(swap) - T(swap disabled): recompute (MEMO's price for the swapped
+                 # tokens' skeletal activations) + any exposed copy time
+                 "swap_vs_no_swap_delta_s": (t_max - nosw_ms) * 1e-3 if nosw_ms else None,
+                 "recompute_s": rec_s,
+                 "exposed_swap_delta_s": (t_max - nosw_ms) * 1e-3 - rec_s if nosw_ms else None,
                  "hbm_free_before_timed_steps": free_before, "hbm_free_after_timed_steps": free_after,
                  "hbm_unchanged_over_timed_steps": free_before == free_after,
                  "forward_blocked_s": sim["forward_blocked"],

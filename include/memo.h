@@ -295,8 +295,8 @@ int memo_exec_plan(memo_exec* ctx, char** json);
  * 189-202) of a plan of memo_exec_trace()'s trace, e.g. from the reference's
  * actmem::plan_model.  Status 2 if it does not place exactly this trace's
  * transient requests or places two live-together requests on shared bytes;
- * 3 if its total_peak exceeds the arena reserved at creation.  Call before
- * the first step. */
+ * 3 if its total_peak exceeds the arena reserved at creation, or the step
+ * has already been captured as a CUDA graph (status 2). */
 int memo_exec_bind_plan(memo_exec* ctx, const char* plan_json);
 /* Device pointer of a named tensor: "<param>", "grad/<param>", "master/<param>"
  * with param in {embedding, g1, wqkv, wo, g2, wgu, wd, gf, wcls, all}

@@ -758,9 +758,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_full = bars + 5;   // [2]
   uint64_t* v_empty = bars + 7;  // [2]
   uint64_t* s_full = bars + 9;   // [2] per group
-  uint64_t* p_full = bars + 11;  // [2] per group
-  uint64_t* o_done = bars + 13;  // [2] per group
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* p_full = bars + 11;  // [2 groups][2 key halves]: P of keys [0,64) / [64,128) written
+  uint64_t* o_done = bars + 15;  // [2] per group
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int n_pairs = S / (2 * TILE);
   const int pp = n_pairs - 1 - static_cast<int>(blockIdx.x);  // heavy pairs first
@@ -781,7 +781,8 @@ __global__ void __launch_bounds__(384, 1)
       dev::mbar_init(&v_full[s2], 1);
       dev::mbar_init(&v_empty[s2], 1);
       dev::mbar_init(&s_full[s2], 1);
-      dev::mbar_init(&p_full[s2], 128);
+      dev::mbar_init(&p_full[2 * s2], 128);
+      dev::mbar_init(&p_full[2 * s2 + 1], 128);
       dev::mbar_init(&o_done[s2], 1);
     }
     dev::fence_barrier_init();
@@ -838,18 +839,24 @@ __global__ void __launch_bounds__(384, 1)
         dev::mma_commit_w(&s_full[g]);
         if (g == 1) dev::mma_commit_w(&k_empty[st]);  // B is the last reader of K_j
       };
-      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j
+      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j, one key half at a time
         const int st = j & 1;
-        dev::mbar_wait_w(&p_full[g], j & 1);
+        dev::mbar_wait_w(&p_full[2 * g], j & 1);
         if (g == 0 || j == nA) {
           dev::mbar_wait_w(&v_full[st], (j >> 1) & 1);
         }
         dev::tc_fence_after();
         const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk)
+        for (int kk = 0; kk < TILE / 32; ++kk)
           dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
                              (j | kk) != 0);
+        // keys [64,128): their P lands while the first half's MMAs run
+        dev::mbar_wait_w(&p_full[2 * g + 1], j & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int kk = TILE / 32; kk < TILE / 16; ++kk)
+          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o, true);
         // S_g(j+1) is issued after PV_g(j), so s_full already orders the
         // softmax's O rescale after PV_g(j); o_done only serves the epilogue.
         if (j == (g ? n_kv - 1 : nA - 1)) dev::mma_commit_w(&o_done[g]);
@@ -916,23 +923,51 @@ __global__ void __launch_bounds__(384, 1)
           factor = j == 0 ? 0.f : dev::ex2(m - m_new);
         }
         uint64_t sum4[4] = {0, 0, 0, 0};
+        // P in two key halves: the first half's P (keys [0,64)) is stored and
+        // released before the second half's exponentials, so the tensor pipe
+        // runs PV over the first half while the second is still computed.
+        auto exps = [&](int i0) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
-                                            __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
-                                    scale_log2, -m_new);
-          float a, b;
-          if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
-            const uint64_t e2 = exp2_fma2(x2);
-            a = f2_lo(e2);
-            b = f2_hi(e2);
-          } else {
-            a = dev::ex2(f2_lo(x2));
-            b = dev::ex2(f2_hi(x2));
+          for (int i = i0; i < i0 + 32; ++i) {
+            const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                              __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
+                                      scale_log2, -m_new);
+            float a, b;
+            if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
+              const uint64_t e2 = exp2_fma2(x2);
+              a = f2_lo(e2);
+              b = f2_hi(e2);
+            } else {
+              a = dev::ex2(f2_lo(x2));
+              b = dev::ex2(f2_hi(x2));
+            }
+            sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
+            p[i] = dev::pack_bf16(a, b);
           }
-          sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
-          p[i] = dev::pack_bf16(a, b);
+        };
+        exps(0);
+        dev::tmem_st32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&p[0]));
+        if (any && j > 0) {
+          // O_g holds P(j-1)V(j-1) (PV_g(j-1) completed before s_full_g(j)
+          // fired); rescaled before PV_g(j) may start, i.e. before half 0 is released
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            dev::tmem_ld32(t_o + c * 32, o);
+            dev::tmem_ld_wait_regs(o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+            dev::tmem_st32(t_o + c * 32, o);
+          }
         }
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&p_full[2 * g]);
+        exps(32);
+        dev::tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&p[32]));
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&p_full[2 * g + 1]);
         const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
         l = l * factor + (f2_lo(s01) + f2_hi(s01));
         m = m_new;
@@ -941,27 +976,6 @@ __global__ void __launch_bounds__(384, 1)
         tile(std::true_type{});
       else
         tile(std::false_type{});
-      {
-        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&p[0]);
-        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&p[32]);
-        dev::tmem_st32(t_s, p0);
-        dev::tmem_st32(t_s + 32, p1);
-      }
-      if (any && j > 0) {
-        // O_g holds P(j-1)V(j-1): PV_g(j-1) completed before s_full_g(j) fired
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          dev::tmem_ld32(t_o + c * 32, o);
-          dev::tmem_ld_wait_regs(o);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
-          dev::tmem_st32(t_o + c * 32, o);
-        }
-      }
-      dev::tmem_st_wait();
-      dev::tc_fence_before();
-      dev::mbar_arrive(&p_full[g]);
     }
     dev::mbar_wait(&o_done[g], 0);  // committed once, after the group's last PV
     dev::tc_fence_after();

@@ -264,9 +264,11 @@ void Executor::build_trace_and_plan() {
 // whole iteration) sharing bytes; status 3 if its total_peak exceeds the arena
 // reserved at creation (allocator.hpp:264-285: the plan never grows the
 // reservation).  On success every arena pointer of later steps follows the
-// bound offsets.  Must precede the first step (a captured graph bakes pointers).
+// bound offsets.  Refused once the step has been captured as a CUDA graph
+// (cuda_graph=1 captures the second step; the graph bakes the pointers).
 void Executor::bind_plan(const std::string& text) {
-  if (eager_done_ || graph_exec_) throw ConfigError("bind_plan: bind the plan before the first step");
+  if (graph_exec_ || capturing_)
+    throw ConfigError("bind_plan: the step is already captured as a CUDA graph (its pointers are baked)");
   Bytes peak = 0;
   std::map<std::pair<std::size_t, TensorId>, Bytes> off;
   std::string canonical = parse_plan_json(text, &peak, &off);

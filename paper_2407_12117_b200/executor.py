@@ -183,8 +183,9 @@ class Executor:
 
     def bind_plan(self, plan_json: str) -> None:
         """Replay an external to_json(GlobalPlan) of this executor's trace
-        (memo_exec_bind_plan): status 2 if it does not fit the trace, 3 if it
-        needs more than the reserved arena.  Before the first step."""
+        (memo_exec_bind_plan): status 2 if it does not fit the trace or the
+        step is already captured as a CUDA graph, 3 if it needs more than the
+        reserved arena."""
         check(lib.memo_exec_bind_plan(self._h, plan_json.encode()))
 
     def tensor_ptr(self, name: str, layer: int = -1):

@@ -43,7 +43,7 @@ def test_fullwidth_step_matches_cpu_oracle_fixture():
     assert sum(e.kind == "recompute" for e in tl) == 1
     ref_loss = float(fx["loss"])
     assert abs(loss - ref_loss) <= 5e-3 * abs(ref_loss), (loss, ref_loss)
-    worst = ("", 0.0)
+    rows = []
     for name, layer, off, cnt in O.layout(O.make_cfg(N, H_, HEADS, F, V, S)):
         key = f"{name}/{layer}"
         g = grads[off:off + cnt]
@@ -51,8 +51,10 @@ def test_fullwidth_step_matches_cpu_oracle_fixture():
         gs = g[sample_indices(name, layer, cnt)]
         rel = float(np.linalg.norm(gs - r) / max(np.linalg.norm(r), 1e-30))
         n_ratio = float(np.sqrt(np.dot(g.astype(np.float64), g.astype(np.float64)) / fx[key + "/norm2"]))
+        rows.append((key, cnt, rel, n_ratio))
+    for key, cnt, rel, n_ratio in rows:
+        print(f"fullwidth {key:14s} n={cnt:>10d} rel-L2 {rel:.3e} norm ratio {n_ratio:.5f}")
+    print(f"fullwidth: loss {loss:.6f} vs {ref_loss:.6f}")
+    for key, cnt, rel, n_ratio in rows:
         assert rel < 2e-2, (key, rel)
         assert abs(n_ratio - 1) < 2e-2, (key, n_ratio)
-        if rel > worst[1]:
-            worst = (key, rel)
-    print(f"fullwidth: loss {loss:.6f} vs {ref_loss:.6f}; worst sampled rel-L2 {worst[1]:.2e} ({worst[0]})")

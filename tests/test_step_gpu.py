@@ -247,8 +247,9 @@ def test_load_batch_rejects_out_of_range_ids():
 def test_bound_external_plan_is_replayed():
     """memo_exec_bind_plan: a different valid placement of the executor's trace
     (every arena tensor mirrored inside total_peak) is replayed -- the step
-    computes on the new addresses, gives the default plan's loss and gradients
-    bit for bit, and device memory is unchanged across the steps."""
+    computes on the new addresses (eager, then captured and replayed as a CUDA
+    graph), gives the default plan's loss and gradients bit for bit, and device
+    memory is unchanged across the steps."""
     import json as _json
 
     import torch
@@ -258,7 +259,7 @@ def test_bound_external_plan_is_replayed():
     toks, labels = O.tokens(31, V, S)
     out = {}
     for bound in (False, True):
-        with Executor(cfg, HW, seed=2, alpha=0.5, optimizer=0, ce_chunk=512) as ex:
+        with Executor(cfg, HW, seed=2, alpha=0.5, optimizer=0, ce_chunk=512, cuda_graph=1) as ex:
             if bound:
                 mp = mirror(ex.plan_json(), ex.trace_text())
                 ex.bind_plan(mp)
@@ -270,6 +271,6 @@ def test_bound_external_plan_is_replayed():
             out[bound] = (loss, ex.read("grad/all"))
             from paper_2407_12117_b200 import _abi
             with pytest.raises(_abi.MemoError):
-                ex.bind_plan(ex.plan_json())  # after the first step: refused
+                ex.bind_plan(ex.plan_json())  # the step is captured as a graph: refused
     assert out[False][0] == out[True][0]
     assert np.array_equal(out[False][1], out[True][1])
