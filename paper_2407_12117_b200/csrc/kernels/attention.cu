@@ -448,7 +448,7 @@ __device__ __forceinline__ uint64_t exp2_fma2(uint64_t x2) {
   const uint32_t hi = static_cast<uint32_t>(p >> 32) + (static_cast<uint32_t>(j >> 32) << 23);
   return (static_cast<uint64_t>(hi) << 32) | lo;
 }
-__device__ __forceinline__ void named_bar(int id, int n) {
+[[maybe_unused]] __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
@@ -740,7 +740,7 @@ struct FwdPpSmem {
   static constexpr int BYTES = BAR_OFF + 256 + 1024;
 };
 
-template <int EMU_EVERY>
+template <int EMU_EVERY, bool SPLIT_P = true>  // SPLIT_P: release P in two key halves
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
@@ -852,8 +852,10 @@ __global__ void __launch_bounds__(384, 1)
           dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
                              (j | kk) != 0);
         // keys [64,128): their P lands while the first half's MMAs run
-        dev::mbar_wait_w(&p_full[2 * g + 1], j & 1);
-        dev::tc_fence_after();
+        if (SPLIT_P) {
+          dev::mbar_wait_w(&p_full[2 * g + 1], j & 1);
+          dev::tc_fence_after();
+        }
 #pragma unroll
         for (int kk = TILE / 32; kk < TILE / 16; ++kk)
           dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o, true);
@@ -960,14 +962,16 @@ __global__ void __launch_bounds__(384, 1)
             dev::tmem_st32(t_o + c * 32, o);
           }
         }
-        dev::tmem_st_wait();
-        dev::tc_fence_before();
-        dev::mbar_arrive(&p_full[2 * g]);
+        if (SPLIT_P) {
+          dev::tmem_st_wait();
+          dev::tc_fence_before();
+          dev::mbar_arrive(&p_full[2 * g]);
+        }
         exps(32);
         dev::tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&p[32]));
         dev::tmem_st_wait();
         dev::tc_fence_before();
-        dev::mbar_arrive(&p_full[2 * g + 1]);
+        dev::mbar_arrive(&p_full[2 * g + (SPLIT_P ? 1 : 0)]);
         const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
         l = l * factor + (f2_lo(s01) + f2_hi(s01));
         m = m_new;
@@ -1651,6 +1655,253 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     dev::tmem_dealloc(tmem, 512);
   }
 }
+
+// ------------------------------------------------------------ dK/dV, decoupled P/dS
+// The product dK/dV kernel.  Same math and operands as attn_bwd_dkdv_tm_kernel
+// (K, V resident in TMEM as the A operands of S^T = K Q^T and dP^T = V dO^T,
+// 32-query steps, two compute warps per TMEM lane quarter), but P^T / dS^T no
+// longer overwrite their S^T / dP^T columns: they go to one of two separate
+// 32-column regions, and S^T / dP^T use a single buffer that is released as
+// soon as the compute warps have loaded it into registers.  The tensor pipe
+// therefore computes S^T(g+1), dP^T(g+1) while the compute warps still work on
+// step g, and the loop that limited the old layout -- P/dS(g) -> dV, dK(g) ->
+// S, dP(g+2) into the freed buffer -> compute(g+2) -- is gone:
+//   [0,128) dV | [128,256) dK | [256,320) K | [320,384) V | [384,416) S^T |
+//   [416,448) dP^T | [448+32b, +16) P^T(b) | [464+32b, +16) dS^T(b), b = g % 2
+// (warp ch of a quarter owns queries 16ch..16ch+15: 8 packed columns of each).
+template <int D>
+__global__ void __launch_bounds__(32 * 12, 1)
+    attn_bwd_dkdv_tm2_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
+                             const __grid_constant__ CUtensorMap map_q,
+                             const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                             const float* __restrict__ delta, __nv_bfloat16* __restrict__ dk,
+                             __nv_bfloat16* __restrict__ dv, long long ld, const float2* __restrict__ rope,
+                             long long pos0, int S, int H, float scale, float scale_log2) {
+  using L = DkdvTmSmem<D>;
+  constexpr int NC = L::NC;
+  constexpr int NS = KV_NS;
+  constexpr int CW = 32 * 8;   // compute threads
+  constexpr int COLS = 16;     // query columns per compute warp per step
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* kv_ready = bars + 0;
+  uint64_t* in_full = bars + 1;        // [NS]
+  uint64_t* in_empty = in_full + NS;   // [NS]
+  uint64_t* s_full = in_empty + NS;    // S^T(g), dP^T(g) computed
+  uint64_t* sd_free = s_full + 1;      // ... and loaded by every compute thread
+  uint64_t* p_ready = sd_free + 1;     // [2] P^T / dS^T of region b written
+  uint64_t* pds_free = p_ready + 2;    // [2] dV / dK MMAs done with region b
+  uint64_t* fin = pds_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+
+  const int n_tiles = S / TILE;
+  const int kt = blockIdx.x;  // key tile
+  const int hh = blockIdx.y;
+  const int n_q = n_tiles - kt;
+  const int n_g = n_q * (TILE / QSTEP);
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_do);
+    dev::mbar_init(kv_ready, CW);
+    for (int s2 = 0; s2 < NS; ++s2) {
+      dev::mbar_init(&in_full[s2], 1);
+      dev::mbar_init(&in_empty[s2], 1);
+    }
+    dev::mbar_init(s_full, 1);
+    dev::mbar_init(sd_free, CW);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      dev::mbar_init(&p_ready[s2], CW);
+      dev::mbar_init(&pds_free[s2], 1);
+    }
+    dev::mbar_init(fin, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dv = tmem, t_dk = tmem + 128, t_k = tmem + 256, t_v = tmem + 320;
+  const uint32_t t_s = tmem + 384, t_dp = tmem + 416;
+  auto region = [&](int b) { return tmem + 448 + 32 * b; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < n_q; ++i) {
+        const int qt = kt + i, st = i % NS;
+        dev::mbar_wait(&in_empty[st], ((i / NS) & 1) ^ 1);
+        dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::RQ_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q, &in_full[st],
+                           hh * D + c * 64, qt * TILE);
+          dev::tma_load_2d(smem + L::RD_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_do, &in_full[st],
+                           hh * D + c * 64, qt * TILE);
+        }
+        float* vec = reinterpret_cast<float*>(smem + L::VEC_OFF + st * 1024);
+        const long long off = static_cast<long long>(hh) * S + qt * TILE;
+        dev::bulk_load(vec, lse2 + off, 512, &in_full[st]);
+        dev::bulk_load(vec + 128, delta + off, 512, &in_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    {  // whole warp, converged: MMAs/commits elect one lane
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, QSTEP, false, false);
+      constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
+      dev::mbar_wait_w(kv_ready, 0);
+      dev::tc_fence_after();
+      auto issue_sd = [&](int g) {
+        const int i = g >> 2, qq = g & 3, st = i % NS;
+        if (qq == 0) {
+          dev::mbar_wait_w(&in_full[st], (i / NS) & 1);
+          dev::tc_fence_after();
+        }
+        const uint32_t roff = qq * QSTEP * 128;  // 32 rows of 128 B inside every 64-col chunk
+        const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
+        const uint64_t dod = kmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ts_w(t_s, t_k + kk * 8, kmajor_step(qd, kk), idesc_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma_bf16_ts_w(t_dp, t_v + kk * 8, kmajor_step(dod, kk), idesc_s, kk > 0);
+        dev::mma_commit_w(s_full);
+      };
+      issue_sd(0);
+      for (int g = 0; g < n_g; ++g) {
+        const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+        if (g + 1 < n_g) {
+          dev::mbar_wait_w(sd_free, g & 1);  // S^T(g), dP^T(g) are in registers
+          dev::tc_fence_after();
+          issue_sd(g + 1);
+        }
+        dev::mbar_wait_w(&p_ready[b], (g >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t roff = qq * QSTEP * 128;
+        const uint64_t qm = mnmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
+        const uint64_t dom = mnmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
+#pragma unroll
+        for (int kk = 0; kk < QSTEP / 16; ++kk)
+          dev::mma_bf16_ts_w(t_dv, region(b) + 8 * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
+#pragma unroll
+        for (int kk = 0; kk < QSTEP / 16; ++kk)
+          dev::mma_bf16_ts_w(t_dk, region(b) + 16 + 8 * kk, mnmajor_step(qm, kk), idesc_g, (g | kk) != 0);
+        dev::mma_commit_w(&pds_free[b]);
+        if (qq == 3) dev::mma_commit_w(&in_empty[st]);
+      }
+      dev::mma_commit_w(fin);
+    }
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int ch = (warp - 4) >> 2;  // 16-query slice of each 32-query step
+    const int r = q4 * 32 + lane;    // key row in tile
+    const int kidx = kt * TILE + r;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const long long hcols = static_cast<long long>(H) * D;
+    // K (ch 0) / V (ch 1) row r -> TMEM A operand
+    row_to_tmem<D>((ch == 0 ? kg : vg) + kidx * hcols + hh * D, (ch == 0 ? t_k : t_v) + lane_off);
+    dev::tmem_st_wait();
+    dev::tc_fence_before();
+    dev::mbar_arrive(kv_ready);
+    for (int g = 0; g < n_g; ++g) {
+      const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+      const bool diag = i == 0;
+      if (qq == 0) dev::mbar_wait(&in_full[st], (i / NS) & 1);
+      const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + COLS * ch) * 4;
+      const uint32_t dl = l2 + 512;
+      // lse2 / delta of this step's columns, loaded before the S/dP wait
+      float4 lvv[COLS / 4], dvv[COLS / 4];
+#pragma unroll
+      for (int j4 = 0; j4 < COLS / 4; ++j4) {
+        lvv[j4] = dev::lds_f4(l2 + 16 * j4);
+        dvv[j4] = dev::lds_f4(dl + 16 * j4);
+      }
+      dev::mbar_wait(s_full, g & 1);
+      dev::tc_fence_after();
+      uint32_t sr[COLS], dr[COLS];
+      dev::tmem_ld16(t_s + lane_off + 16 * ch, sr);
+      dev::tmem_ld16(t_dp + lane_off + 16 * ch, dr);
+      dev::tmem_ld_wait_regs(sr, dr);
+      dev::tc_fence_before();
+      dev::mbar_arrive(sd_free);  // the tensor pipe may overwrite S^T / dP^T now
+      uint32_t pp[COLS / 2], dd[COLS / 2];
+      auto body = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+#pragma unroll
+        for (int j4 = 0; j4 < COLS / 4; ++j4) {
+          const float4 lv = lvv[j4];
+          const float4 dv4 = dvv[j4];
+          const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
+          const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+          float p4[4], d4[4];
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {  // column pairs: FFMA2 / FADD2 / FMUL2
+            const uint64_t x2 = ffma2_v(f2_pack(__uint_as_float(sr[4 * j4 + e]), __uint_as_float(sr[4 * j4 + e + 1])),
+                                        scale_log2, f2_pack(lq[e], lq[e + 1]));
+            float pa = dev::ex2(f2_lo(x2));
+            float pb = dev::ex2(f2_hi(x2));
+            if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e < r) pa = 0.f;
+            if (DIAG && qq * QSTEP + COLS * ch + 4 * j4 + e + 1 < r) pb = 0.f;
+            const uint64_t d2 = fmul2(f2_pack(pa, pb),
+                                      fadd2(f2_pack(__uint_as_float(dr[4 * j4 + e]), __uint_as_float(dr[4 * j4 + e + 1])),
+                                            f2_pack(dq4[e], dq4[e + 1])));
+            p4[e] = pa;
+            p4[e + 1] = pb;
+            d4[e] = f2_lo(d2);
+            d4[e + 1] = f2_hi(d2);
+          }
+          pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
+          pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
+          dd[2 * j4] = dev::pack_bf16(d4[0], d4[1]);
+          dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
+        }
+      };
+      if (diag)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
+      if (g >= 2) {  // region b was last read by dV / dK of step g - 2
+        dev::mbar_wait(&pds_free[b], ((g - 2) >> 1) & 1);
+        dev::tc_fence_after();
+      }
+      dev::tmem_st8(region(b) + lane_off + 8 * ch, pp);
+      dev::tmem_st8(region(b) + lane_off + 16 + 8 * ch, dd);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_ready[b]);
+    }
+    dev::mbar_wait(fin, 0);
+    dev::tc_fence_after();
+    __nv_bfloat16* dvrow = dv + static_cast<long long>(kidx) * ld + hh * D;
+    __nv_bfloat16* dkrow = dk + static_cast<long long>(kidx) * ld + hh * D;
+#pragma unroll 1
+    for (int c = ch; c < D / 32; c += 2) {  // 32-column chunks of dV/dK spread over the quarter's warps
+      uint32_t r32[32];
+      float x[32];
+      dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
+      dev::tmem_ld_wait_regs(r32);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dvrow + c * 32, x, 1.f, nullptr);
+      dev::tmem_ld32(t_dk + lane_off + c * 32, r32);
+      dev::tmem_ld_wait_regs(r32);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dkrow + c * 32, x, scale, rope ? rope + (pos0 + kidx) * (D / 2) + c * 16 : nullptr);
+    }
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
 
 // AT: Q and dO live in TMEM (A operands) instead of shared memory.
 template <int D, bool AT>
@@ -2338,7 +2589,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   static std::once_flag f;
   std::call_once(f, [] {
-    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
@@ -2352,6 +2603,8 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
@@ -2370,8 +2623,14 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
 #ifdef MEMO_ATTN_ABLATIONS
   // MEMO_ATTN_DKDV_VARIANT: 1 K/V in shared memory, 2 four warps per lane
   // quarter, 3 P^T/dS^T behind separate barriers, 4/5 every 2nd/4th column
-  // pair's exponentials on the FMA pipe
+  // pair's exponentials on the FMA pipe, 6 P^T/dS^T over their S^T/dP^T
+  // columns (double-buffered S/dP; the round-1 product)
   switch (abl_env("MEMO_ATTN_DKDV_VARIANT", 0)) {
+    case 6:
+      attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
     case 1:
       attn_bwd_dkdv_kernel<D><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
           mq, mk, mv, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.softmax_scale, scale_log2);
@@ -2398,7 +2657,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
       break;
     default:
 #endif
-      attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+      attn_bwd_dkdv_tm2_kernel<D><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
           a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
           scale_log2);
 #ifdef MEMO_ATTN_ABLATIONS
@@ -2448,17 +2707,20 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
 #ifdef MEMO_ATTN_ABLATIONS
   // MEMO_ATTN_FWD_VARIANT: 0-3 one softmax warp per row (bit0 Q in TMEM, bit1
   // FMA exp2 share); 5-7 split rows (1/4, none, 1/8 FMA share); 8-12 ping-pong
-  // with FMA share 1/3 (product), none, 1/8, 1/4, 1/2
+  // with FMA share 1/3 (product), none, 1/8, 1/4, 1/2; 13 ping-pong without the
+  // two-half P release (the round-1 product)
   const int v = abl_env("MEMO_ATTN_FWD_VARIANT", 8);
   if (v != 8) {
     if (v >= 9 && a.D == 128 && a.S % (2 * TILE) == 0) {
       static std::once_flag fa;
       std::call_once(fa, [] {
-        for (auto k : {attn_fwd_pp_kernel<0>, attn_fwd_pp_kernel<8>, attn_fwd_pp_kernel<4>, attn_fwd_pp_kernel<2>})
+        for (auto k : {attn_fwd_pp_kernel<0>, attn_fwd_pp_kernel<8>, attn_fwd_pp_kernel<4>, attn_fwd_pp_kernel<2>,
+                       attn_fwd_pp_kernel<3, false>})
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
       });
       auto kern = v == 9 ? attn_fwd_pp_kernel<0> : v == 10 ? attn_fwd_pp_kernel<8>
-                : v == 11 ? attn_fwd_pp_kernel<4> : attn_fwd_pp_kernel<2>;
+                : v == 11 ? attn_fwd_pp_kernel<4> : v == 12 ? attn_fwd_pp_kernel<2>
+                : attn_fwd_pp_kernel<3, false>;
       kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
                                                                           scale_log2);
     } else if ((v == 5 || v == 6 || v == 7) && a.D == 128) {

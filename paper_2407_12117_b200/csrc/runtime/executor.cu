@@ -1088,11 +1088,18 @@ GemmDesc rows_of(GemmDesc g, int r0, int m) {
 }
 }  // namespace
 
-void Executor::gemm_reduce_rows(GemmDesc g, float* part, float* out) {
+// row0 > 0: only rows [row0, Sl) of every rank's block (the recompute suffix);
+// `part` and `out` keep their [Sl, N] layout, so the reduced rows land where a
+// full-block call puts them, bitwise equal (per-row GEMM results do not depend
+// on M, and the sum order is unchanged).
+void Executor::gemm_reduce_rows(GemmDesc g, float* part, float* out, int row0) {
   const int t = d_.t, Sl = d_.Sl, r = d_.r;
-  const auto* a = static_cast<const __nv_bfloat16*>(g.a);
-  const size_t count = static_cast<size_t>(Sl) * g.N;
-  g.M = Sl;
+  if (row0 >= Sl) return;
+  const auto* a = static_cast<const __nv_bfloat16*>(g.a) + static_cast<Bytes>(row0) * g.lda;
+  const size_t count = static_cast<size_t>(Sl - row0) * g.N;
+  part += static_cast<Bytes>(row0) * g.N;
+  out += static_cast<Bytes>(row0) * g.N;
+  g.M = Sl - row0;
   g.c = part;
   g.ldc = g.N;
   if (!peer()) {
@@ -1267,8 +1274,9 @@ void Executor::layer_recompute_tp(int i) {
       g.q = Q; g.k = K; g.v = Vv; g.hidden = hl; g.head_dim = D; g.rope = rope_; g.pos0 = 0;
       gather_gemm(XN, xn_full, g, sw);  // suffix rows [sw, S) only
     }
-    // attn_proj needs every rank's partial: redo the out-projection + RS exactly as forward
-    gemm_reduce_rows(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, nullptr, h), a_part, a_red);
+    // attn_proj needs every rank's partial of its suffix rows: the out-projection
+    // + reduce-scatter of rows [swl, Sl) of every rank's block only
+    gemm_reduce_rows(gd(S, h, hl, O, hl, 0, P("wo"), hl, 0, GEMM_EPI_F32, nullptr, h), a_part, a_red, swl);
     if (Rl > 0) {
       G(resid_round(X + r0 * h, a_red + r0 * h, A + r0 * h, x1 + r0 * h,
                     static_cast<long long>(Rl) * h, cs_));

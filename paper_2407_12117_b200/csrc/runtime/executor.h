@@ -142,7 +142,7 @@ class Executor {
   // Row-parallel GEMM (A [S, K] bf16 K-major, f32 output) followed by the
   // sequence reduce-scatter, one rank's row block at a time: part holds S/t
   // rows; rank k's block is reduced onto rank k's out.
-  void gemm_reduce_rows(GemmDesc g, float* part, float* out);
+  void gemm_reduce_rows(GemmDesc g, float* part, float* out, int row0 = 0);
   // Sequence all-gather of `shard` ([S/t, K] bf16) into `full` ([S, K]) fused
   // with the column-parallel GEMM g (A = full, rows [row0, S)).  On a peer
   // backend the row blocks are pulled by the copy engine on the comm stream

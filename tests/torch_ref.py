@@ -92,3 +92,39 @@ def loss_and_grads(cfg, params_np, tokens, labels):
     loss = loss_fn(cfg, p, tokens, labels)
     loss.backward()
     return loss.item(), p.grad.numpy()
+
+
+def amp_loss_and_grads(cfg, params_np, tokens, labels, device="cuda"):
+    """The same model as PyTorch's standard bf16 mixed-precision step: fp32
+    master parameters, torch.autocast(bfloat16) GEMMs, scaled_dot_product_attention
+    (flash, bf16) and fp32 autograd.  No straight-through roundings: autocast's
+    own bf16 casts are the storage points.  Used as the yardstick of what bf16
+    training error looks like at a given width (tests/test_fullwidth_gpu.py)."""
+    S, h, H, D, F = cfg.seq, cfg.hidden, cfg.n_heads, cfg.head_dim, cfg.ffn
+    p = torch.tensor(params_np, dtype=torch.float32, device=device, requires_grad=True)
+    E, layers, gf, W = unpack(cfg, p)
+    cs = rope_tables(S, D, cfg.rope_theta).float().to(device)
+    tok = torch.as_tensor(tokens, dtype=torch.long, device=device)
+    lab = torch.as_tensor(labels, dtype=torch.long, device=device)
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        x = E[tok]
+        for L in layers:
+            xn = rmsnorm(x.float(), L["g1"], cfg.eps)
+            qkv = xn @ L["wqkv"].t()
+            q = rope(qkv[:, :h].float(), cs, H, D).to(torch.bfloat16)
+            k = rope(qkv[:, h:2 * h].float(), cs, H, D).to(torch.bfloat16)
+            v = qkv[:, 2 * h:]
+            qh, kh, vh = (t.reshape(S, H, D).transpose(0, 1)[None] for t in (q, k, v))
+            o = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=True)
+            o = o[0].transpose(0, 1).reshape(S, h)
+            x1 = x.float() + (o @ L["wo"].t()).float()
+            xn2 = rmsnorm(x1, L["g2"], cfg.eps)
+            gu = xn2 @ L["wgu"].t()
+            act = torch.nn.functional.silu(gu[:, :F].float()) * gu[:, F:].float()
+            x = x1 + (act @ L["wd"].t()).float()
+        xf = rmsnorm(x.float(), gf, cfg.eps)
+        logits = (xf @ W.t()).float()
+        keep = lab >= 0
+        loss = torch.nn.functional.cross_entropy(logits[keep], lab[keep])
+    loss.backward()
+    return loss.item(), p.grad.detach().cpu().numpy()
