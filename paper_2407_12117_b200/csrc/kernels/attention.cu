@@ -1656,8 +1656,10 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   }
 }
 
+#ifdef MEMO_ATTN_ABLATIONS  // decoupled P/dS dK/dV (ablation build only)
 // ------------------------------------------------------------ dK/dV, decoupled P/dS
-// The product dK/dV kernel.  Same math and operands as attn_bwd_dkdv_tm_kernel
+// Ablation (measured 12 % SLOWER at 128K than attn_bwd_dkdv_tm_kernel<D, 2>:
+// 231-232 vs 206-207 ms, H=32, D=128, interleaved runs).  Same math and operands as attn_bwd_dkdv_tm_kernel
 // (K, V resident in TMEM as the A operands of S^T = K Q^T and dP^T = V dO^T,
 // 32-query steps, two compute warps per TMEM lane quarter), but P^T / dS^T no
 // longer overwrite their S^T / dP^T columns: they go to one of two separate
@@ -1904,6 +1906,8 @@ __global__ void __launch_bounds__(32 * 12, 1)
 
 
 // AT: Q and dO live in TMEM (A operands) instead of shared memory.
+#endif  // MEMO_ATTN_ABLATIONS
+
 template <int D, bool AT>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_dq_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dout,
@@ -2589,7 +2593,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   if (!ok) return cudaErrorInvalidValue;
   static std::once_flag f;
   std::call_once(f, [] {
-    cudaFuncSetAttribute(attn_bwd_dkdv_tm2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
@@ -2604,7 +2608,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
-    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
@@ -2623,11 +2627,11 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
 #ifdef MEMO_ATTN_ABLATIONS
   // MEMO_ATTN_DKDV_VARIANT: 1 K/V in shared memory, 2 four warps per lane
   // quarter, 3 P^T/dS^T behind separate barriers, 4/5 every 2nd/4th column
-  // pair's exponentials on the FMA pipe, 6 P^T/dS^T over their S^T/dP^T
-  // columns (double-buffered S/dP; the round-1 product)
+  // pair's exponentials on the FMA pipe, 7 P^T/dS^T decoupled from a single
+  // S^T/dP^T buffer (attn_bwd_dkdv_tm2_kernel: 231-232 vs 206-207 ms at 128K)
   switch (abl_env("MEMO_ATTN_DKDV_VARIANT", 0)) {
-    case 6:
-      attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+    case 7:
+      attn_bwd_dkdv_tm2_kernel<D><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
           a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
           scale_log2);
       break;
@@ -2657,7 +2661,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
       break;
     default:
 #endif
-      attn_bwd_dkdv_tm2_kernel<D><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+      attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
           a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
           scale_log2);
 #ifdef MEMO_ATTN_ABLATIONS

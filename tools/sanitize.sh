@@ -33,6 +33,13 @@ for D in 64 128; do
       > $OUT/perturb_attn$D.txt 2>&1
   echo "attn D=$D under racecheck vs normal: $(grep -c DIFFERS $OUT/perturb_attn$D.txt) differing outputs" | tee -a $OUT/summary.txt
 done
+# ... and for every GEMM kernel variant (racecheck reports hazards on the
+# CTA-pair kernel's tcgen05.alloc.cta_group::2 result slot; equal outputs under
+# its perturbation are the evidence that no data race reaches the results)
+a=$(python tools/gemm_variants_probe.py | grep sha256)
+b=$(timeout 900 $CS --tool racecheck python tools/gemm_variants_probe.py 2>/dev/null | grep sha256)
+[ -n "$a" ] && [ "$a" == "$b" ] && r=equal || r=DIFFERS
+echo "GEMM variants under racecheck vs normal: $r" | tee -a $OUT/summary.txt
 # The same check for whole training steps: single GPU (D=64 and D=128) and the
 # SP+TP t=2 peer-memory path.
 for args in "0 1 4" "0 1 2" "3 2 4"; do
