@@ -80,7 +80,8 @@ class GemmArgsC(C.Structure):
                 ("out_f32", C.c_void_p), ("resid", C.c_void_p), ("ld_f32", C.c_int64),
                 ("q", C.c_void_p), ("k", C.c_void_p), ("v", C.c_void_p),
                 ("hidden", C.c_int32), ("head_dim", C.c_int32),
-                ("rope", C.c_void_p), ("pos0", C.c_int64), ("variant", C.c_int32)]
+                ("rope", C.c_void_p), ("pos0", C.c_int64), ("variant", C.c_int32),
+                ("raster", C.c_int32)]
 
 
 class MemoError(RuntimeError):

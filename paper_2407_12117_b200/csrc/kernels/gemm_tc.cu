@@ -67,7 +67,8 @@ struct EpiParams {
   int head_dim;
   const float2* rope;
   long long pos0;
-  int staged;  // BF16/F32 stores through the shared-memory slab (MEMO_GEMM_EPI_STAGE)
+  int staged;  // BF16/F32 stores through the shared-memory slab
+  int serpentine;  // odd raster bands walk N backwards (the last band's B tiles are still in L2)
 };
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* x) {
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int local = t - g * group_size;
     mb = first_m + local % gm;
     nb = local / gm;
+    if (ep.serpentine && (g & 1)) nb = n_units - 1 - nb;
     if (MC) mb = 2 * mb + static_cast<int>(rm);
     if (CL == 4) nb = 2 * nb + static_cast<int>(rn);
   };
@@ -509,6 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int local = t - g * group_size;
     mb = first_m + local % gm;
     nb = local / gm;
+    if (ep.serpentine && (g & 1)) nb = n_tiles - 1 - nb;
   };
 
   if (warp == 0) {
@@ -668,6 +671,10 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   ep.rope = reinterpret_cast<const float2*>(d.rope);
   ep.pos0 = d.pos0;
   ep.staged = 1;  // swizzled shared-memory slab stores (the direct stores remain for the fused epilogues)
+  // Serpentine raster: every other band of GROUP_M row tiles walks the N tiles
+  // backwards, so a band starts on the B tiles the previous band read last
+  // (still L2-resident).  Tile order only: results are bitwise unchanged.
+  ep.serpentine = d.raster == GEMM_RASTER_LEGACY ? 0 : 1;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<A_MN, B_MN, 1>,

@@ -23,6 +23,9 @@ enum GemmVariant {
   GEMM_VARIANT_PAIR = 4,    // CTA-pair 256x256 tiles (cta_group::2)
 };
 
+// Tile order: GEMM_RASTER_AUTO (serpentine bands) or the round-1 order (A/B tools).
+enum GemmRaster { GEMM_RASTER_AUTO = 0, GEMM_RASTER_LEGACY = 1 };
+
 // C = A . B^T with A logical [M, K], B logical [N, K].
 //   a_mn_major = 0: A stored [M][lda], K contiguous;  1: stored [K][lda], M contiguous.
 //   b_mn_major = 0: B stored [N][ldb], K contiguous;  1: stored [K][ldb], N contiguous.
@@ -48,6 +51,7 @@ struct GemmDesc {
   const void* rope = nullptr;  // float2 [positions][head_dim/2] (cos, sin)
   long long pos0 = 0;          // absolute position of row 0
   int variant = GEMM_VARIANT_AUTO;
+  int raster = GEMM_RASTER_AUTO;
 };
 
 cudaError_t gemm_tc(const GemmDesc& d, cudaStream_t stream);

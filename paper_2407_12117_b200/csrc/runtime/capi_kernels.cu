@@ -37,6 +37,7 @@ extern "C" int memo_gemm(const memo_gemm_args* a, void* stream) {
   d.rope = a->rope;
   d.pos0 = a->pos0;
   d.variant = a->variant;
+  d.raster = a->raster;
   cudaError_t e = memo::gemm_tc(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess)
     return set_error(MEMO_ERR_INTERNAL, std::string("memo_gemm: ") + cudaGetErrorString(e));

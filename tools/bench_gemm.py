@@ -30,6 +30,7 @@ def run(M, N, K, layout, iters=10):
     # GEMM_VARIANT (this tool's switch): 0 product choice, 1 single CTA, 2 B-multicast
     # cluster, 3 2x2 cluster, 4 CTA pair (memo_gemm_args.variant)
     args.variant = int(os.environ.get("GEMM_VARIANT", "0"))
+    args.raster = int(os.environ.get("GEMM_RASTER", "0"))  # 1: the round-1 tile order
     for _ in range(3):
         _abi.check(_abi.lib.memo_gemm(C.byref(args), None))
     torch.cuda.synchronize()

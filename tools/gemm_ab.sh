@@ -7,6 +7,6 @@ OUT=${1:-gpurun_out/gemm_ab.jsonl}; S=${2:-131072}
 mkdir -p $(dirname $OUT)
 for rep in $(seq ${REPS:-4}); do
   for v in ${VARIANTS:-0 2 4}; do
-    GEMM_VARIANT=$v timeout 300 python tools/bench_gemm.py $S | sed "s/^{/{\"variant\": $v, \"rep\": $rep, /" >> $OUT
+    GEMM_VARIANT=$v GEMM_RASTER=${RASTER:-0} timeout 300 python tools/bench_gemm.py $S | sed "s/^{/{\"variant\": $v, \"raster\": ${RASTER:-0}, \"rep\": $rep, /" >> $OUT
   done
 done
