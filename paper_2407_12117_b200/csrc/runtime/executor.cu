@@ -1150,14 +1150,14 @@ void Executor::gemm_reduce_rows(GemmDesc g, float* part, float* out, int row0) {
   stats_.kernel_launches += t - 1;
 }
 
-void Executor::gather_gemm(const __nv_bfloat16* shard, __nv_bfloat16* full, GemmDesc g, int row0) {
-  const int t = d_.t, Sl = d_.Sl, r = d_.r, S = d_.S;
-  const size_t shard_elems = static_cast<size_t>(Sl) * g.K;
-  if (!peer()) {
-    ag(comm_.get(), shard, full, shard_elems, cs_);
-    if (row0 < S) gemm(rows_of(g, row0, S - row0));
-    return;
-  }
+// Peer all-gather of the t row blocks of `full` ([S, width] bf16; this rank's
+// block is `shard`): the copy engines pull every peer's block on its own
+// stream, each rank starting at its own index so every link is busy, and
+// ev_blk_[j] marks block (r + j) % t landed.  gather_release() must follow
+// once the consumers of `full` have been enqueued behind those events.
+void Executor::gather_pull(const __nv_bfloat16* shard, __nv_bfloat16* full, size_t width) {
+  const int t = d_.t, Sl = d_.Sl, r = d_.r;
+  const size_t shard_elems = static_cast<size_t>(Sl) * width;
   for (int k = 0; k < t; ++k)
     if (k != r) comm_->signal(k, CH_AG_READY, cs_);
   ck(cudaEventRecord(ev_cs2xs_, cs_), "record");
@@ -1178,14 +1178,56 @@ void Executor::gather_gemm(const __nv_bfloat16* shard, __nv_bfloat16* full, Gemm
   for (int j = 1; j < t; ++j) ck(cudaStreamWaitEvent(xs_, ev_blk_[j], 0), "wait");  // all pulls done
   for (int k = 0; k < t; ++k)
     if (k != r) comm_->signal(k, CH_AG_DONE, xs_);
+}
+
+void Executor::gather_release() {
+  for (int k = 0; k < d_.t; ++k)
+    if (k != d_.r) comm_->wait(k, CH_AG_DONE, cs_);  // nobody reads my shard any more
+}
+
+void Executor::gather_gemm(const __nv_bfloat16* shard, __nv_bfloat16* full, GemmDesc g, int row0) {
+  const int t = d_.t, Sl = d_.Sl, r = d_.r, S = d_.S;
+  if (!peer()) {
+    ag(comm_.get(), shard, full, static_cast<size_t>(Sl) * g.K, cs_);
+    if (row0 < S) gemm(rows_of(g, row0, S - row0));
+    return;
+  }
+  gather_pull(shard, full, static_cast<size_t>(g.K));
   for (int j = 0; j < t; ++j) {
     const int k = (r + j) % t;
     ck(cudaStreamWaitEvent(cs_, ev_blk_[j], 0), "wait");
     const int lo = std::max(row0, k * Sl), hi = (k + 1) * Sl;
     if (lo < hi) gemm(rows_of(g, lo, hi - lo));
   }
-  for (int k = 0; k < t; ++k)
-    if (k != r) comm_->wait(k, CH_AG_DONE, cs_);  // nobody reads my shard any more
+  gather_release();
+}
+
+// All-gather -> weight-gradient GEMM (dW = dY^T X_full, K = S): the gathered
+// input's row blocks are the K blocks of the GEMM, so block k's partial is
+// accumulated as soon as it has landed (GEMM_EPI_F32 for block 0, F32_ACC
+// after), in the fixed order k = 0..t-1 on every communicator -- loopback,
+// NCCL and peer memory sum the same way, bitwise.
+void Executor::gather_wgrad(const __nv_bfloat16* shard, __nv_bfloat16* full, GemmDesc g) {
+  const int t = d_.t, Sl = d_.Sl, r = d_.r;
+  auto block = [&](int k) {
+    GemmDesc gk = g;
+    gk.K = Sl;
+    gk.a = static_cast<const char*>(g.a) + static_cast<Bytes>(k) * Sl * g.lda * 2;
+    gk.b = static_cast<const char*>(g.b) + static_cast<Bytes>(k) * Sl * g.ldb * 2;
+    gk.epi = k == 0 ? GEMM_EPI_F32 : GEMM_EPI_F32_ACC;
+    gemm(gk);
+  };
+  if (!peer()) {
+    ag(comm_.get(), shard, full, static_cast<size_t>(Sl) * g.ldb, cs_);
+    for (int k = 0; k < t; ++k) block(k);
+    return;
+  }
+  gather_pull(shard, full, static_cast<size_t>(g.ldb));
+  for (int k = 0; k < t; ++k) {
+    ck(cudaStreamWaitEvent(cs_, ev_blk_[(k - r + t) % t], 0), "wait");
+    block(k);
+  }
+  gather_release();
 }
 
 void Executor::layer_fwd_tp(int i) {
@@ -1328,15 +1370,13 @@ void Executor::layer_bwd_tp(int i) {
   float* dxn = static_cast<float*>(A_("dxn"));
   auto* xn_full = static_cast<__nv_bfloat16*>(A_("b_xn_full"));
   float* part1 = static_cast<float*>(A_("part1"));
-  const size_t shard = static_cast<size_t>(Sl) * h;
 
   // MLP (down is row-parallel: its input gradient is the gathered output grad)
   gather_gemm(dxb, dy_full, gd(S, Fl, h, dy_full, h, 0, P("wd"), Fl, 1, GEMM_EPI_BF16, dact, Fl), 0);
   gemm(gd(h, Fl, S, dy_full, h, 1, ACT, Fl, 1, GEMM_EPI_F32, Gr("wd"), Fl));
   G(swiglu_bwd(GU, dact, dgu, S, Fl, cs_));
   gemm_reduce_rows(gd(S, h, 2 * Fl, dgu, 2 * Fl, 0, P("wgu"), h, 1, GEMM_EPI_F32, nullptr, h), dxn2_part, dxn2);
-  ag(comm_.get(), XN2, xn2_full, shard, cs_);
-  gemm(gd(2 * Fl, h, S, dgu, 2 * Fl, 1, xn2_full, h, 1, GEMM_EPI_F32, Gr("wgu"), h));
+  gather_wgrad(XN2, xn2_full, gd(2 * Fl, h, S, dgu, 2 * Fl, 1, xn2_full, h, 1, GEMM_EPI_F32, Gr("wgu"), h));
   G(rmsnorm_bwd(X, A, P("g2"), dxn2, dxc, dxc, da, part2, Gr("g2"), Sl, h, opt_.eps, false, cs_));
   // attention output projection (row-parallel)
   gather_gemm(da, da_full, gd(S, hl, h, da_full, h, 0, P("wo"), hl, 1, GEMM_EPI_BF16, dout, hl), 0);
@@ -1349,8 +1389,7 @@ void Executor::layer_bwd_tp(int i) {
   attention_bwd(ba);
   // QKV projection (column-parallel)
   gemm_reduce_rows(gd(S, h, 3 * hl, dqkv, 3 * hl, 0, P("wqkv"), h, 1, GEMM_EPI_F32, nullptr, h), dxn_part, dxn);
-  ag(comm_.get(), XN, xn_full, shard, cs_);
-  gemm(gd(3 * hl, h, S, dqkv, 3 * hl, 1, xn_full, h, 1, GEMM_EPI_F32, Gr("wqkv"), h));
+  gather_wgrad(XN, xn_full, gd(3 * hl, h, S, dqkv, 3 * hl, 1, xn_full, h, 1, GEMM_EPI_F32, Gr("wqkv"), h));
   G(rmsnorm_bwd(X, nullptr, P("g1"), dxn, dxc, dxc, dxb, part1, Gr("g1"), Sl, h, opt_.eps, false, cs_));
   stats_.kernel_launches += 5;
   mark(0, static_cast<int>(Kind::LayerBwd), i, false);

@@ -149,6 +149,9 @@ class Executor {
   // (own block first) and the GEMM of block k starts as soon as k has landed;
   // otherwise it is the collective followed by one GEMM.
   void gather_gemm(const __nv_bfloat16* shard, __nv_bfloat16* full, GemmDesc g, int row0);
+  void gather_wgrad(const __nv_bfloat16* shard, __nv_bfloat16* full, GemmDesc g);
+  void gather_pull(const __nv_bfloat16* shard, __nv_bfloat16* full, size_t width);
+  void gather_release();
   bool peer() const { return comm_ && comm_->peer_ready(); }
   void attention_fwd(AttnFwdArgs a);
   void attention_bwd(AttnBwdArgs a);
