@@ -740,7 +740,29 @@ struct FwdPpSmem {
   static constexpr int BYTES = BAR_OFF + 256 + 1024;
 };
 
-template <int EMU_EVERY, bool SPLIT_P = true>  // SPLIT_P: release P in two key halves
+// Optional cycle accounting of the ping-pong forward (build with -DMEMO_FWD_PROF,
+// tools/fwd_prof.py), one softmax thread per group (g = 0, 1), summed over
+// tiles: [8g+0] waiting for S, [8g+1] S ready -> keys [0,64) released, [8g+2]
+// S ready -> all of P released, [8g+3] release -> end of tile (row sum), [8g+4]
+// tiles; [16] MMA warp waiting for P, [17] MMA warp waiting for K/V, [18] MMA
+// warp total.
+#ifdef MEMO_FWD_PROF
+__device__ unsigned long long g_fwd_prof[24];
+#define FWD_PROF(...) __VA_ARGS__
+#else
+#define FWD_PROF(...)
+#endif
+
+// SPLIT_P: release P in two key halves.  NULL_SM (ablation build only): no row
+// max and no exponentials (P = bf16(S)); every load, store, barrier and MMA is
+// kept, so its time is the kernel's ceiling with free softmax math.
+// SEQ (ablation): the two groups' softmax warps of one SMSP take turns on the
+// exponential phase (named barriers: A(j) -> B(j) -> A(j+1) ...), so each runs
+// alone on its SMSP instead of both slowing each other down.
+// QSTORE (ablation): P in four quarters stored as packed, keys [0,64) released
+// after the third quarter, row sum after the release (measured 1-2 % slower).
+template <int EMU_EVERY, bool SPLIT_P = true, bool NULL_SM = false, bool NULL_MMA = false, bool SEQ = false,
+          bool QSTORE = false>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
@@ -825,40 +847,51 @@ __global__ void __launch_bounds__(384, 1)
                               kmajor_base(dev::smem_u32(smem + L::QB_OFF))};
       const int nA = n_kv - 1;
       dev::mbar_wait_w(q_full, 0);
+      FWD_PROF(long long pf_total = clock64(); long long pf_kv = 0, pf_p = 0;)
       auto issue_s = [&](int g, int j) {  // S_g(j) = Q_g K_j^T ; group A always issues first for tile j
         const int st = j & 1;
         if (g == 0 || j == nA) {
+          FWD_PROF(long long t = clock64();)
           dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
+          FWD_PROF(pf_kv += clock64() - t;)
           dev::tc_fence_after();
         }
         const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          dev::mma_bf16_ss_w(tmem + g * 128, kmajor_step(g ? qd[1] : qd[0], kk), kmajor_step(kd, kk), idesc_s,
-                             kk > 0);
+          if (!NULL_MMA)
+            dev::mma_bf16_ss_w(tmem + g * 128, kmajor_step(g ? qd[1] : qd[0], kk), kmajor_step(kd, kk), idesc_s,
+                               kk > 0);
         dev::mma_commit_w(&s_full[g]);
         if (g == 1) dev::mma_commit_w(&k_empty[st]);  // B is the last reader of K_j
       };
       auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j, one key half at a time
         const int st = j & 1;
+        FWD_PROF(long long t = clock64();)
         dev::mbar_wait_w(&p_full[2 * g], j & 1);
+        FWD_PROF(long long t2 = clock64(); pf_p += t2 - t;)
         if (g == 0 || j == nA) {
           dev::mbar_wait_w(&v_full[st], (j >> 1) & 1);
         }
+        FWD_PROF(pf_kv += clock64() - t2;)
         dev::tc_fence_after();
         const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
 #pragma unroll
         for (int kk = 0; kk < TILE / 32; ++kk)
-          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
-                             (j | kk) != 0);
+          if (!NULL_MMA)
+            dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
+                               (j | kk) != 0);
         // keys [64,128): their P lands while the first half's MMAs run
         if (SPLIT_P) {
+          FWD_PROF(long long t3 = clock64();)
           dev::mbar_wait_w(&p_full[2 * g + 1], j & 1);
+          FWD_PROF(pf_p += clock64() - t3;)
           dev::tc_fence_after();
         }
 #pragma unroll
         for (int kk = TILE / 32; kk < TILE / 16; ++kk)
-          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o, true);
+          if (!NULL_MMA)
+            dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o, true);
         // S_g(j+1) is issued after PV_g(j), so s_full already orders the
         // softmax's O rescale after PV_g(j); o_done only serves the epilogue.
         if (j == (g ? n_kv - 1 : nA - 1)) dev::mma_commit_w(&o_done[g]);
@@ -874,6 +907,11 @@ __global__ void __launch_bounds__(384, 1)
         issue_pv(1, j);
         if (j + 1 < n_kv) issue_s(1, j + 1);
       }
+      FWD_PROF(if (lane == 0) {
+        atomicAdd(&g_fwd_prof[16], static_cast<unsigned long long>(pf_p));
+        atomicAdd(&g_fwd_prof[17], static_cast<unsigned long long>(pf_kv));
+        atomicAdd(&g_fwd_prof[18], static_cast<unsigned long long>(clock64() - pf_total));
+      })
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
@@ -887,8 +925,11 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t t_s = tmem + g * 128 + lane_off;
     const uint32_t t_o = tmem + 256 + g * D + lane_off;
     float m = -INFINITY, l = 0.f;
+    FWD_PROF(const bool pf_on = (q4 == 0 && lane == 0); long long pf[4] = {0, 0, 0, 0}; long long pf_t1 = 0;)
     for (int j = 0; j < n_my; ++j) {
+      FWD_PROF(long long pf_t0 = clock64();)
       dev::mbar_wait(&s_full[g], j & 1);
+      FWD_PROF(pf_t1 = clock64(); pf[0] += pf_t1 - pf_t0;)
       dev::tc_fence_after();
       uint32_t r[4][32];
 #pragma unroll
@@ -905,7 +946,7 @@ __global__ void __launch_bounds__(384, 1)
             if (i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
         }
         // row max: 8 independent chains of 3-input FMNMX3 (68 instructions, not 134)
-        auto rv = [&](int i) { return __uint_as_float(r[i >> 5][i & 31]); };
+        auto rv = [&](int i) { return NULL_SM ? 0.f : __uint_as_float(r[i >> 5][i & 31]); };
         float mx8[8];
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(rv(k2), rv(8 + k2));
@@ -924,10 +965,12 @@ __global__ void __launch_bounds__(384, 1)
           m_new = cand;
           factor = j == 0 ? 0.f : dev::ex2(m - m_new);
         }
-        uint64_t sum4[4] = {0, 0, 0, 0};
+        if constexpr (!QSTORE) {
         // P in two key halves: the first half's P (keys [0,64)) is stored and
         // released before the second half's exponentials, so the tensor pipe
-        // runs PV over the first half while the second is still computed.
+        // can run PV over the first half while the second is computed (ptxas
+        // interleaves the two halves' exponentials; tools/fwd_prof.py).
+        uint64_t sum4[4] = {0, 0, 0, 0};
         auto exps = [&](int i0) {
 #pragma unroll
           for (int i = i0; i < i0 + 32; ++i) {
@@ -935,7 +978,10 @@ __global__ void __launch_bounds__(384, 1)
                                               __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
                                       scale_log2, -m_new);
             float a, b;
-            if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
+            if (NULL_SM) {
+              a = f2_lo(x2);
+              b = f2_hi(x2);
+            } else if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
               const uint64_t e2 = exp2_fma2(x2);
               a = f2_lo(e2);
               b = f2_hi(e2);
@@ -966,21 +1012,134 @@ __global__ void __launch_bounds__(384, 1)
           dev::tmem_st_wait();
           dev::tc_fence_before();
           dev::mbar_arrive(&p_full[2 * g]);
+          FWD_PROF(pf[1] += clock64() - pf_t1;)
         }
         exps(32);
         dev::tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&p[32]));
         dev::tmem_st_wait();
         dev::tc_fence_before();
         dev::mbar_arrive(&p_full[2 * g + (SPLIT_P ? 1 : 0)]);
+        FWD_PROF(long long pf_t3 = clock64(); pf[2] += pf_t3 - pf_t1;)
         const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
         l = l * factor + (f2_lo(s01) + f2_hi(s01));
         m = m_new;
+        FWD_PROF(pf[3] += clock64() - pf_t3;)
+        } else {
+        // P in four key quarters, each stored (tcgen05.st, asynchronous) as soon
+        // as it is packed.  Keys [0,64) are released after the third quarter's
+        // exponentials, when their stores have long landed (no exposed store
+        // wait), so PV over them overlaps the last quarter; keys [64,128) at the
+        // end.  The exponentials overwrite their logits in r: the row sum is
+        // taken after the release, off the S -> P critical path.
+        auto exq = [&](int q, float neg_m) {  // column pairs [16q, 16q+16)
+#pragma unroll
+          for (int i = 16 * q; i < 16 * q + 16; ++i) {
+            const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                              __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
+                                      scale_log2, neg_m);
+            float a, b;
+            if (NULL_SM) {
+              a = f2_lo(x2);
+              b = f2_hi(x2);
+            } else if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
+              const uint64_t e2 = exp2_fma2(x2);
+              a = f2_lo(e2);
+              b = f2_hi(e2);
+            } else {
+              a = dev::ex2(f2_lo(x2));
+              b = dev::ex2(f2_hi(x2));
+            }
+            r[i >> 4][(2 * i) & 31] = __float_as_uint(a);
+            r[i >> 4][(2 * i + 1) & 31] = __float_as_uint(b);
+            p[i] = dev::pack_bf16(a, b);
+          }
+        };
+        auto st_q = [&](int q) { dev::tmem_st16(t_s + 16 * q, *reinterpret_cast<uint32_t(*)[16]>(&p[16 * q])); };
+        if (any && j > 0) {
+          // O_g holds P(j-1)V(j-1) (PV_g(j-1) completed before s_full_g(j)
+          // fired); rescaled before any P of this tile is released
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            dev::tmem_ld32(t_o + c * 32, o);
+            dev::tmem_ld_wait_regs(o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+            dev::tmem_st32(t_o + c * 32, o);
+          }
+        }
+        // The same ordering problem for the stores: ptxas keeps the volatile
+        // tcgen05.st in program order but would hoist the next quarters'
+        // exponentials above them, issuing every store just before the wait.  A
+        // clock read after each store (ordered with it) seeds the next quarter's
+        // bias with a signed zero.
+        auto after_store = [&]() {
+          uint32_t c;
+          asm volatile("mov.u32 %0, %%clock;" : "=r"(c)::"memory");
+          return -m_new + __uint_as_float(c & 0x80000000u) * 0.f;
+        };
+        // turn: A(j) waits for B(j-1), B(j) waits for A(j) (B's last tile has no A(j))
+        float neg_m0 = -m_new;
+        if (SEQ && (g == 1 ? j + 1 < n_my : j > 0)) {
+          named_bar(g == 0 ? 5 + q4 : 1 + q4, 64);
+          neg_m0 = after_store();  // clock read after the barrier: the exponentials stay below it
+        }
+        exq(0, neg_m0);
+        st_q(0);
+        exq(1, after_store());
+        st_q(1);
+        exq(2, after_store());
+        // ptxas would otherwise schedule the last quarter's exponentials above
+        // the release (no data dependency keeps them below it): their bias
+        // carries a signed zero derived from the arrive's state token.
+        float neg_m3 = -m_new;
+        if (SPLIT_P) {
+          dev::tmem_st_wait();
+          dev::tc_fence_before();
+          const uint64_t tok0 = dev::mbar_arrive_token(&p_full[2 * g]);
+          neg_m3 += __uint_as_float(static_cast<uint32_t>(tok0) & 0x80000000u) * 0.f;
+          FWD_PROF(pf[1] += clock64() - pf_t1;)
+        }
+        st_q(2);
+        exq(3, neg_m3);
+        if (SEQ) {  // pass the turn: A(j) -> B(j) always; B(j) -> A(j+1) if A has tile j+1
+          if (g == 0)
+            asm volatile("bar.arrive %0, %1;" ::"r"(1 + q4), "r"(64) : "memory");
+          else if (j + 1 < n_my - 1)
+            asm volatile("bar.arrive %0, %1;" ::"r"(5 + q4), "r"(64) : "memory");
+        }
+        st_q(3);
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        const uint64_t tok = dev::mbar_arrive_token(&p_full[2 * g + (SPLIT_P ? 1 : 0)]);
+        FWD_PROF(long long pf_t3 = clock64(); pf[2] += pf_t3 - pf_t1;)
+        // Row sum, same pairing and order as when it ran inside the exponential
+        // loop (bitwise equal).  Its four chains start from a signed zero derived
+        // from the arrive's state token, so ptxas cannot hoist the adds back
+        // above the arrive (onto the S -> P critical path).
+        const float z = __uint_as_float(static_cast<uint32_t>(tok) & 0x80000000u) * 0.f;
+        uint64_t sum4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sum4[k] = f2_pack(z, z);
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                                   __uint_as_float(r[i >> 4][(2 * i + 1) & 31])));
+        const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+        l = l * factor + (f2_lo(s01) + f2_hi(s01));
+        m = m_new;
+        FWD_PROF(pf[3] += clock64() - pf_t3;)
+        }
       };
       if (j == qt)
         tile(std::true_type{});
       else
         tile(std::false_type{});
     }
+    FWD_PROF(if (pf_on) {
+      for (int k = 0; k < 4; ++k) atomicAdd(&g_fwd_prof[8 * g + k], static_cast<unsigned long long>(pf[k]));
+      atomicAdd(&g_fwd_prof[8 * g + 4], static_cast<unsigned long long>(n_my));
+    })
     dev::mbar_wait(&o_done[g], 0);  // committed once, after the group's last PV
     dev::tc_fence_after();
     const float inv = 1.f / l;
@@ -1002,6 +1161,329 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(l)) * kLn2;
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------- forward, ping-pong, split rows
+// The ping-pong schedule of attn_fwd_pp_kernel (two query tiles A/B per CTA,
+// TMEM S_A | S_B | O_A | O_B, one MMA warp alternating PV_A S_A PV_B S_B), with
+// each query row's softmax split over two warps: warpgroup (g, hf) handles key
+// columns [64hf, 64hf+64) of group g's tile, so every SMSP runs four softmax
+// warps instead of two.  The per-tile softmax latency (S ready -> P released)
+// is what sets the tensor pipe's idle time in the one-warp-per-row kernel
+// (tools/fwd_prof.py: ~1650 of a ~2800-cycle step); halving each warp's share
+// of the row shortens it.  The two halves exchange their row maxima through
+// shared memory behind a 64-thread named barrier (one per group and lane
+// quarter) and release their P halves independently: P of keys [0,64) lands in
+// S columns [0,32) (half 0's own columns), keys [64,128) in columns [64,96).
+// Only the hf = 0 warp rescales O (all 128 columns, before it releases the
+// first P half, which is what starts PV_g(j)).
+struct FwdPp2wSmem {
+  static constexpr int TILE_BYTES = 2 * CHUNK_BYTES;  // D = 128
+  static constexpr int QA_OFF = 0;
+  static constexpr int QB_OFF = TILE_BYTES;
+  static constexpr int K_OFF = 2 * TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + 2 * TILE_BYTES;  // 2-stage K and V rings
+  static constexpr int X_OFF = V_OFF + 2 * TILE_BYTES;  // [2 parity][2 g][2 hf][128] f32
+  static constexpr int BAR_OFF = X_OFF + 2 * 2 * 2 * 128 * 4;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+constexpr int PP2W_THREADS = 32 * 20;
+
+template <int EMU_EVERY>
+__global__ void __launch_bounds__(PP2W_THREADS, 1)
+    attn_fwd_pp2w_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                         const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
+                         float* __restrict__ lse, int S, int H, float scale_log2) {
+  constexpr int D = 128;
+  constexpr bool NULL_MMA = false;
+  using L = FwdPp2wSmem;
+  constexpr int NC = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2] per group
+  uint64_t* p_full = bars + 11;  // [2 groups][2 key halves], one warpgroup each
+  uint64_t* o_done = bars + 15;  // [2] per group
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  const uint32_t xchg_s = dev::smem_u32(smem + L::X_OFF);
+
+  const int n_pairs = S / (2 * TILE);
+  const int pp = n_pairs - 1 - static_cast<int>(blockIdx.x);  // heavy pairs first
+  const int hh = blockIdx.y;
+  const int qt0 = 2 * pp;
+  const int n_kv = qt0 + 2;  // key tiles of group B; group A uses n_kv - 1
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_k);
+    dev::tma_prefetch_desc(&map_v);
+    dev::mbar_init(q_full, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      dev::mbar_init(&k_full[s2], 1);
+      dev::mbar_init(&k_empty[s2], 1);
+      dev::mbar_init(&v_full[s2], 1);
+      dev::mbar_init(&v_empty[s2], 1);
+      dev::mbar_init(&s_full[s2], 1);
+      dev::mbar_init(&p_full[2 * s2], 128);
+      dev::mbar_init(&p_full[2 * s2 + 1], 128);
+      dev::mbar_init(&o_done[s2], 1);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (warp == 0) {
+      if (lane == 0) {
+        dev::mbar_expect_tx(q_full, 2 * L::TILE_BYTES);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::QA_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, qt0 * TILE);
+          dev::tma_load_2d(smem + L::QB_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, (qt0 + 1) * TILE);
+        }
+        for (int j = 0; j < n_kv; ++j) {
+          const int st = j & 1;
+          const uint32_t ph = (j >> 1) & 1;
+          dev::mbar_wait(&k_empty[st], ph ^ 1);
+          dev::mbar_expect_tx(&k_full[st], L::TILE_BYTES);
+          for (int c = 0; c < NC; ++c)
+            dev::tma_load_2d(smem + L::K_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_k, &k_full[st],
+                             hh * D + c * 64, j * TILE);
+          dev::mbar_wait(&v_empty[st], ph ^ 1);
+          dev::mbar_expect_tx(&v_full[st], L::TILE_BYTES);
+          for (int c = 0; c < NC; ++c)
+            dev::tma_load_2d(smem + L::V_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_v, &v_full[st],
+                             hh * D + c * 64, j * TILE);
+        }
+      }
+    } else if (warp == 1) {
+      // whole warp, converged: MMAs/commits elect one lane
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc_o = dev::idesc_bf16_f32(128, D, false, true);
+      const uint64_t qd[2] = {kmajor_base(dev::smem_u32(smem + L::QA_OFF)),
+                              kmajor_base(dev::smem_u32(smem + L::QB_OFF))};
+      const int nA = n_kv - 1;
+      FWD_PROF(long long pf_total = clock64(); long long pf_kv = 0, pf_p = 0;)
+      dev::mbar_wait_w(q_full, 0);
+      auto issue_s = [&](int g, int j) {  // S_g(j) = Q_g K_j^T ; group A always issues first for tile j
+        const int st = j & 1;
+        if (g == 0 || j == nA) {
+          FWD_PROF(long long t = clock64();)
+          dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
+          FWD_PROF(pf_kv += clock64() - t;)
+          dev::tc_fence_after();
+        }
+        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::TILE_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          if (!NULL_MMA)
+            dev::mma_bf16_ss_w(tmem + g * 128, kmajor_step(g ? qd[1] : qd[0], kk), kmajor_step(kd, kk), idesc_s,
+                               kk > 0);
+        dev::mma_commit_w(&s_full[g]);
+        if (g == 1) dev::mma_commit_w(&k_empty[st]);  // B is the last reader of K_j
+      };
+      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j, one key half at a time
+        const int st = j & 1;
+        FWD_PROF(long long t = clock64();)
+        dev::mbar_wait_w(&p_full[2 * g], j & 1);
+        FWD_PROF(long long t2 = clock64(); pf_p += t2 - t;)
+        if (g == 0 || j == nA) dev::mbar_wait_w(&v_full[st], (j >> 1) & 1);
+        FWD_PROF(pf_kv += clock64() - t2;)
+        dev::tc_fence_after();
+        const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::TILE_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < TILE / 32; ++kk)  // keys [0,64): P in S cols [0,32)
+          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
+                             (j | kk) != 0);
+        FWD_PROF(long long t3 = clock64();)
+        dev::mbar_wait_w(&p_full[2 * g + 1], j & 1);
+        FWD_PROF(pf_p += clock64() - t3;)
+        dev::tc_fence_after();
+#pragma unroll
+        for (int kk = TILE / 32; kk < TILE / 16; ++kk)  // keys [64,128): P in S cols [64,96)
+          dev::mma_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + 32 + kk * 8, mnmajor_step(vd, kk), idesc_o,
+                             true);
+        if (j == (g ? n_kv - 1 : nA - 1)) dev::mma_commit_w(&o_done[g]);
+        if (g == 1) dev::mma_commit_w(&v_empty[st]);
+      };
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j < nA) {
+          issue_pv(0, j);
+          if (j + 1 < nA) issue_s(0, j + 1);
+        }
+        issue_pv(1, j);
+        if (j + 1 < n_kv) issue_s(1, j + 1);
+      }
+      FWD_PROF(if (lane == 0) {
+        atomicAdd(&g_fwd_prof[16], static_cast<unsigned long long>(pf_p));
+        atomicAdd(&g_fwd_prof[17], static_cast<unsigned long long>(pf_kv));
+        atomicAdd(&g_fwd_prof[18], static_cast<unsigned long long>(clock64() - pf_total));
+      })
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    const int wg = (warp - 4) >> 2;
+    const int g = wg >> 1;   // softmax group: 0 -> tile A, 1 -> tile B
+    const int hf = wg & 1;   // key columns [64hf, 64hf+64) of every S tile
+    const uint32_t q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const int qt = qt0 + g;
+    const int qidx = qt * TILE + row;
+    const int n_my = qt + 1;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const uint32_t t_s = tmem + g * 128 + lane_off;
+    const uint32_t t_o = tmem + 256 + g * D + lane_off;
+    const int bar_id = 1 + 4 * g + q4;  // the two warps holding these rows of this group
+    const uint32_t xmine = xchg_s + ((g * 2 + hf) * 128 + row) * 4;
+    const uint32_t xother = xchg_s + ((g * 2 + (hf ^ 1)) * 128 + row) * 4;
+    float m = -INFINITY, l = 0.f;
+    FWD_PROF(const bool pf_on = (q4 == 0 && lane == 0 && hf == 0); long long pf[4] = {0, 0, 0, 0};)
+    for (int j = 0; j < n_my; ++j) {
+      FWD_PROF(long long pf_t0 = clock64();)
+      dev::mbar_wait(&s_full[g], j & 1);
+      FWD_PROF(long long pf_t1 = clock64(); pf[0] += pf_t1 - pf_t0;)
+      dev::tc_fence_after();
+      uint32_t r[2][32];
+      dev::tmem_ld32(t_s + 64 * hf, r[0]);
+      dev::tmem_ld32(t_s + 64 * hf + 32, r[1]);
+      dev::tmem_ld_wait_regs(r[0], r[1]);
+      auto tile = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+        if (DIAG) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (64 * hf + i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
+        }
+        auto rv = [&](int i) { return __uint_as_float(r[i >> 5][i & 31]); };
+        float mx8[8];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(rv(k2), rv(8 + k2));
+#pragma unroll
+        for (int i = 16; i < 64; i += 16)
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmax3f(mx8[k2], rv(i + k2), rv(i + 8 + k2));
+        const float mxa = fmax3f(mx8[0], mx8[1], mx8[2]);
+        const float mxb = fmax3f(mx8[3], mx8[4], mx8[5]);
+        const float mxh = fmax3f(mxa, mxb, fmaxf(mx8[6], mx8[7]));
+        // row max across the two halves (parity-double-buffered slot: the
+        // partner has read slot j&1 before it passes the barrier of tile j+1)
+        const uint32_t par = (j & 1) * (2 * 2 * 128 * 4);
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xmine + par), "f"(mxh) : "memory");
+        named_bar(bar_id, 64);
+        float other;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xother + par) : "memory");
+        const float cand = fmaxf(m, fmaxf(mxh, other) * scale_log2);
+        const bool need = j == 0 || cand > m + kRescaleThreshold;
+        const bool any = __any_sync(0xffffffffu, need);  // same rows, same vote in both halves
+        float m_new = m, factor = 1.f;
+        if (any) {
+          m_new = cand;
+          factor = j == 0 ? 0.f : dev::ex2(m - m_new);
+        }
+        if (hf == 0 && any && j > 0) {
+          // O_g holds P(j-1)V(j-1) (PV_g(j-1) completed before s_full_g(j)
+          // fired); rescaled before this warp releases keys [0,64), which
+          // starts PV_g(j)
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            dev::tmem_ld32(t_o + c * 32, o);
+            dev::tmem_ld_wait_regs(o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+            dev::tmem_st32(t_o + c * 32, o);
+          }
+        }
+        uint64_t sum4[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {  // 16 column pairs per store
+          uint32_t p[16];
+#pragma unroll
+          for (int i = 16 * qq; i < 16 * qq + 16; ++i) {
+            const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                              __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
+                                      scale_log2, -m_new);
+            float a, b;
+            const int gi = 32 * hf + i;  // pair index within the row: same exponentials emulated as the pp kernel
+            if (EMU_EVERY > 0 && (gi % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
+              const uint64_t e2 = exp2_fma2(x2);
+              a = f2_lo(e2);
+              b = f2_hi(e2);
+            } else {
+              a = dev::ex2(f2_lo(x2));
+              b = dev::ex2(f2_hi(x2));
+            }
+            sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
+            p[i - 16 * qq] = dev::pack_bf16(a, b);
+          }
+          dev::tmem_st16(t_s + 64 * hf + 16 * qq, p);  // inside this warp's own S columns
+        }
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&p_full[2 * g + hf]);
+        FWD_PROF(pf[2] += clock64() - pf_t1;)
+        const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+        l = l * factor + (f2_lo(s01) + f2_hi(s01));
+        m = m_new;
+      };
+      if (j == qt)
+        tile(std::true_type{});
+      else
+        tile(std::false_type{});
+    }
+    FWD_PROF(if (pf_on) {
+      for (int k = 0; k < 4; ++k) atomicAdd(&g_fwd_prof[8 * g + k], static_cast<unsigned long long>(pf[k]));
+      atomicAdd(&g_fwd_prof[8 * g + 4], static_cast<unsigned long long>(n_my));
+    })
+    // epilogue: combine the two partial row sums, write O columns [64hf, 64hf+64) and the LSE
+    const uint32_t par = (n_my & 1) * (2 * 2 * 128 * 4);
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(xmine + par), "f"(l) : "memory");
+    named_bar(bar_id, 64);
+    float l_other;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(l_other) : "r"(xother + par) : "memory");
+    const float lt = hf == 0 ? l + l_other : l_other + l;  // same sum in both halves
+    dev::mbar_wait(&o_done[g], 0);  // committed once, after the group's last PV
+    dev::tc_fence_after();
+    const float inv = 1.f / lt;
+    __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D + 64 * hf;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      dev::tmem_ld32(t_o + 64 * hf + c * 32, o);
+      dev::tmem_ld_wait_regs(o);
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 u;
+        u.x = dev::pack_bf16(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
+        u.y = dev::pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
+        u.z = dev::pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
+        u.w = dev::pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
+        dst[i] = u;
+      }
+    }
+    if (hf == 0) lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(lt)) * kLn2;
     dev::tc_fence_before();
   }
   __syncthreads();
@@ -2712,18 +3194,49 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   // MEMO_ATTN_FWD_VARIANT: 0-3 one softmax warp per row (bit0 Q in TMEM, bit1
   // FMA exp2 share); 5-7 split rows (1/4, none, 1/8 FMA share); 8-12 ping-pong
   // with FMA share 1/3 (product), none, 1/8, 1/4, 1/2; 13 ping-pong without the
-  // two-half P release (the round-1 product)
+  // two-half P release (the round-1 product); 14, 15 ping-pong with share 1/6, 1/16;
+  // 16 ping-pong with no softmax math (NULL_SM: the MMA/TMA/TMEM ceiling, wrong output);
+  // 17-20 ping-pong with split rows (attn_fwd_pp2w_kernel), FMA share 1/3, 1/4, none, 1/8;
+  // 21-23 ping-pong without MMAs (NULL_MMA: the softmax-throughput ceiling, wrong output), share 1/3, none, 1/4;
+  // 24-26 ping-pong with the groups taking turns on the exponentials (SEQ), share 1/3, none, 1/4;
+  // 27 ping-pong with quarter P stores and the row sum after the release (QSTORE)
   const int v = abl_env("MEMO_ATTN_FWD_VARIANT", 8);
   if (v != 8) {
-    if (v >= 9 && a.D == 128 && a.S % (2 * TILE) == 0) {
+    if (v >= 17 && v <= 20 && a.D == 128 && a.S % (2 * TILE) == 0) {
+      static std::once_flag fw;
+      std::call_once(fw, [] {
+        for (auto k : {attn_fwd_pp2w_kernel<3>, attn_fwd_pp2w_kernel<4>, attn_fwd_pp2w_kernel<0>,
+                       attn_fwd_pp2w_kernel<8>})
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPp2wSmem::BYTES);
+      });
+      auto kern = v == 17 ? attn_fwd_pp2w_kernel<3> : v == 18 ? attn_fwd_pp2w_kernel<4>
+                : v == 19 ? attn_fwd_pp2w_kernel<0> : attn_fwd_pp2w_kernel<8>;
+      kern<<<dim3(a.S / (2 * TILE), a.H), PP2W_THREADS, FwdPp2wSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
+                                                                                     a.H, scale_log2);
+    } else if (v >= 9 && a.D == 128 && a.S % (2 * TILE) == 0) {
       static std::once_flag fa;
       std::call_once(fa, [] {
         for (auto k : {attn_fwd_pp_kernel<0>, attn_fwd_pp_kernel<8>, attn_fwd_pp_kernel<4>, attn_fwd_pp_kernel<2>,
-                       attn_fwd_pp_kernel<3, false>})
+                       attn_fwd_pp_kernel<3, false>, attn_fwd_pp_kernel<6>, attn_fwd_pp_kernel<16>,
+                       attn_fwd_pp_kernel<3, true, true>, attn_fwd_pp_kernel<3, true, false, true>,
+                       attn_fwd_pp_kernel<0, true, false, true>, attn_fwd_pp_kernel<4, true, false, true>,
+                       attn_fwd_pp_kernel<3, true, false, false, true, true>,
+                       attn_fwd_pp_kernel<0, true, false, false, true, true>,
+                       attn_fwd_pp_kernel<4, true, false, false, true, true>,
+                       attn_fwd_pp_kernel<3, true, false, false, false, true>})
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
       });
       auto kern = v == 9 ? attn_fwd_pp_kernel<0> : v == 10 ? attn_fwd_pp_kernel<8>
                 : v == 11 ? attn_fwd_pp_kernel<4> : v == 12 ? attn_fwd_pp_kernel<2>
+                : v == 14 ? attn_fwd_pp_kernel<6> : v == 15 ? attn_fwd_pp_kernel<16>
+                : v == 16 ? attn_fwd_pp_kernel<3, true, true>
+                : v == 21 ? attn_fwd_pp_kernel<3, true, false, true>
+                : v == 22 ? attn_fwd_pp_kernel<0, true, false, true>
+                : v == 23 ? attn_fwd_pp_kernel<4, true, false, true>
+                : v == 24 ? attn_fwd_pp_kernel<3, true, false, false, true, true>
+                : v == 25 ? attn_fwd_pp_kernel<0, true, false, false, true, true>
+                : v == 26 ? attn_fwd_pp_kernel<4, true, false, false, true, true>
+                : v == 27 ? attn_fwd_pp_kernel<3, true, false, false, false, true>
                 : attn_fwd_pp_kernel<3, false>;
       kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
                                                                           scale_log2);
@@ -2789,6 +3302,17 @@ cudaError_t attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   if (a.D == 64) return launch_bwd<64>(a, stream);
   return cudaErrorInvalidValue;
 }
+#ifdef MEMO_FWD_PROF
+extern "C" int memo_debug_fwd_prof(unsigned long long* out24, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out24, g_fwd_prof, 24 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[24] = {};
+    cudaMemcpyToSymbol(g_fwd_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 #ifdef MEMO_DKDV_PROF
 extern "C" int memo_debug_dkdv_prof(unsigned long long* out8, int reset) {
   cudaDeviceSynchronize();

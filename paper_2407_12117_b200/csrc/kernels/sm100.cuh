@@ -34,6 +34,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// Arrive and return the barrier state token: arithmetic on the token is
+// data-dependent on the arrive, so ptxas cannot schedule it above the arrive.
+__device__ __forceinline__ uint64_t mbar_arrive_token(uint64_t* bar) {
+  uint64_t st;
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 %0, [%1];" : "=l"(st) : "r"(smem_u32(bar))
+               : "memory");
+  return st;
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
                    smem_u32(bar)),

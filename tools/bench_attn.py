@@ -32,6 +32,8 @@ def bench(S, H, D, iters=5, bwd=False):
     flops = 2.0 * S * S * H * D  # causal half of 4*S^2*h
     out = {"S": S, "H": H, "D": D, "fwd_ms": ms, "fwd_tflops": flops / ms / 1e9}
     try:
+        if os.environ.get("MEMO_NO_FA2"):
+            raise RuntimeError("skipped (MEMO_NO_FA2)")
         from flash_attn import flash_attn_func
         qq, kk, vv = (t.view(1, S, H, D) for t in (q, k, v))
         flash_attn_func(qq, kk, vv, causal=True)
