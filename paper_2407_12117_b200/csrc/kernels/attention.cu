@@ -1170,6 +1170,7 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+#ifdef MEMO_ATTN_ABLATIONS  // split-row ping-pong forward (ablation build only)
 // ------------------------------------------------------- forward, ping-pong, split rows
 // The ping-pong schedule of attn_fwd_pp_kernel (two query tiles A/B per CTA,
 // TMEM S_A | S_B | O_A | O_B, one MMA warp alternating PV_A S_A PV_B S_B), with
@@ -1492,6 +1493,7 @@ __global__ void __launch_bounds__(PP2W_THREADS, 1)
     dev::tmem_dealloc(tmem, 512);
   }
 }
+#endif  // MEMO_ATTN_ABLATIONS
 
 // ============================================================== backward
 // ndelta[h][t] = -sum_d dO*O ; nlse2[h][t] = -lse * log2(e)  (the delta / lse2 workspace)
