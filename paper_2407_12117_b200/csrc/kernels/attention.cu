@@ -761,8 +761,14 @@ __device__ unsigned long long g_fwd_prof[24];
 // alone on its SMSP instead of both slowing each other down.
 // QSTORE (ablation): P in four quarters stored as packed, keys [0,64) released
 // after the third quarter, row sum after the release (measured 1-2 % slower).
+// LDSB: no tcgen05.wait::ld after the S loads.  ptxas scoreboards the
+// tcgen05.ld destination registers like any load's (CUTLASS's sm_100 kernels
+// issue no wait::ld at all), so the row max starts on the first 32 columns
+// while the other three loads are in flight.  Safe here because nothing
+// reuses S's columns before this thread's P stores, which depend on every
+// loaded value.  0.5-1 % at 128K, bitwise equal (LDSB = false: ablation 33).
 template <int EMU_EVERY, bool SPLIT_P = true, bool NULL_SM = false, bool NULL_MMA = false, bool SEQ = false,
-          bool QSTORE = false>
+          bool QSTORE = false, bool LDSB = true>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
@@ -934,7 +940,7 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t r[4][32];
 #pragma unroll
       for (int c = 0; c < 4; ++c) dev::tmem_ld32(t_s + c * 32, r[c]);
-      dev::tmem_ld_wait_regs(r[0], r[1], r[2], r[3]);
+      if (!LDSB) dev::tmem_ld_wait_regs(r[0], r[1], r[2], r[3]);
       bool any = false;
       float factor = 1.f;
       uint32_t p[64];
@@ -1987,7 +1993,11 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         dev::tmem_ld8(buf(b) + lane_off + 8 * ch, sr);
         dev::tmem_ld8(buf(b) + lane_off + 32 + 8 * ch, dr);
       }
-      dev::tmem_ld_wait_regs(sr, dr);
+      // COLS 16: no wait::ld, the consumers wait on the registers' scoreboard
+      // (this warp's P^T/dS^T stores depend on every loaded value, and nothing
+      // else reuses these columns first).  COLS 8 writes into other warps'
+      // columns behind a named barrier, which needs the loads complete.
+      if constexpr (COLS != 16) dev::tmem_ld_wait_regs(sr, dr);
       MEMO_PROF(if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[6], static_cast<unsigned long long>(clock64() - prof_t1));)
       uint32_t pp[COLS / 2], dd[COLS / 2];
       auto body = [&](auto diag_tag) {
@@ -2549,7 +2559,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           uint32_t sr[32], dr[32];
           dev::tmem_ld32(t_s + c * 32, sr);
           dev::tmem_ld32(t_dp + c * 32, dr);
-          dev::tmem_ld_wait_regs(sr, dr);
+          // no wait::ld: the consumers wait on the registers' scoreboard (the dS
+          // stores below depend on every loaded value, nothing reuses S/dP first)
           uint32_t dd[16];
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) {  // key pairs: FFMA2 / FADD2 / FMUL2
@@ -3201,7 +3212,9 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   // 17-20 ping-pong with split rows (attn_fwd_pp2w_kernel), FMA share 1/3, 1/4, none, 1/8;
   // 21-23 ping-pong without MMAs (NULL_MMA: the softmax-throughput ceiling, wrong output), share 1/3, none, 1/4;
   // 24-26 ping-pong with the groups taking turns on the exponentials (SEQ), share 1/3, none, 1/4;
-  // 27 ping-pong with quarter P stores and the row sum after the release (QSTORE)
+  // 27 ping-pong with quarter P stores and the row sum after the release (QSTORE);
+  // 28-31 ping-pong without the wait::ld after the S loads (LDSB), share 1/3, 1/8, none, 1/4;
+  // 32 LDSB + QSTORE, share 1/8; 33 the round-2 product before LDSB (wait::ld after the S loads)
   const int v = abl_env("MEMO_ATTN_FWD_VARIANT", 8);
   if (v != 8) {
     if (v >= 17 && v <= 20 && a.D == 128 && a.S % (2 * TILE) == 0) {
@@ -3225,7 +3238,13 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
                        attn_fwd_pp_kernel<3, true, false, false, true, true>,
                        attn_fwd_pp_kernel<0, true, false, false, true, true>,
                        attn_fwd_pp_kernel<4, true, false, false, true, true>,
-                       attn_fwd_pp_kernel<3, true, false, false, false, true>})
+                       attn_fwd_pp_kernel<3, true, false, false, false, true>,
+                       attn_fwd_pp_kernel<3, true, false, false, false, false, true>,
+                       attn_fwd_pp_kernel<8, true, false, false, false, false, true>,
+                       attn_fwd_pp_kernel<0, true, false, false, false, false, true>,
+                       attn_fwd_pp_kernel<4, true, false, false, false, false, true>,
+                       attn_fwd_pp_kernel<8, true, false, false, false, true, true>,
+                       attn_fwd_pp_kernel<3, true, false, false, false, false, false>})
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
       });
       auto kern = v == 9 ? attn_fwd_pp_kernel<0> : v == 10 ? attn_fwd_pp_kernel<8>
@@ -3239,6 +3258,12 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
                 : v == 25 ? attn_fwd_pp_kernel<0, true, false, false, true, true>
                 : v == 26 ? attn_fwd_pp_kernel<4, true, false, false, true, true>
                 : v == 27 ? attn_fwd_pp_kernel<3, true, false, false, false, true>
+                : v == 28 ? attn_fwd_pp_kernel<3, true, false, false, false, false, true>
+                : v == 29 ? attn_fwd_pp_kernel<8, true, false, false, false, false, true>
+                : v == 30 ? attn_fwd_pp_kernel<0, true, false, false, false, false, true>
+                : v == 31 ? attn_fwd_pp_kernel<4, true, false, false, false, false, true>
+                : v == 32 ? attn_fwd_pp_kernel<8, true, false, false, false, true, true>
+                : v == 33 ? attn_fwd_pp_kernel<3, true, false, false, false, false, false>
                 : attn_fwd_pp_kernel<3, false>;
       kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
                                                                           scale_log2);
