@@ -1203,7 +1203,10 @@ struct FwdPp2wSmem {
 };
 constexpr int PP2W_THREADS = 32 * 20;
 
-template <int EMU_EVERY>
+// SEQ: the groups take turns on the exponential phase (mbarriers per lane
+// quarter, 64 arrivals = the group's two warps), so a tile's softmax gets the
+// SMSP's MUFU/issue to itself: A(j) -> B(j) -> A(j+1) ...
+template <int EMU_EVERY, bool SEQ = false>
 __global__ void __launch_bounds__(PP2W_THREADS, 1)
     attn_fwd_pp2w_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                          const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
@@ -1225,6 +1228,8 @@ __global__ void __launch_bounds__(PP2W_THREADS, 1)
   uint64_t* p_full = bars + 11;  // [2 groups][2 key halves], one warpgroup each
   uint64_t* o_done = bars + 15;  // [2] per group
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* turn_ab = bars + 18;  // [4] per lane quarter: A's exponentials of tile j done
+  uint64_t* turn_ba = bars + 22;  // [4]: B's exponentials of tile j done
   const uint32_t xchg_s = dev::smem_u32(smem + L::X_OFF);
 
   const int n_pairs = S / (2 * TILE);
@@ -1249,6 +1254,10 @@ __global__ void __launch_bounds__(PP2W_THREADS, 1)
       dev::mbar_init(&p_full[2 * s2], 128);
       dev::mbar_init(&p_full[2 * s2 + 1], 128);
       dev::mbar_init(&o_done[s2], 1);
+    }
+    for (int q = 0; q < 4; ++q) {
+      dev::mbar_init(&turn_ab[q], 64);
+      dev::mbar_init(&turn_ba[q], 64);
     }
     dev::fence_barrier_init();
   }
@@ -1422,6 +1431,15 @@ __global__ void __launch_bounds__(PP2W_THREADS, 1)
             dev::tmem_st32(t_o + c * 32, o);
           }
         }
+        float neg_m = -m_new;
+        if (SEQ && (g == 1 ? j + 1 < n_my : j > 0)) {
+          // A(j) waits for B(j-1), B(j) for A(j) (B's last tile has no A(j));
+          // a clock read after the wait keeps ptxas from hoisting the exponentials
+          dev::mbar_wait(g == 0 ? &turn_ba[q4] : &turn_ab[q4], g == 0 ? (j - 1) & 1 : j & 1);
+          uint32_t c;
+          asm volatile("mov.u32 %0, %%clock;" : "=r"(c)::"memory");
+          neg_m += __uint_as_float(c & 0x80000000u) * 0.f;
+        }
         uint64_t sum4[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {  // 16 column pairs per store
@@ -1430,7 +1448,7 @@ __global__ void __launch_bounds__(PP2W_THREADS, 1)
           for (int i = 16 * qq; i < 16 * qq + 16; ++i) {
             const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
                                               __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
-                                      scale_log2, -m_new);
+                                      scale_log2, neg_m);
             float a, b;
             const int gi = 32 * hf + i;  // pair index within the row: same exponentials emulated as the pp kernel
             if (EMU_EVERY > 0 && (gi % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
@@ -1443,6 +1461,12 @@ __global__ void __launch_bounds__(PP2W_THREADS, 1)
             }
             sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
             p[i - 16 * qq] = dev::pack_bf16(a, b);
+          }
+          if (SEQ && qq == 1) {  // pass the turn once this warp's exponentials are done
+            if (g == 0)
+              dev::mbar_arrive(&turn_ab[q4]);
+            else if (j + 1 < n_my - 1)
+              dev::mbar_arrive(&turn_ba[q4]);
           }
           dev::tmem_st16(t_s + 64 * hf + 16 * qq, p);  // inside this warp's own S columns
         }
@@ -3214,18 +3238,23 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   // 24-26 ping-pong with the groups taking turns on the exponentials (SEQ), share 1/3, none, 1/4;
   // 27 ping-pong with quarter P stores and the row sum after the release (QSTORE);
   // 28-31 ping-pong without the wait::ld after the S loads (LDSB), share 1/3, 1/8, none, 1/4;
-  // 32 LDSB + QSTORE, share 1/8; 33 the round-2 product before LDSB (wait::ld after the S loads)
+  // 32 LDSB + QSTORE, share 1/8; 33 the round-2 product before LDSB (wait::ld after the S loads);
+  // 34-37 QSTORE (with LDSB), share 1/4, 1/6, 1/16, none;
+  // 38-41 split rows with the groups taking turns (attn_fwd_pp2w_kernel SEQ), share 1/4, 1/8, none, 1/16
   const int v = abl_env("MEMO_ATTN_FWD_VARIANT", 8);
   if (v != 8) {
-    if (v >= 17 && v <= 20 && a.D == 128 && a.S % (2 * TILE) == 0) {
+    if (((v >= 17 && v <= 20) || (v >= 38 && v <= 41)) && a.D == 128 && a.S % (2 * TILE) == 0) {
       static std::once_flag fw;
       std::call_once(fw, [] {
         for (auto k : {attn_fwd_pp2w_kernel<3>, attn_fwd_pp2w_kernel<4>, attn_fwd_pp2w_kernel<0>,
-                       attn_fwd_pp2w_kernel<8>})
+                       attn_fwd_pp2w_kernel<8>, attn_fwd_pp2w_kernel<4, true>, attn_fwd_pp2w_kernel<8, true>,
+                       attn_fwd_pp2w_kernel<0, true>, attn_fwd_pp2w_kernel<16, true>})
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPp2wSmem::BYTES);
       });
       auto kern = v == 17 ? attn_fwd_pp2w_kernel<3> : v == 18 ? attn_fwd_pp2w_kernel<4>
-                : v == 19 ? attn_fwd_pp2w_kernel<0> : attn_fwd_pp2w_kernel<8>;
+                : v == 19 ? attn_fwd_pp2w_kernel<0> : v == 20 ? attn_fwd_pp2w_kernel<8>
+                : v == 38 ? attn_fwd_pp2w_kernel<4, true> : v == 39 ? attn_fwd_pp2w_kernel<8, true>
+                : v == 40 ? attn_fwd_pp2w_kernel<0, true> : attn_fwd_pp2w_kernel<16, true>;
       kern<<<dim3(a.S / (2 * TILE), a.H), PP2W_THREADS, FwdPp2wSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S,
                                                                                      a.H, scale_log2);
     } else if (v >= 9 && a.D == 128 && a.S % (2 * TILE) == 0) {
@@ -3244,7 +3273,11 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
                        attn_fwd_pp_kernel<0, true, false, false, false, false, true>,
                        attn_fwd_pp_kernel<4, true, false, false, false, false, true>,
                        attn_fwd_pp_kernel<8, true, false, false, false, true, true>,
-                       attn_fwd_pp_kernel<3, true, false, false, false, false, false>})
+                       attn_fwd_pp_kernel<3, true, false, false, false, false, false>,
+                       attn_fwd_pp_kernel<4, true, false, false, false, true>,
+                       attn_fwd_pp_kernel<6, true, false, false, false, true>,
+                       attn_fwd_pp_kernel<16, true, false, false, false, true>,
+                       attn_fwd_pp_kernel<0, true, false, false, false, true>})
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
       });
       auto kern = v == 9 ? attn_fwd_pp_kernel<0> : v == 10 ? attn_fwd_pp_kernel<8>
@@ -3264,6 +3297,10 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
                 : v == 31 ? attn_fwd_pp_kernel<4, true, false, false, false, false, true>
                 : v == 32 ? attn_fwd_pp_kernel<8, true, false, false, false, true, true>
                 : v == 33 ? attn_fwd_pp_kernel<3, true, false, false, false, false, false>
+                : v == 34 ? attn_fwd_pp_kernel<4, true, false, false, false, true>
+                : v == 35 ? attn_fwd_pp_kernel<6, true, false, false, false, true>
+                : v == 36 ? attn_fwd_pp_kernel<16, true, false, false, false, true>
+                : v == 37 ? attn_fwd_pp_kernel<0, true, false, false, false, true>
                 : attn_fwd_pp_kernel<3, false>;
       kern<<<dim3(a.S / (2 * TILE), a.H), 384, FwdPpSmem::BYTES, stream>>>(mq, mk, mv, a.o, a.lse, a.S, a.H,
                                                                           scale_log2);
