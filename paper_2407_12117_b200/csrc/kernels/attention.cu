@@ -1816,7 +1816,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 // [2] compute warp 4 waiting for S/dP (tensor), [3] compute warp 4 busy per step,
 // [4] steps (MMA warp), [5] total kernel cycles of the MMA warp.
 #ifdef MEMO_DKDV_PROF
-__device__ unsigned long long g_dkdv_prof[8];
+__device__ unsigned long long g_dkdv_prof[16];
 #define MEMO_PROF(x) x
 #else
 #define MEMO_PROF(x)
@@ -1837,6 +1837,8 @@ constexpr int QSTEP = 32;  // queries per pipeline step
 template <int D>
 struct DkdvTmSmem {
   static constexpr int NC = D / 64;
+  static constexpr int CH_BYTES = CHUNK_BYTES;
+  static constexpr int STAGE_BYTES = NC * CHUNK_BYTES;
   static constexpr int TILE_BYTES = NC * CHUNK_BYTES;
   static constexpr int RQ_OFF = 0;                             // [KV_NS] Q tiles
   static constexpr int RD_OFF = KV_NS * TILE_BYTES;            // [KV_NS] dO tiles
@@ -1845,12 +1847,36 @@ struct DkdvTmSmem {
   static constexpr int BYTES = BAR_OFF + 256 + 1024;
 };
 
+// One-step stages (attn_bwd_dkdv_tm_kernel TS > 0): [TS] Q slices of QSTEP rows,
+// [TS] dO slices, [TS][lse2 32 | delta 32] f32.
+template <int D, int TSN>
+struct DkdvTsSmem {
+  static constexpr int NC = D / 64;
+  static constexpr int CH_BYTES = QSTEP * 128;             // one 64-col chunk of a QSTEP-row slice
+  static constexpr int STAGE_BYTES = NC * CH_BYTES;
+  static constexpr int TILE_BYTES = STAGE_BYTES;
+  static constexpr int RQ_OFF = 0;
+  static constexpr int RD_OFF = TSN * STAGE_BYTES;
+  static constexpr int VEC_OFF = 2 * TSN * STAGE_BYTES;
+  static constexpr int BAR_OFF = VEC_OFF + TSN * 256;
+  static constexpr int BYTES = BAR_OFF + 512 + 1024;
+};
+// Descriptor helpers for operand tiles whose 64-col chunks are CH bytes apart.
+template <int CH>
+__device__ __forceinline__ uint64_t kmajor_step_c(uint64_t d, int kk) {
+  return d + static_cast<uint64_t>(((kk >> 2) * CH + (kk & 3) * 32) >> 4);
+}
+template <int CH>
+__device__ __forceinline__ uint64_t mnmajor_base_c(uint32_t base) {
+  return dev::umma_desc_sw128(base, CH, 1024);
+}
+
 // WPQ: softmax-gradient warps per TMEM lane quarter (2: 16 query columns each;
 // 4: 8 columns each, compacted P/dS write-back behind a per-quarter named barrier).
 // EMU: every EMU-th column pair's exponentials run on the FMA pipe (exp2_fma)
 // instead of MUFU.EX2 (0: none).  The MUFU is the largest single item of the
 // compute warps' per-step critical path (tools/dkdv_prof.py).
-template <int D, int WPQ, int EMU = 0, bool SPLIT = false>
+template <int D, int WPQ, int EMU = 0, bool SPLIT = false, int TS = 0>
 __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     attn_bwd_dkdv_tm_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
                             const __grid_constant__ CUtensorMap map_q,
@@ -1858,9 +1884,12 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
                             const float* __restrict__ delta, __nv_bfloat16* __restrict__ dk,
                             __nv_bfloat16* __restrict__ dv, long long ld, const float2* __restrict__ rope,
                             long long pos0, int S, int H, float scale, float scale_log2) {
-  using L = DkdvTmSmem<D>;
+  // TS > 0: the Q/dO ring holds TS one-step (QSTEP-query) stages instead of
+  // KV_NS whole 128-query tiles (same shared memory), so a stage is released
+  // and refilled every step and the loads run TS-1 steps ahead.
+  using L = std::conditional_t<(TS > 0), DkdvTsSmem<D, (TS > 0 ? TS : 1)>, DkdvTmSmem<D>>;
   constexpr int NC = L::NC;
-  constexpr int NS = KV_NS;
+  constexpr int NS = TS > 0 ? TS : KV_NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1908,12 +1937,34 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   const uint32_t t_dv = tmem, t_dk = tmem + 128, t_k = tmem + 256, t_v = tmem + 320;
   auto buf = [&](int b) { return tmem + 384 + 64 * b; };
 
+  MEMO_PROF(__shared__ volatile long long pf_issue[4];)
   if (warp == 0) {
     if (lane == 0) {
+      if constexpr (TS > 0) {
+        for (int g = 0; g < n_g; ++g) {
+          const int st = g % NS;
+          const int q0 = (kt + (g >> 2)) * TILE + (g & 3) * QSTEP;  // first query of the step
+          dev::mbar_wait(&in_empty[st], ((g / NS) & 1) ^ 1);
+          dev::mbar_expect_tx(&in_full[st], 2 * L::STAGE_BYTES + 2 * QSTEP * 4);
+          for (int c = 0; c < NC; ++c) {
+            dev::tma_load_2d(smem + L::RQ_OFF + st * L::STAGE_BYTES + c * L::CH_BYTES, &map_q, &in_full[st],
+                             hh * D + c * 64, q0);
+            dev::tma_load_2d(smem + L::RD_OFF + st * L::STAGE_BYTES + c * L::CH_BYTES, &map_do, &in_full[st],
+                             hh * D + c * 64, q0);
+          }
+          float* vec = reinterpret_cast<float*>(smem + L::VEC_OFF + st * 256);
+          const long long off = static_cast<long long>(hh) * S + q0;
+          dev::bulk_load(vec, lse2 + off, QSTEP * 4, &in_full[st]);
+          dev::bulk_load(vec + 32, delta + off, QSTEP * 4, &in_full[st]);
+        }
+      } else
       for (int i = 0; i < n_q; ++i) {
         const int qt = kt + i, st = i % NS;
+        MEMO_PROF(long long pe = clock64();)
         dev::mbar_wait(&in_empty[st], ((i / NS) & 1) ^ 1);
+        MEMO_PROF(if (i >= NS) atomicAdd(&g_dkdv_prof[14], static_cast<unsigned long long>(clock64() - pe));)
         dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
+        MEMO_PROF(pf_issue[st] = clock64();)
         for (int c = 0; c < NC; ++c) {
           dev::tma_load_2d(smem + L::RQ_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q, &in_full[st],
                            hh * D + c * 64, qt * TILE);
@@ -1933,13 +1984,37 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       dev::mbar_wait_w(kv_ready, 0);
       dev::tc_fence_after();
       auto issue_sd = [&](int g) {
-        const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
-        if (qq == 0) {
+        const int i = g >> 2, qq = g & 3, b = g & 1;
+        const int st = TS > 0 ? g % NS : i % NS;
+        if constexpr (TS > 0) {
+          dev::mbar_wait_w(&in_full[st], (g / NS) & 1);
+          dev::tc_fence_after();
+        } else if (qq == 0) {
           MEMO_PROF(long long prof_b = clock64();)
           dev::mbar_wait_w(&in_full[st], (i / NS) & 1);
-          MEMO_PROF(if (lane == 0) atomicAdd(&g_dkdv_prof[0], static_cast<unsigned long long>(clock64() - prof_b));)
+          MEMO_PROF(if (lane == 0) {
+            const unsigned long long w = static_cast<unsigned long long>(clock64() - prof_b);
+            atomicAdd(&g_dkdv_prof[0], w);
+            if (i == 0) atomicAdd(&g_dkdv_prof[8], w);          // first tile of the CTA
+            if (i > 0 && w > 200) {
+              atomicAdd(&g_dkdv_prof[9], w);
+              atomicAdd(&g_dkdv_prof[10], 1ull);
+              atomicAdd(&g_dkdv_prof[12], static_cast<unsigned long long>(clock64() - pf_issue[st]));
+            }
+            if (i > 0) atomicAdd(&g_dkdv_prof[11], 1ull);
+          })
           dev::tc_fence_after();
         }
+        if constexpr (TS > 0) {
+          const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::STAGE_BYTES));
+          const uint64_t dod = kmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::STAGE_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            dev::mma_bf16_ts_w(buf(b), t_k + kk * 8, kmajor_step_c<L::CH_BYTES>(qd, kk), idesc_s, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            dev::mma_bf16_ts_w(buf(b) + 32, t_v + kk * 8, kmajor_step_c<L::CH_BYTES>(dod, kk), idesc_s, kk > 0);
+        } else {
         const uint32_t roff = qq * QSTEP * 128;  // 32 rows of 128 B inside every 64-col chunk
         const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
         const uint64_t dod = kmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
@@ -1949,20 +2024,23 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           dev::mma_bf16_ts_w(buf(b) + 32, t_v + kk * 8, kmajor_step(dod, kk), idesc_s, kk > 0);
+        }
         dev::mma_commit_w(&s_full[b]);
       };
       MEMO_PROF(long long prof_s = clock64();)
       issue_sd(0);
       for (int g = 0; g < n_g; ++g) {
         if (g + 1 < n_g) issue_sd(g + 1);
-        const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+        const int i = g >> 2, qq = g & 3, b = g & 1;
+        const int st = TS > 0 ? g % NS : i % NS;
         MEMO_PROF(long long prof_a = clock64();)
         dev::mbar_wait_w(&p_ready[b], (g >> 1) & 1);
         MEMO_PROF(if (lane == 0) atomicAdd(&g_dkdv_prof[1], static_cast<unsigned long long>(clock64() - prof_a));)
         dev::tc_fence_after();
-        const uint32_t roff = qq * QSTEP * 128;
-        const uint64_t qm = mnmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
-        const uint64_t dom = mnmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
+        const uint32_t roff = TS > 0 ? 0u : qq * QSTEP * 128;
+        const uint32_t sbytes = TS > 0 ? L::STAGE_BYTES : L::TILE_BYTES;
+        const uint64_t qm = mnmajor_base_c<L::CH_BYTES>(dev::smem_u32(smem + L::RQ_OFF + st * sbytes) + roff);
+        const uint64_t dom = mnmajor_base_c<L::CH_BYTES>(dev::smem_u32(smem + L::RD_OFF + st * sbytes) + roff);
 #pragma unroll
         for (int kk = 0; kk < QSTEP / 16; ++kk)
           dev::mma_bf16_ts_w(t_dv, buf(b) + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
@@ -1974,7 +2052,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         for (int kk = 0; kk < QSTEP / 16; ++kk)
           dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(qm, kk), idesc_g,
                              (g | kk) != 0);
-        if (qq == 3) dev::mma_commit_w(&in_empty[st]);
+        if (TS > 0 || qq == 3) dev::mma_commit_w(&in_empty[st]);
       }
       dev::mma_commit_w(fin);
       MEMO_PROF(if (lane == 0) { atomicAdd(&g_dkdv_prof[5], static_cast<unsigned long long>(clock64() - prof_s)); atomicAdd(&g_dkdv_prof[4], static_cast<unsigned long long>(n_g)); })
@@ -1992,11 +2070,13 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     dev::tc_fence_before();
     dev::mbar_arrive(kv_ready);
     for (int g = 0; g < n_g; ++g) {
-      const int i = g >> 2, qq = g & 3, st = i % NS, b = g & 1;
+      const int i = g >> 2, qq = g & 3, b = g & 1;
+      const int st = TS > 0 ? g % NS : i % NS;
       const bool diag = i == 0;
-      if (qq == 0) dev::mbar_wait(&in_full[st], (i / NS) & 1);
-      const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + COLS * ch) * 4;
-      const uint32_t dl = l2 + 512;
+      if (TS > 0 || qq == 0) dev::mbar_wait(&in_full[st], TS > 0 ? (g / NS) & 1 : (i / NS) & 1);
+      const uint32_t l2 = TS > 0 ? dev::smem_u32(smem + L::VEC_OFF + st * 256) + (COLS * ch) * 4
+                                 : dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + COLS * ch) * 4;
+      const uint32_t dl = l2 + (TS > 0 ? 128 : 512);
       // lse2 / delta of this step's columns, loaded before the S/dP wait so the
       // shared-memory latency is off the critical path
       float4 lvv[COLS / 4], dvv[COLS / 4];
@@ -3147,8 +3227,32 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   // MEMO_ATTN_DKDV_VARIANT: 1 K/V in shared memory, 2 four warps per lane
   // quarter, 3 P^T/dS^T behind separate barriers, 4/5 every 2nd/4th column
   // pair's exponentials on the FMA pipe, 7 P^T/dS^T decoupled from a single
-  // S^T/dP^T buffer (attn_bwd_dkdv_tm2_kernel: 231-232 vs 206-207 ms at 128K)
+  // S^T/dP^T buffer (attn_bwd_dkdv_tm2_kernel: 231-232 vs 206-207 ms at 128K),
+  // 8/9 one-step Q/dO stages (TS = 12 / 8)
   switch (abl_env("MEMO_ATTN_DKDV_VARIANT", 0)) {
+    case 8:
+    case 9: {
+      // one-step Q/dO stages (TS = 12 / 8): loads run TS-1 steps ahead
+      CUtensorMap mq32, mdo32;
+      if (!make_tma_2d_bf16(&mq32, a.q, h, a.S, h, 64, QSTEP) || !make_tma_2d_bf16(&mdo32, a.dout, h, a.S, h, 64, QSTEP))
+        return cudaErrorInvalidValue;
+      static std::once_flag fts;
+      std::call_once(fts, [] {
+        cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DkdvTsSmem<D, 12>::BYTES);
+        cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DkdvTsSmem<D, 8>::BYTES);
+      });
+      if (abl_env("MEMO_ATTN_DKDV_VARIANT", 0) == 8)
+        attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 12><<<grid, 32 * (4 + 8), DkdvTsSmem<D, 12>::BYTES, stream>>>(
+            a.k, a.v, mq32, mdo32, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+            scale_log2);
+      else
+        attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 8><<<grid, 32 * (4 + 8), DkdvTsSmem<D, 8>::BYTES, stream>>>(
+            a.k, a.v, mq32, mdo32, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+            scale_log2);
+      break;
+    }
     case 7:
       attn_bwd_dkdv_tm2_kernel<D><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
           a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
@@ -3378,11 +3482,11 @@ extern "C" int memo_debug_fwd_prof(unsigned long long* out24, int reset) {
 }
 #endif
 #ifdef MEMO_DKDV_PROF
-extern "C" int memo_debug_dkdv_prof(unsigned long long* out8, int reset) {
+extern "C" int memo_debug_dkdv_prof(unsigned long long* out16, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out8, g_dkdv_prof, 8 * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(out16, g_dkdv_prof, 16 * sizeof(unsigned long long));
   if (reset) {
-    unsigned long long z[8] = {};
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(g_dkdv_prof, z, sizeof(z));
   }
   return 0;

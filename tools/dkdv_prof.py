@@ -23,7 +23,7 @@ def main(S, H, D):
     ws = torch.empty((_abi.lib.memo_attn_bwd_workspace_bytes(S, H, D) + 3) // 4, device="cuda")
     dqkv = torch.empty(S, 3 * h, device="cuda", dtype=torch.bfloat16)
     P = lambda t: C.c_void_p(t.data_ptr())
-    buf = (C.c_ulonglong * 8)()
+    buf = (C.c_ulonglong * 16)()
     _abi.check(_abi.lib.memo_attn_fwd(P(q), P(k), P(v), P(o), P(lse), S, H, D, sc, None))
     for it in range(2):
         _abi.lib.memo_debug_dkdv_prof(buf, 1)
@@ -40,6 +40,15 @@ def main(S, H, D):
           "compute busy %.1f (TMEM load+wait %.1f, tcgen05.st wait %.1f), MMA-warp total %.1f "
           "(ideal tensor time 512)" % (buf[0] / steps, buf[1] / steps, buf[2] / steps, buf[3] / steps,
                                         buf[6] / steps, buf[7] / steps, buf[5] / steps))
+    tile_waits(buf)
+
+
+def tile_waits(buf):
+    print("Q/dO tile waits: first tile of each CTA %.0f cycles total (%.2f per step); later tiles: %d of %d waits "
+          "over 200 cycles, %.0f cycles each on average" % (buf[8], buf[8] / max(buf[4], 1), buf[10], buf[11],
+                                                            buf[9] / max(buf[10], 1)))
+    print("  for those waits, issue -> arrival %.0f cycles on average; TMA producer waited %.0f cycles per tile "
+          "for a free stage" % (buf[12] / max(buf[10], 1), buf[14] / max(buf[11], 1)))
 
 
 if __name__ == "__main__":
