@@ -40,6 +40,14 @@ __global__ void kern(float* out, long long* cyc) {
       } else if (OP == 6) {  // MUFU + FFMA2 interleaved (1:1)
         asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
         asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(v[i]));
+      } else if (OP == 8) {  // MUFU.EX2 on f16x2 (two exponentials per lane)
+        uint32_t r = __float_as_uint(a[i]);
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(r));
+        a[i] = __uint_as_float(r);
+      } else if (OP == 9) {  // MUFU.EX2 on bf16x2
+        uint32_t r = __float_as_uint(a[i]);
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(r));
+        a[i] = __uint_as_float(r);
       } else if (OP == 7) {  // MUFU + FMNMX3 + F2FP (1:1:1)
         asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
         uint32_t r;
@@ -90,6 +98,8 @@ int main() {
     run<5>("FFMA", w, out, cyc, n_sm);
     run<6>("EX2+FFMA2", w, out, cyc, n_sm);
     run<7>("EX2+F2FP+FMNMX3+FFMA", w, out, cyc, n_sm);
+    run<8>("EX2.F16x2", w, out, cyc, n_sm);
+    run<9>("EX2.BF16x2", w, out, cyc, n_sm);
   }
   return 0;
 }
