@@ -419,8 +419,9 @@ def main():
         t_layer = tt.item()
     torch.cuda.synchronize()
     free0, _ = torch.cuda.mem_get_info()
-    # single-GPU step as one CUDA graph (captured on the second step, replayed after)
-    use_graph = 1 if (cfg.tp_degree == 1 and not args.no_graph) else 0
+    # the step as one CUDA graph (captured on the second step, replayed after): single GPU,
+    # and SP+TP over CUDA-IPC peer memory, whose signals the executor rebases per replay
+    use_graph = 1 if (not args.no_graph and (cfg.tp_degree == 1 or (tp_spec is not None and tp_spec[0] == KIND_IPC))) else 0
     ex = Executor(cfg, hw, tp=tp_spec, alpha=forced_alpha, t_layer=t_layer, op_timing=1, cuda_graph=use_graph)
     connect(ex)
     free1, _ = torch.cuda.mem_get_info()

@@ -329,6 +329,9 @@ int memo_exec_create_tp(const memo_model_config* cfg, const memo_hardware_config
 int memo_exec_peer_handle(memo_exec* ctx, void* out, size_t cap, size_t* len);
 /* kind 2 bootstrap: all ranks' handles concatenated in rank order (t * len bytes). */
 int memo_exec_peer_connect(memo_exec* ctx, const void* all, size_t bytes);
+/* kind 2 diagnostics: this rank's signal flag page (uint64 [channel][source rank], the
+ * signal count each peer has posted on each channel), synchronously; *len = values copied. */
+int memo_exec_peer_flags(memo_exec* ctx, uint64_t* out, size_t n, size_t* len);
 
 /* Synchronous copy of a named tensor (as memo_exec_tensor) into host memory. */
 int memo_exec_read(memo_exec* ctx, const char* name, int32_t layer, void* host, size_t bytes);

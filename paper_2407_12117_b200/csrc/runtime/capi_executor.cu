@@ -129,6 +129,15 @@ extern "C" int memo_exec_peer_connect(memo_exec* ctx, const void* all, size_t by
   });
 }
 
+extern "C" int memo_exec_peer_flags(memo_exec* ctx, uint64_t* out, size_t n, size_t* len) {
+  return guard([&] {
+    if (!ctx || !out || !len) throw memo::ConfigError("null argument");
+    memo::Comm* c = ctx->ex->comm();
+    if (!c || c->handle_bytes() == 0) throw memo::ConfigError("executor has no IPC peer communicator (kind 2)");
+    *len = c->read_flags(out, n);
+  });
+}
+
 extern "C" int memo_exec_create(const memo_model_config* cfg, const memo_hardware_config* hw,
                                 const memo_exec_options* o, memo_exec** out) {
   return guard([&] {

@@ -62,6 +62,19 @@ class Comm {
   // issued on one stream (device order == host order).
   virtual void signal(int /*dst*/, int /*ch*/, cudaStream_t /*st*/) {}
   virtual void wait(int /*src*/, int /*ch*/, cudaStream_t /*st*/) {}
+  // CUDA-graph support.  graph_capturable(): every collective and signal/wait
+  // is pure stream work (no host rendezvous), so a step can be captured once
+  // and replayed.  The hooks bracket the capture of one step and precede every
+  // replay k = 0, 1, ...: the IPC backend's signal values and stream waits are
+  // absolute counters, so replay k rebases them by k x (the captured step's
+  // signals per channel) in the instantiated graph.
+  virtual bool graph_capturable() const { return false; }
+  virtual void capture_begin() {}
+  virtual void capture_end(cudaGraph_t /*g*/) {}
+  virtual void before_replay(cudaGraphExec_t /*x*/, long long /*k*/) {}
+  // IPC backend: this rank's flag page ([channel][source rank] signal counts),
+  // synchronously (tests: a replayed graph must advance them like eager steps).
+  virtual size_t read_flags(uint64_t* /*out*/, size_t /*n*/) const { return 0; }
   // IPC bootstrap (multi-process peer backend): export this rank's handle
   // after attach, then connect with every rank's handle (rank order).
   virtual size_t handle_bytes() const { return 0; }

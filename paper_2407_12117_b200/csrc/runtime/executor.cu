@@ -108,8 +108,9 @@ Executor::Executor(const ModelConfig& cfg_in, const HardwareConfig& hw, const Ex
   d_.n = static_cast<int>(cfg_.n_layers);
   d_.t = static_cast<int>(cfg_.tp_degree);
   d_.r = comm_ ? comm_->rank() : 0;
-  if (opt_.cuda_graph && d_.t > 1)
-    throw ConfigError("cuda_graph: the SP+TP communicators synchronise on the host; capture needs tp_degree 1");
+  if (opt_.cuda_graph && d_.t > 1 && !(comm_ && comm_->graph_capturable()))
+    throw ConfigError("cuda_graph at tp_degree > 1 needs a stream-only communicator (CUDA-IPC peer memory); "
+                      "the loopback and in-process peer groups rendezvous on the host");
   if (d_.t > 1 && (!comm_ || comm_->size() != d_.t) && !opt_.dry_run)
     throw ConfigError("tp_degree > 1 needs a communicator of that size");
   if (d_.h % d_.H || (d_.D != 64 && d_.D != 128)) throw ConfigError("head_dim must be 64 or 128");
@@ -1478,7 +1479,9 @@ void Executor::step_resident() {
     record_step();
     return;
   }
+  const bool tp = d_.t > 1 && comm_;
   if (!graph_exec_ && eager_done_) {
+    if (tp) comm_->capture_begin();
     G(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
     capturing_ = true;
     try {
@@ -1492,9 +1495,14 @@ void Executor::step_resident() {
     }
     G(cudaStreamEndCapture(cs_, &graph_));
     capturing_ = false;
+    if (tp) comm_->capture_end(graph_);
     G(cudaGraphInstantiate(&graph_exec_, graph_, 0));
+    replays_ = 0;
   }
   if (graph_exec_) {
+    // SP+TP: the signal values / wait thresholds of this replay (IPC backend)
+    if (tp) comm_->before_replay(graph_exec_, replays_);
+    ++replays_;
     G(cudaGraphLaunch(graph_exec_, cs_));
     return;
   }
@@ -1543,6 +1551,10 @@ void Executor::record_step() {
   G(cudaEventRecord(ev_join_ps_, ps_));
   G(cudaStreamWaitEvent(cs_, ev_join_os_, 0));
   G(cudaStreamWaitEvent(cs_, ev_join_ps_, 0));
+  if (xs_) {  // SP+TP: the collectives' side stream (its last signals) joins too
+    G(cudaEventRecord(ev_xs2cs_, xs_));
+    G(cudaStreamWaitEvent(cs_, ev_xs2cs_, 0));
+  }
   mark(0, 99, -1, true);  // step end marker
 }
 

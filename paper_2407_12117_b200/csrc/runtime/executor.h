@@ -220,6 +220,7 @@ class Executor {
   bool eager_done_ = false, capturing_ = false;
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
+  long long replays_ = 0;  // graph launches since the capture (SP+TP rebasing)
   std::vector<cudaEvent_t> ev_fwd_done_, ev_bwd_done_, ev_off_done_, ev_off_x_, ev_pre_mand_, ev_pre_done_;
   struct Mark {
     int stream, kind, layer;

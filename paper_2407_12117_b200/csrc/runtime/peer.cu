@@ -218,18 +218,30 @@ class PeerComm : public Comm {
 
 // ------------------------------------------------------------------ IPC (multi-process)
 typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*NodeTypeFn)(CUgraphNode, CUgraphNodeType*);
+typedef CUresult (*MemOpGetFn)(CUgraphNode, CUDA_BATCH_MEM_OP_NODE_PARAMS*);
+typedef CUresult (*MemOpExecSetFn)(CUgraphExec, CUgraphNode, const CUDA_BATCH_MEM_OP_NODE_PARAMS*);
 struct StreamMemOps {
   StreamValueFn wait = nullptr;
+  NodeTypeFn node_type = nullptr;          // the graph-replay rebasing (IpcComm::capture_end)
+  MemOpGetFn memop_get = nullptr;
+  MemOpExecSetFn memop_exec_set = nullptr;
 };
 const StreamMemOps& mem_ops() {
   static StreamMemOps ops;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      ops.wait = reinterpret_cast<StreamValueFn>(p);
+    auto get = [](const char* name) -> void* {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        return p;
+      return nullptr;
+    };
+    ops.wait = reinterpret_cast<StreamValueFn>(get("cuStreamWaitValue64"));
+    ops.node_type = reinterpret_cast<NodeTypeFn>(get("cuGraphNodeGetType"));
+    ops.memop_get = reinterpret_cast<MemOpGetFn>(get("cuGraphBatchMemOpNodeGetParams"));
+    ops.memop_exec_set = reinterpret_cast<MemOpExecSetFn>(get("cuGraphExecBatchMemOpNodeSetParams"));
   });
   return ops;
 }
@@ -308,12 +320,141 @@ class IpcComm final : public PeerComm {
       throw std::runtime_error("cuStreamWaitValue64 failed");
   }
 
+  // ---- CUDA graphs.  A captured step bakes each signal's value and each
+  // stream wait's threshold; replay k of the step must use those plus
+  // k x (the step's signals on that channel).  capture_end finds the signal
+  // kernel nodes and the wait-value memop nodes, maps each to its channel by
+  // its flag address, and before_replay rewrites them in the executable graph
+  // (plain node-parameter updates: no re-instantiation, no host-device sync).
+  size_t read_flags(uint64_t* out, size_t n) const override {
+    const size_t m = std::min(n, kFlagBytes / 8);
+    if (!flags_ || m == 0) return 0;
+    cuda_ck(cudaDeviceSynchronize(), "sync(flags)");
+    cuda_ck(cudaMemcpy(out, flags_, m * 8, cudaMemcpyDeviceToHost), "read flags");
+    return m;
+  }
+  bool graph_capturable() const override {
+    return mem_ops().node_type && mem_ops().memop_get && mem_ops().memop_exec_set;
+  }
+  void capture_begin() override {
+    std::memcpy(sent0_, sent_, sizeof(sent_));
+    std::memcpy(expect0_, expect_, sizeof(expect_));
+    sig_nodes_.clear();
+    wait_nodes_.clear();
+  }
+  void capture_end(cudaGraph_t g) override {
+    for (int c = 0; c < kPeerChannels; ++c)
+      for (int k = 0; k < kMaxPeers; ++k) {
+        dsent_[c][k] = sent_[c][k] - sent0_[c][k];
+        dexpect_[c][k] = expect_[c][k] - expect0_[c][k];
+      }
+    size_t n = 0;
+    cuda_ck(cudaGraphGetNodes(g, nullptr, &n), "graph nodes");
+    std::vector<cudaGraphNode_t> nodes(n);
+    cuda_ck(cudaGraphGetNodes(g, nodes.data(), &n), "graph nodes");
+    for (auto nd : nodes) {
+      CUgraphNodeType ty;
+      if (mem_ops().node_type(reinterpret_cast<CUgraphNode>(nd), &ty) != CUDA_SUCCESS)
+        throw std::runtime_error("cuGraphNodeGetType failed");
+      if (ty == CU_GRAPH_NODE_TYPE_KERNEL) {
+        cudaKernelNodeParams kp{};
+        cuda_ck(cudaGraphKernelNodeGetParams(nd, &kp), "kernel node params");
+        if (kp.func != reinterpret_cast<void*>(peer_signal_kernel)) continue;
+        SigNode sn;
+        sn.node = nd;
+        sn.p = kp;
+        sn.flag = *static_cast<unsigned long long**>(kp.kernelParams[0]);
+        sn.v0 = *static_cast<unsigned long long*>(kp.kernelParams[1]);
+        sn.delta = channel_delta(reinterpret_cast<const char*>(sn.flag), true);
+        sig_nodes_.push_back(sn);
+      } else if (ty == CU_GRAPH_NODE_TYPE_BATCH_MEM_OP) {
+        CUDA_BATCH_MEM_OP_NODE_PARAMS mp{};
+        if (mem_ops().memop_get(reinterpret_cast<CUgraphNode>(nd), &mp) != CUDA_SUCCESS)
+          throw std::runtime_error("cuGraphBatchMemOpNodeGetParams failed");
+        WaitNode wn;
+        wn.node = nd;
+        wn.p = mp;
+        wn.ops.assign(mp.paramArray, mp.paramArray + mp.count);
+        for (const auto& op : wn.ops) {
+          if (op.operation != CU_STREAM_MEM_OP_WAIT_VALUE_64)
+            throw std::runtime_error("graph capture: unexpected stream memory operation");
+          wn.v0.push_back(op.waitValue.value64);
+          wn.delta.push_back(channel_delta(reinterpret_cast<const char*>(op.waitValue.address), false));
+        }
+        wait_nodes_.push_back(std::move(wn));
+      }
+    }
+  }
+  void before_replay(cudaGraphExec_t x, long long k) override {
+    if (k > 0) {
+      for (auto& sn : sig_nodes_) {
+        unsigned long long* flag = sn.flag;
+        unsigned long long v = sn.v0 + static_cast<unsigned long long>(k) * sn.delta;
+        void* args[2] = {&flag, &v};
+        cudaKernelNodeParams kp = sn.p;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        cuda_ck(cudaGraphExecKernelNodeSetParams(x, sn.node, &kp), "rebase signal node");
+      }
+      for (auto& wn : wait_nodes_) {
+        std::vector<CUstreamBatchMemOpParams> ops = wn.ops;
+        for (size_t i = 0; i < ops.size(); ++i)
+          ops[i].waitValue.value64 = wn.v0[i] + static_cast<uint64_t>(k) * wn.delta[i];
+        CUDA_BATCH_MEM_OP_NODE_PARAMS mp = wn.p;
+        mp.paramArray = ops.data();
+        if (mem_ops().memop_exec_set(reinterpret_cast<CUgraphExec>(x), reinterpret_cast<CUgraphNode>(wn.node), &mp) !=
+            CUDA_SUCCESS)
+          throw std::runtime_error("cuGraphExecBatchMemOpNodeSetParams failed");
+      }
+    }
+    // the host counters continue after replay k as if k + 1 steps had been recorded eagerly
+    for (int c = 0; c < kPeerChannels; ++c)
+      for (int j = 0; j < kMaxPeers; ++j) {
+        sent_[c][j] = sent0_[c][j] + static_cast<uint64_t>(k + 1) * dsent_[c][j];
+        expect_[c][j] = expect0_[c][j] + static_cast<uint64_t>(k + 1) * dexpect_[c][j];
+      }
+  }
+
  private:
   IpcHandle h_{};
   char* flags_ = nullptr;
   char* peer_flags_[kMaxPeers] = {};
   uint64_t sent_[kPeerChannels][kMaxPeers] = {};
   uint64_t expect_[kPeerChannels][kMaxPeers] = {};
+  // graph replay rebasing (capture_begin / capture_end / before_replay)
+  struct SigNode {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams p;
+    unsigned long long* flag;
+    unsigned long long v0, delta;
+  };
+  struct WaitNode {
+    cudaGraphNode_t node;
+    CUDA_BATCH_MEM_OP_NODE_PARAMS p;
+    std::vector<CUstreamBatchMemOpParams> ops;
+    std::vector<uint64_t> v0, delta;
+  };
+  std::vector<SigNode> sig_nodes_;
+  std::vector<WaitNode> wait_nodes_;
+  uint64_t sent0_[kPeerChannels][kMaxPeers] = {}, expect0_[kPeerChannels][kMaxPeers] = {};
+  uint64_t dsent_[kPeerChannels][kMaxPeers] = {}, dexpect_[kPeerChannels][kMaxPeers] = {};
+  // signals per step on the channel a flag address belongs to: a peer's page
+  // (outgoing signal: [channel][this rank] on peer k) or this rank's own page
+  // (incoming wait: [channel][source rank])
+  uint64_t channel_delta(const char* addr, bool outgoing) const {
+    for (int k = 0; k < size_; ++k) {
+      const char* page = outgoing ? peer_flags_[k] : flags_;
+      if (!page || addr < page || addr >= page + kFlagBytes) continue;
+      const size_t slot = static_cast<size_t>(addr - page) / 8;
+      const int ch = static_cast<int>(slot / kMaxPeers), who = static_cast<int>(slot % kMaxPeers);
+      if (outgoing) {
+        if (who != rank_) continue;
+        return dsent_[ch][k];
+      }
+      return dexpect_[ch][who];
+    }
+    throw std::runtime_error("graph capture: a signal/wait address outside the flag pages");
+  }
 };
 
 // ------------------------------------------------------------------ local (threads on one GPU)

@@ -49,6 +49,7 @@ lib.memo_exec_stream.argtypes = [C.c_void_p]
 lib.memo_exec_destroy.argtypes = [C.c_void_p]
 lib.memo_exec_peer_handle.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
 lib.memo_exec_peer_connect.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+lib.memo_exec_peer_flags.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(C.c_size_t)]
 
 
 def default_options() -> ExecOptionsC:
@@ -98,6 +99,13 @@ class Executor:
         """Map every rank's allocation (handles in rank order, kind 2)."""
         blob = b"".join(handles)
         check(lib.memo_exec_peer_connect(self._h, C.c_char_p(blob), C.c_size_t(len(blob))))
+
+    def peer_flags(self):
+        """This rank's IPC signal flag page: signal counts per [channel][source rank] (kind 2)."""
+        buf = (C.c_uint64 * 64)()
+        n = C.c_size_t()
+        check(lib.memo_exec_peer_flags(self._h, buf, C.c_size_t(64), C.byref(n)))
+        return [int(buf[i]) for i in range(n.value)]
 
     def close(self):
         if self._h:

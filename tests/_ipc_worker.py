@@ -32,7 +32,7 @@ def main():
         dist.all_gather_object(handles, ex.peer_handle())
         ex.peer_connect(handles)
         losses = [ex.step(toks, labels) for _ in range(spec.get("steps", 1))]
-        out = {"loss": np.array(losses, dtype=np.float32)}
+        out = {"loss": np.array(losses, dtype=np.float32), "peer_flags": np.array(ex.peer_flags(), dtype=np.uint64)}
         for name, layer, _, _ in O.layout(ocfg):
             out[f"{name}:{layer}"] = ex.read("grad/" + name, layer)
     dist.barrier()
