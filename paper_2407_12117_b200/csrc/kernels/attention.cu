@@ -64,6 +64,15 @@ __device__ __forceinline__ uint64_t mnmajor_base(uint32_t base) {
 __device__ __forceinline__ uint64_t kmajor_step(uint64_t d, int kk) {
   return d + static_cast<uint64_t>(((kk >> 2) * CHUNK_BYTES + (kk & 3) * 32) >> 4);
 }
+// Descriptor helpers for operand tiles whose 64-col chunks are CH bytes apart.
+template <int CH>
+__device__ __forceinline__ uint64_t kmajor_step_c(uint64_t d, int kk) {
+  return d + static_cast<uint64_t>(((kk >> 2) * CH + (kk & 3) * 32) >> 4);
+}
+template <int CH>
+__device__ __forceinline__ uint64_t mnmajor_base_c(uint32_t base) {
+  return dev::umma_desc_sw128(base, CH, 1024);
+}
 // MN-major tile: 128 K-rows of 128 B per 64-wide MN chunk; k-step of 16 rows.
 __device__ __forceinline__ uint64_t mnmajor_step(uint64_t d, int kk) {
   return d + static_cast<uint64_t>((kk * 2048) >> 4);
@@ -1176,6 +1185,315 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+#ifdef MEMO_ATTN_ABLATIONS  // CTA-pair ping-pong forward (ablation build only)
+// ------------------------------------------------- forward, ping-pong over a CTA pair
+// attn_fwd_pp_kernel's schedule on a CTA pair (cta_group::2): the pair holds
+// four query tiles (CTA r, group g -> tile 4q + 2g + r) and every MMA spans
+// both CTAs (M = 256).  S_g = Q_g K_j^T reads each CTA's own Q rows and half
+// of K_j (keys [64r, 64r+64)) from that CTA's shared memory; O_g += P_g V_j
+// reads P from each CTA's TMEM and half of V_j (head-dim columns [64r, 64r+64)).
+// Per SM that is 96 instead of 128 B/cycle of operand reads for S and 32
+// instead of 64 for PV, and half the K/V TMA bytes: the one-CTA kernel's S
+// runs at the 128 B/cycle shared-memory cap (tools/ubench_mma.cu).  The
+// leader CTA issues the MMAs; both CTAs' softmax warps release P to barriers
+// in the leader.  A group's two tiles need different key ranges (4q+2g+1 vs
+// +2): the lower tile's last key tile is fully masked and only writes P = 0.
+// Measured (ablation variants 42/44): bitwise equal to attn_fwd_pp_kernel,
+// 131.9 ms at 128K against 111.4 ms -- both CTAs' softmax must release P
+// before each pair MMA, and the cross-CTA arrivals lengthen the S -> P -> PV
+// chain -- while its MMA-side ceiling (P = 0) is the same 95 ms as the
+// one-CTA kernel's: the shared-memory operand rate was not what bounds it.
+struct FwdPairSmem {
+  static constexpr int Q_BYTES = 2 * CHUNK_BYTES;   // one 128-row Q tile, D = 128
+  static constexpr int KV_BYTES = CHUNK_BYTES;      // half a K tile (64 rows x 128) / half a V tile (128 x 64)
+  static constexpr int STAGES = 3;
+  static constexpr int QA_OFF = 0;
+  static constexpr int QB_OFF = Q_BYTES;
+  static constexpr int K_OFF = 2 * Q_BYTES;
+  static constexpr int V_OFF = K_OFF + STAGES * KV_BYTES;
+  static constexpr int BAR_OFF = V_OFF + STAGES * KV_BYTES;
+  static constexpr int BYTES = BAR_OFF + 256 + 1024;
+};
+
+template <int EMU_EVERY, bool NULL_SM = false>  // NULL_SM (ablation): P = 0 everywhere, the MMA-side ceiling
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k64,
+                         const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
+                         float* __restrict__ lse, int S, int H, float scale_log2) {
+  constexpr int D = 128;
+  using L = FwdPairSmem;
+  constexpr int NST = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars + 0;                 // leader: both CTAs' Q tiles
+  uint64_t* k_full = bars + 1;                 // [NST] leader: both halves of K_j
+  uint64_t* k_empty = k_full + NST;            // [NST] each CTA (leader's multicast commit)
+  uint64_t* v_full = k_empty + NST;            // [NST] leader
+  uint64_t* v_empty = v_full + NST;            // [NST] each CTA
+  uint64_t* s_full = v_empty + NST;            // [2] each CTA
+  uint64_t* p_full = s_full + 2;               // [2 groups][2 key halves] leader, 256 arrivals
+  uint64_t* o_done = p_full + 4;               // [2] each CTA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const uint32_t rank = dev::cluster_ctarank();
+  const int n_quads = S / (4 * TILE);
+  const int quad = n_quads - 1 - static_cast<int>(blockIdx.x >> 1);  // heavy quads first
+  const int hh = blockIdx.y;
+  const int nA = 4 * quad + 2;  // key tiles of group A (its upper tile 4q+1 is diagonal at nA-1)
+  const int n_kv = 4 * quad + 4;
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_k64);
+    dev::tma_prefetch_desc(&map_v);
+    dev::mbar_init(q_full, 1);
+    for (int s2 = 0; s2 < NST; ++s2) {
+      dev::mbar_init(&k_full[s2], 1);
+      dev::mbar_init(&k_empty[s2], 1);
+      dev::mbar_init(&v_full[s2], 1);
+      dev::mbar_init(&v_empty[s2], 1);
+    }
+    for (int g = 0; g < 2; ++g) {
+      dev::mbar_init(&s_full[g], 1);
+      dev::mbar_init(&p_full[2 * g], 256);
+      dev::mbar_init(&p_full[2 * g + 1], 256);
+      dev::mbar_init(&o_done[g], 1);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc_cg2(tmem_slot, 512);
+  dev::tc_fence_before();
+  dev::cluster_sync();  // both CTAs' barriers initialised before any remote arrival
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (warp == 0) {
+      if (lane == 0) {
+        // ---- TMA producer (both CTAs): own Q tiles, own halves of K_j and V_j,
+        // completion on the leader's barriers
+        const uint32_t qf = dev::mapa(dev::smem_u32(q_full), 0);
+        if (rank == 0) dev::mbar_expect_tx(q_full, 4 * L::Q_BYTES);
+        for (int g = 0; g < 2; ++g)
+          for (int c = 0; c < 2; ++c)
+            dev::tma_load_2d_cg2(smem + (g ? L::QB_OFF : L::QA_OFF) + c * CHUNK_BYTES, &map_q, qf,
+                                 hh * D + c * 64, (4 * quad + 2 * g + static_cast<int>(rank)) * TILE);
+        for (int j = 0; j < n_kv; ++j) {
+          const int st = j % NST;
+          const uint32_t ph = (j / NST) & 1;
+          dev::mbar_wait(&k_empty[st], ph ^ 1);
+          if (rank == 0) dev::mbar_expect_tx(&k_full[st], 2 * L::KV_BYTES);
+          for (int c = 0; c < 2; ++c)  // keys [64 rank, +64) of K_j, both 64-col chunks
+            dev::tma_load_2d_cg2(smem + L::K_OFF + st * L::KV_BYTES + c * (L::KV_BYTES / 2), &map_k64,
+                                 dev::mapa(dev::smem_u32(&k_full[st]), 0), hh * D + c * 64,
+                                 j * TILE + static_cast<int>(rank) * 64);
+          dev::mbar_wait(&v_empty[st], ph ^ 1);
+          if (rank == 0) dev::mbar_expect_tx(&v_full[st], 2 * L::KV_BYTES);
+          // head-dim columns [64 rank, +64) of V_j, all 128 keys
+          dev::tma_load_2d_cg2(smem + L::V_OFF + st * L::KV_BYTES, &map_v, dev::mapa(dev::smem_u32(&v_full[st]), 0),
+                               hh * D + static_cast<int>(rank) * 64, j * TILE);
+        }
+      }
+    } else if (warp == 1 && rank == 0) {
+      // ---- MMA issuer (leader only; whole warp converged, elect.sync issues)
+      constexpr uint32_t idesc_s = dev::idesc_bf16_f32(256, 128, false, false);
+      constexpr uint32_t idesc_o = dev::idesc_bf16_f32(256, D, false, true);
+      const uint64_t qd[2] = {kmajor_base(dev::smem_u32(smem + L::QA_OFF)),
+                              kmajor_base(dev::smem_u32(smem + L::QB_OFF))};
+      dev::mbar_wait_cluster_w(q_full, 0);
+      dev::tc_fence_after();
+      auto issue_s = [&](int g, int j) {  // S_g(j), both CTAs' rows
+        const int st = j % NST;
+        if (g == 0 || j == nA) {
+          dev::mbar_wait_cluster_w(&k_full[st], (j / NST) & 1);
+          dev::tc_fence_after();
+        }
+        const uint64_t kd = kmajor_base(dev::smem_u32(smem + L::K_OFF + st * L::KV_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          dev::mma2_bf16_ss_w(tmem + g * 128, kmajor_step(g ? qd[1] : qd[0], kk),
+                              kmajor_step_c<L::KV_BYTES / 2>(kd, kk), idesc_s, kk > 0);
+        dev::mma2_commit_mc_w(&s_full[g], 0x3);
+        if (g == 1) dev::mma2_commit_mc_w(&k_empty[st], 0x3);  // B is the last reader of K_j
+      };
+      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j, one key half at a time
+        const int st = j % NST;
+        dev::mbar_wait_cluster_w(&p_full[2 * g], j & 1);
+        if (g == 0 || j == nA) dev::mbar_wait_cluster_w(&v_full[st], (j / NST) & 1);
+        dev::tc_fence_after();
+        const uint64_t vd = mnmajor_base(dev::smem_u32(smem + L::V_OFF + st * L::KV_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < TILE / 32; ++kk)
+          dev::mma2_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o,
+                              (j | kk) != 0);
+        dev::mbar_wait_cluster_w(&p_full[2 * g + 1], j & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int kk = TILE / 32; kk < TILE / 16; ++kk)
+          dev::mma2_bf16_ts_w(tmem + 256 + g * D, tmem + g * 128 + kk * 8, mnmajor_step(vd, kk), idesc_o, true);
+        if (j == (g ? n_kv - 1 : nA - 1)) dev::mma2_commit_mc_w(&o_done[g], 0x3);
+        if (g == 1) dev::mma2_commit_mc_w(&v_empty[st], 0x3);
+      };
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j < nA) {
+          issue_pv(0, j);
+          if (j + 1 < nA) issue_s(0, j + 1);
+        }
+        issue_pv(1, j);
+        if (j + 1 < n_kv) issue_s(1, j + 1);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    const int g = (warp - 4) >> 2;  // softmax group: 0 -> tile A, 1 -> tile B
+    const uint32_t q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const int qt = 4 * quad + 2 * g + static_cast<int>(rank);
+    const int qidx = qt * TILE + row;
+    const int n_my = g ? n_kv : nA;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const uint32_t t_s = tmem + g * 128 + lane_off;
+    const uint32_t t_o = tmem + 256 + g * D + lane_off;
+    const uint32_t pf0 = dev::mapa(dev::smem_u32(&p_full[2 * g]), 0);
+    const uint32_t pf1 = dev::mapa(dev::smem_u32(&p_full[2 * g + 1]), 0);
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_my; ++j) {
+      dev::mbar_wait(&s_full[g], j & 1);
+      dev::tc_fence_after();
+      if (NULL_SM || j > qt) {  // the group's other tile reaches one key tile further: all masked, P = 0
+        uint32_t z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0u;
+        dev::tmem_st32(t_s, z);
+        dev::tmem_st32(t_s + 32, z);
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive_cluster(pf0);
+        dev::mbar_arrive_cluster(pf1);
+        continue;
+      }
+      uint32_t r[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dev::tmem_ld32(t_s + c * 32, r[c]);
+      // no wait::ld: consumers wait on the registers' scoreboard (attn_fwd_pp_kernel LDSB)
+      bool any = false;
+      float factor = 1.f;
+      uint32_t p[64];
+      auto tile = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+        if (DIAG) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i > row) r[i >> 5][i & 31] = __float_as_uint(-INFINITY);
+        }
+        auto rv = [&](int i) { return __uint_as_float(r[i >> 5][i & 31]); };
+        float mx8[8];
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(rv(k2), rv(8 + k2));
+#pragma unroll
+        for (int i = 16; i < 128; i += 16)
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmax3f(mx8[k2], rv(i + k2), rv(i + 8 + k2));
+        const float mxa = fmax3f(mx8[0], mx8[1], mx8[2]);
+        const float mxb = fmax3f(mx8[3], mx8[4], mx8[5]);
+        const float mxr = fmax3f(mxa, mxb, fmaxf(mx8[6], mx8[7]));
+        const float cand = fmaxf(m, mxr * scale_log2);
+        const bool need = j == 0 || cand > m + kRescaleThreshold;
+        any = __any_sync(0xffffffffu, need);
+        float m_new = m;
+        if (any) {
+          m_new = cand;
+          factor = j == 0 ? 0.f : dev::ex2(m - m_new);
+        }
+        uint64_t sum4[4] = {0, 0, 0, 0};
+        auto exps = [&](int i0) {
+#pragma unroll
+          for (int i = i0; i < i0 + 32; ++i) {
+            const uint64_t x2 = ffma2(f2_pack(__uint_as_float(r[i >> 4][(2 * i) & 31]),
+                                              __uint_as_float(r[i >> 4][(2 * i + 1) & 31])),
+                                      scale_log2, -m_new);
+            float a, b;
+            if (EMU_EVERY > 0 && (i % (EMU_EVERY > 0 ? EMU_EVERY : 1)) == EMU_EVERY - 1) {
+              const uint64_t e2 = exp2_fma2(x2);
+              a = f2_lo(e2);
+              b = f2_hi(e2);
+            } else {
+              a = dev::ex2(f2_lo(x2));
+              b = dev::ex2(f2_hi(x2));
+            }
+            sum4[i & 3] = fadd2(sum4[i & 3], f2_pack(a, b));
+            p[i] = dev::pack_bf16(a, b);
+          }
+        };
+        exps(0);
+        dev::tmem_st32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&p[0]));
+        if (any && j > 0) {
+          // O_g holds P(j-1)V(j-1) (PV_g(j-1) completed before s_full_g(j) fired)
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            dev::tmem_ld32(t_o + c * 32, o);
+            dev::tmem_ld_wait_regs(o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+            dev::tmem_st32(t_o + c * 32, o);
+          }
+        }
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive_cluster(pf0);
+        exps(32);
+        dev::tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&p[32]));
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive_cluster(pf1);
+        const uint64_t s01 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+        l = l * factor + (f2_lo(s01) + f2_hi(s01));
+        m = m_new;
+      };
+      if (j == qt)
+        tile(std::true_type{});
+      else
+        tile(std::false_type{});
+    }
+    dev::mbar_wait(&o_done[g], 0);  // committed once, after the group's last PV
+    dev::tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + static_cast<long long>(qidx) * H * D + hh * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      dev::tmem_ld32(t_o + c * 32, o);
+      dev::tmem_ld_wait_regs(o);
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 u;
+        u.x = dev::pack_bf16(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
+        u.y = dev::pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
+        u.z = dev::pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
+        u.w = dev::pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
+        dst[i] = u;
+      }
+    }
+    lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(l)) * kLn2;
+  }
+  dev::tc_fence_before();
+  dev::cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc_cg2(tmem, 512);
+  }
+}
+#endif  // MEMO_ATTN_ABLATIONS
+
 #ifdef MEMO_ATTN_ABLATIONS  // split-row ping-pong forward (ablation build only)
 // ------------------------------------------------------- forward, ping-pong, split rows
 // The ping-pong schedule of attn_fwd_pp_kernel (two query tiles A/B per CTA,
@@ -1861,15 +2179,6 @@ struct DkdvTsSmem {
   static constexpr int BAR_OFF = VEC_OFF + TSN * 256;
   static constexpr int BYTES = BAR_OFF + 512 + 1024;
 };
-// Descriptor helpers for operand tiles whose 64-col chunks are CH bytes apart.
-template <int CH>
-__device__ __forceinline__ uint64_t kmajor_step_c(uint64_t d, int kk) {
-  return d + static_cast<uint64_t>(((kk >> 2) * CH + (kk & 3) * 32) >> 4);
-}
-template <int CH>
-__device__ __forceinline__ uint64_t mnmajor_base_c(uint32_t base) {
-  return dev::umma_desc_sw128(base, CH, 1024);
-}
 
 // WPQ: softmax-gradient warps per TMEM lane quarter (2: 16 query columns each;
 // 4: 8 columns each, compacted P/dS write-back behind a per-quarter named barrier).
@@ -1940,6 +2249,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   MEMO_PROF(__shared__ volatile long long pf_issue[4];)
   if (warp == 0) {
     if (lane == 0) {
+      MEMO_PROF(long long pe_acc = 0;)
       if constexpr (TS > 0) {
         for (int g = 0; g < n_g; ++g) {
           const int st = g % NS;
@@ -1962,7 +2272,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         const int qt = kt + i, st = i % NS;
         MEMO_PROF(long long pe = clock64();)
         dev::mbar_wait(&in_empty[st], ((i / NS) & 1) ^ 1);
-        MEMO_PROF(if (i >= NS) atomicAdd(&g_dkdv_prof[14], static_cast<unsigned long long>(clock64() - pe));)
+        MEMO_PROF(if (i >= NS) pe_acc += clock64() - pe;)
         dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
         MEMO_PROF(pf_issue[st] = clock64();)
         for (int c = 0; c < NC; ++c) {
@@ -1976,6 +2286,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         dev::bulk_load(vec, lse2 + off, 512, &in_full[st]);
         dev::bulk_load(vec + 128, delta + off, 512, &in_full[st]);
       }
+      MEMO_PROF(atomicAdd(&g_dkdv_prof[14], static_cast<unsigned long long>(pe_acc));)
     }
   } else if (warp == 1) {
     {  // whole warp, converged: MMAs/commits elect one lane
@@ -1983,6 +2294,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
       dev::mbar_wait_w(kv_ready, 0);
       dev::tc_fence_after();
+      MEMO_PROF(long long pf_acc[16] = {};)
       auto issue_sd = [&](int g) {
         const int i = g >> 2, qq = g & 3, b = g & 1;
         const int st = TS > 0 ? g % NS : i % NS;
@@ -1992,16 +2304,16 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         } else if (qq == 0) {
           MEMO_PROF(long long prof_b = clock64();)
           dev::mbar_wait_w(&in_full[st], (i / NS) & 1);
-          MEMO_PROF(if (lane == 0) {
-            const unsigned long long w = static_cast<unsigned long long>(clock64() - prof_b);
-            atomicAdd(&g_dkdv_prof[0], w);
-            if (i == 0) atomicAdd(&g_dkdv_prof[8], w);          // first tile of the CTA
+          MEMO_PROF({  // per-CTA register sums, one atomic each at the end (no per-step atomics)
+            const long long w = clock64() - prof_b;
+            pf_acc[0] += w;
+            if (i == 0) pf_acc[8] += w;  // first tile of the CTA
             if (i > 0 && w > 200) {
-              atomicAdd(&g_dkdv_prof[9], w);
-              atomicAdd(&g_dkdv_prof[10], 1ull);
-              atomicAdd(&g_dkdv_prof[12], static_cast<unsigned long long>(clock64() - pf_issue[st]));
+              pf_acc[9] += w;
+              pf_acc[10] += 1;
+              pf_acc[12] += clock64() - pf_issue[st];
             }
-            if (i > 0) atomicAdd(&g_dkdv_prof[11], 1ull);
+            if (i > 0) pf_acc[11] += 1;
           })
           dev::tc_fence_after();
         }
@@ -2035,7 +2347,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         const int st = TS > 0 ? g % NS : i % NS;
         MEMO_PROF(long long prof_a = clock64();)
         dev::mbar_wait_w(&p_ready[b], (g >> 1) & 1);
-        MEMO_PROF(if (lane == 0) atomicAdd(&g_dkdv_prof[1], static_cast<unsigned long long>(clock64() - prof_a));)
+        MEMO_PROF(pf_acc[1] += clock64() - prof_a;)
         dev::tc_fence_after();
         const uint32_t roff = TS > 0 ? 0u : qq * QSTEP * 128;
         const uint32_t sbytes = TS > 0 ? L::STAGE_BYTES : L::TILE_BYTES;
@@ -2055,7 +2367,13 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         if (TS > 0 || qq == 3) dev::mma_commit_w(&in_empty[st]);
       }
       dev::mma_commit_w(fin);
-      MEMO_PROF(if (lane == 0) { atomicAdd(&g_dkdv_prof[5], static_cast<unsigned long long>(clock64() - prof_s)); atomicAdd(&g_dkdv_prof[4], static_cast<unsigned long long>(n_g)); })
+      MEMO_PROF(if (lane == 0) {
+        pf_acc[5] += clock64() - prof_s;
+        pf_acc[4] += n_g;
+        for (int k = 0; k < 16; ++k)
+          if (k != 2 && k != 3 && k != 6 && k != 7 && k != 14)
+            atomicAdd(&g_dkdv_prof[k], static_cast<unsigned long long>(pf_acc[k]));
+      })
     }
   } else if (warp >= 4) {
     const uint32_t q4 = warp & 3;
@@ -2069,6 +2387,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     dev::tmem_st_wait();
     dev::tc_fence_before();
     dev::mbar_arrive(kv_ready);
+    MEMO_PROF(long long cp_acc[8] = {};)
     for (int g = 0; g < n_g; ++g) {
       const int i = g >> 2, qq = g & 3, b = g & 1;
       const int st = TS > 0 ? g % NS : i % NS;
@@ -2087,7 +2406,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       }
       MEMO_PROF(long long prof_t0 = clock64();)
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
-      MEMO_PROF(long long prof_t1 = clock64(); if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[2], static_cast<unsigned long long>(prof_t1 - prof_t0));)
+      MEMO_PROF(long long prof_t1 = clock64(); cp_acc[2] += prof_t1 - prof_t0;)
       dev::tc_fence_after();
       uint32_t sr[COLS], dr[COLS];
       if constexpr (COLS == 16) {
@@ -2102,7 +2421,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       // else reuses these columns first).  COLS 8 writes into other warps'
       // columns behind a named barrier, which needs the loads complete.
       if constexpr (COLS != 16) dev::tmem_ld_wait_regs(sr, dr);
-      MEMO_PROF(if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[6], static_cast<unsigned long long>(clock64() - prof_t1));)
+      MEMO_PROF(cp_acc[6] += clock64() - prof_t1;)
       uint32_t pp[COLS / 2], dd[COLS / 2];
       auto body = [&](auto diag_tag) {
         constexpr bool DIAG = decltype(diag_tag)::value;
@@ -2221,11 +2540,13 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       }
       MEMO_PROF(long long prof_t2 = clock64();)
       dev::tmem_st_wait();
-      MEMO_PROF(if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[7], static_cast<unsigned long long>(clock64() - prof_t2));)
+      MEMO_PROF(cp_acc[7] += clock64() - prof_t2;)
       dev::tc_fence_before();
       dev::mbar_arrive(&p_ready[b]);
-      MEMO_PROF(if (warp == 4 && lane == 0) atomicAdd(&g_dkdv_prof[3], static_cast<unsigned long long>(clock64() - prof_t1));)
+      MEMO_PROF(cp_acc[3] += clock64() - prof_t1;)
     }
+    MEMO_PROF(if (warp == 4 && lane == 0) for (int k2 : {2, 3, 6, 7})
+                atomicAdd(&g_dkdv_prof[k2], static_cast<unsigned long long>(cp_acc[k2]));)
     dev::mbar_wait(fin, 0);
     dev::tc_fence_after();
     __nv_bfloat16* dvrow = dv + static_cast<long long>(kidx) * ld + hh * D;
@@ -3343,11 +3664,25 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   // 27 ping-pong with quarter P stores and the row sum after the release (QSTORE);
   // 28-31 ping-pong without the wait::ld after the S loads (LDSB), share 1/3, 1/8, none, 1/4;
   // 32 LDSB + QSTORE, share 1/8; 33 the round-2 product before LDSB (wait::ld after the S loads);
-  // 34-37 QSTORE (with LDSB), share 1/4, 1/6, 1/16, none;
+  // 34-37 QSTORE (with LDSB), share 1/4, 1/6, 1/16, none; 42/43 CTA-pair ping-pong (share 1/3, 1/4), 44 its MMA-side ceiling (P = 0);
   // 38-41 split rows with the groups taking turns (attn_fwd_pp2w_kernel SEQ), share 1/4, 1/8, none, 1/16
   const int v = abl_env("MEMO_ATTN_FWD_VARIANT", 8);
   if (v != 8) {
-    if (((v >= 17 && v <= 20) || (v >= 38 && v <= 41)) && a.D == 128 && a.S % (2 * TILE) == 0) {
+    if ((v == 42 || v == 43 || v == 44) && a.D == 128 && a.S % (4 * TILE) == 0) {
+      // CTA-pair ping-pong (attn_fwd_pair_kernel), FMA share 1/3 / 1/4
+      CUtensorMap mk64;
+      if (!make_tma_2d_bf16(&mk64, a.k, h, a.S, h, 64, 64)) return cudaErrorInvalidValue;
+      static std::once_flag fpair;
+      std::call_once(fpair, [] {
+        cudaFuncSetAttribute(attn_fwd_pair_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPairSmem::BYTES);
+        cudaFuncSetAttribute(attn_fwd_pair_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPairSmem::BYTES);
+        cudaFuncSetAttribute(attn_fwd_pair_kernel<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             FwdPairSmem::BYTES);
+      });
+      auto kern = v == 42 ? attn_fwd_pair_kernel<3> : v == 43 ? attn_fwd_pair_kernel<4> : attn_fwd_pair_kernel<3, true>;
+      kern<<<dim3(2 * (a.S / (4 * TILE)), a.H), 384, FwdPairSmem::BYTES, stream>>>(mq, mk64, mv, a.o, a.lse, a.S, a.H,
+                                                                                 scale_log2);
+    } else if (((v >= 17 && v <= 20) || (v >= 38 && v <= 41)) && a.D == 128 && a.S % (2 * TILE) == 0) {
       static std::once_flag fw;
       std::call_once(fw, [] {
         for (auto k : {attn_fwd_pp2w_kernel<3>, attn_fwd_pp2w_kernel<4>, attn_fwd_pp2w_kernel<0>,

@@ -335,6 +335,34 @@ __device__ __forceinline__ void mma2_bf16_ss_w(uint32_t d_tmem, uint64_t a_desc,
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Pair MMA with A from TMEM (each CTA supplies its own 128 rows of A from its
+// TMEM; B split over the pair's shared memory as for the SS form).
+__device__ __forceinline__ void mma2_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Wait (whole warp, converged) on a barrier that the peer CTA arrives on:
+// acquire at cluster scope, so the peer's prior writes (and, after
+// tcgen05.fence::after_thread_sync, its TMEM stores) are visible.
+__device__ __forceinline__ void mbar_wait_cluster_w(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+  __syncwarp();
+}
 // 2-D tile load multicast to the same shared-memory offset in every CTA of
 // `mask`; each destination CTA's barrier at `bar`'s offset gets the tx bytes.
 __device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
