@@ -1845,25 +1845,34 @@ __global__ void __launch_bounds__(PP2W_THREADS, 1)
 
 // ============================================================== backward
 // ndelta[h][t] = -sum_d dO*O ; nlse2[h][t] = -lse * log2(e)  (the delta / lse2 workspace)
+// D/8 threads per (t, head) row, each loading 16 bytes of O and of dO (one
+// 128-bit load each, whole rows per warp), then a shuffle tree over the row's
+// lanes.  HBM-bound: 4·D bytes read and 8 written per row.
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                      const __nv_bfloat16* __restrict__ dout,
                                      const float* __restrict__ lse, float* __restrict__ delta,
                                      float* __restrict__ lse2, int S, int H, int D) {
-  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);  // row = t*H + hh
-  const int lane = threadIdx.x & 31;
-  if (row >= S * H) return;
-  const int t = row / H, hh = row - t * H;
-  const __nv_bfloat16* op = o + static_cast<long long>(t) * H * D + hh * D;
-  const __nv_bfloat16* dp = dout + static_cast<long long>(t) * H * D + hh * D;
+  const int tpr = D / 8;  // threads per row (16 at D = 128, 8 at D = 64)
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gtid / tpr;  // row = t*H + hh
+  const int sub = gtid - row * tpr;
+  const bool live = row < S * H;
   float acc = 0.f;
-  for (int d = lane * 2; d < D; d += 64) {
-    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(op + d);
-    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(dp + d);
-    acc += __bfloat162float(a.x) * __bfloat162float(b.x) + __bfloat162float(a.y) * __bfloat162float(b.y);
-  }
+  if (live) {
+    const long long base = static_cast<long long>(row) * D + sub * 8;  // [S][H][D] contiguous
+    const uint4 a = *reinterpret_cast<const uint4*>(o + base);
+    const uint4 b = *reinterpret_cast<const uint4*>(dout + base);
+    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) {
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&av[i]);
+      const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(&bv[i]);
+      acc += __bfloat162float(x.x) * __bfloat162float(y.x) + __bfloat162float(x.y) * __bfloat162float(y.y);
+    }
+  }
+  for (int off = tpr / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (live && sub == 0) {
+    const int t = row / H, hh = row - t * H;
     const long long i = static_cast<long long>(hh) * S + t;
     delta[i] = -acc;            // stored negated: consumers add (FFMA2/FADD2, no negation)
     lse2[i] = -lse[i] * kLog2e;
@@ -3479,7 +3488,8 @@ cudaError_t launch_bwd_fused(const AttnBwdArgs& a, cudaStream_t stream) {
   uint32_t* ticket = counters + n_ctr;
   if (a.ev[0]) record_timing_event(a.ev[0], stream);
   cudaMemsetAsync(counters, 0, (n_ctr + 4) * sizeof(uint32_t), stream);
-  attn_bwd_prep_kernel<<<(a.S * a.H + 7) / 8, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S, a.H, D);
+  attn_bwd_prep_kernel<<<(a.S * a.H * (D / 8) + 255) / 256, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S,
+                                                                              a.H, D);
   if (a.ev[1]) record_timing_event(a.ev[1], stream);
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   auto kern = pend >= 4 ? attn_bwd_fused_kernel<D, 4>
@@ -3538,7 +3548,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   float* lse2 = a.delta + static_cast<long long>(a.H) * a.S;
   const int rows = a.S * a.H;
   if (a.ev[0]) record_timing_event(a.ev[0], stream);
-  attn_bwd_prep_kernel<<<(rows + 7) / 8, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S,
+  attn_bwd_prep_kernel<<<(rows * (D / 8) + 255) / 256, 256, 0, stream>>>(a.o, a.dout, a.lse, delta, lse2, a.S,
                                                             a.H, D);
   const float scale_log2 = a.softmax_scale * kLog2e;
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
