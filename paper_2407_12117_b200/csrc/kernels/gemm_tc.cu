@@ -460,8 +460,14 @@ constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256 + SLAB_BYTES;
 constexpr int P_GROUP_M = 16;  // raster band of pair tiles (8 measured slower)
 
-template <bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+// PC = 2: clusters of two CTA pairs on vertically adjacent pair tiles (same
+// N columns).  Each stage's B half is shared across the pairs by multicast:
+// CTA (pair p, half h) loads 64 of its 128 B rows and multicasts them to the
+// same half of the other pair, so each SM reads 8 instead of 16 KiB of B per
+// k-block from L2 (cuBLAS's 2x1-cluster 2-CTA layout).  A stage is then
+// released by both pair leaders (empty barrier count 2).
+template <bool A_MN, bool B_MN, int PC = 1>
+__global__ void __cluster_dims__(2 * PC, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     int M, int N, int K, EpiParams ep) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -476,12 +482,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
-  const uint32_t rank = dev::cluster_ctarank();
-  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const uint32_t crank = dev::cluster_ctarank();
+  const uint32_t rank = crank & 1;             // rank inside the CTA pair
+  const uint32_t pair = crank >> 1;            // pair inside the cluster (PC = 2)
+  const uint32_t leader = crank & ~1u;         // the pair's MMA-issuing CTA
+  const int cluster = blockIdx.x / (2 * PC), n_clusters = gridDim.x / (2 * PC);
 
-  const int m_tiles = (M + 2 * P_BM - 1) / (2 * P_BM);
+  const int m_tiles = PC * ((M + 2 * PC * P_BM - 1) / (2 * PC * P_BM));  // pair tiles, whole clusters
   const int n_tiles = (N + P_BN - 1) / P_BN;
-  const int num_tiles = m_tiles * n_tiles;
+  const int num_tiles = (m_tiles / PC) * n_tiles;  // cluster units
   const int num_kb = (K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -489,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     dev::tma_prefetch_desc(&map_b);
     for (int s = 0; s < P_STAGES; ++s) {
       dev::mbar_init(&full_bar[s], 1);
-      dev::mbar_init(&empty_bar[s], 1);
+      dev::mbar_init(&empty_bar[s], PC);  // one release per pair leader
     }
     for (int b = 0; b < 2; ++b) {
       dev::mbar_init(&tfull_bar[b], 1);
@@ -503,13 +512,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   dev::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto tile_coords = [&](int t, int& mb, int& nb) {
-    const int group_size = P_GROUP_M * n_tiles;
+  auto tile_coords = [&](int t, int& mb, int& nb) {  // cluster unit t -> this pair's tile
+    const int mu_tiles = m_tiles / PC;
+    const int group_m = P_GROUP_M / PC;
+    const int group_size = group_m * n_tiles;
     const int g = t / group_size;
-    const int first_m = g * P_GROUP_M;
-    const int gm = min(P_GROUP_M, m_tiles - first_m);
+    const int first_m = g * group_m;
+    const int gm = min(group_m, mu_tiles - first_m);
     const int local = t - g * group_size;
-    mb = first_m + local % gm;
+    mb = (first_m + local % gm) * PC + static_cast<int>(pair);
     nb = local / gm;
     if (ep.serpentine && (g & 1)) nb = n_tiles - 1 - nb;
   };
@@ -528,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           dev::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * P_STAGE_BYTES;
           uint8_t* sb = sa + P_A_BYTES;
-          const uint32_t fb = dev::mapa(dev::smem_u32(&full_bar[stage]), 0);  // leader's barrier
+          const uint32_t fb = dev::mapa(dev::smem_u32(&full_bar[stage]), leader);  // pair leader's barrier
           if (rank == 0) dev::mbar_expect_tx(&full_bar[stage], 2 * P_STAGE_BYTES);
           if (!A_MN) {
             dev::tma_load_2d_cg2(sa, &map_a, fb, kb * BK, m0);
@@ -536,7 +547,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < P_BM / 64; ++j) dev::tma_load_2d_cg2(sa + j * 8192, &map_a, fb, m0 + j * 64, kb * BK);
           }
-          if (!B_MN) {
+          if (PC == 2 && !B_MN) {
+            // 64 of this half's 128 B rows, multicast to the same half of both pairs
+            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
+            dev::tma_load_2d_cg2_mc(sb + pair * (P_B_BYTES / 2), &map_b, fb, kb * BK,
+                                    n0 + static_cast<int>(pair) * (P_BN / 4), mask);
+          } else if (!B_MN) {
             dev::tma_load_2d_cg2(sb, &map_b, fb, kb * BK, n0);
           } else {
 #pragma unroll
@@ -585,13 +601,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bd = bd0 + static_cast<uint64_t>((B_MN ? k * 2048 : k * 32) >> 4);
             dev::mma2_bf16_ss_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          dev::mma2_commit_mc_w(&empty_bar[stage], 0x3);
+          dev::mma2_commit_mc_w(&empty_bar[stage], PC == 2 ? 0xF : 0x3);  // every CTA the stage's B reached
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        dev::mma2_commit_mc_w(&tfull_bar[buf], 0x3);
+        dev::mma2_commit_mc_w(&tfull_bar[buf], static_cast<uint16_t>(0x3u << leader));
       }
     }
   } else {
@@ -608,7 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       epilogue_rows<P_BN>(ep, slab + q * 256, tmem_base + ((q * 32) << 16) + buf * P_BN,
                           mb * 2 * P_BM + rank * P_BM + q * 32, M, nb * P_BN, N, lane);
       dev::tc_fence_before();
-      dev::mbar_arrive_cluster(dev::mapa(dev::smem_u32(&tempty_bar[buf]), 0));
+      dev::mbar_arrive_cluster(dev::mapa(dev::smem_u32(&tempty_bar[buf]), leader));
     }
   }
   dev::tc_fence_before();
@@ -634,17 +650,23 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   // multicast (half the B bytes per CTA; bitwise equal to unclustered tiles):
   // 3 % less GEMM time per cfg2 step.  d.variant (tests and A/B tools only)
   // forces one kernel: GEMM_VARIANT_SINGLE / _MC2 / _MC4 (2x2 clusters that
-  // also share A) / _PAIR.
+  // also share A) / _PAIR / _PAIR2 (two pairs per cluster, the pair default).
   bool pair;
   int cl;
+  int pc = 1;  // CTA pairs per cluster (2: B shared across the pairs, K-major B only)
   switch (d.variant) {
     case GEMM_VARIANT_SINGLE: pair = false; cl = 1; break;
     case GEMM_VARIANT_MC2: pair = false; cl = 2; break;
     case GEMM_VARIANT_MC4: pair = false; cl = 4; break;
     case GEMM_VARIANT_PAIR: pair = true; cl = 1; break;
+    case GEMM_VARIANT_PAIR2: pair = true; cl = 1; pc = B_MN ? 1 : 2; break;
     default:
       pair = !A_MN && !B_MN && d.K <= 4096 && d.N >= 8192;
       cl = pair ? 1 : 2;
+      // the pair tiles run as two pairs per cluster sharing B (K-major B here):
+      // +0.6 % per cfg2 step in three alternating whole-step runs, QKV +10 %
+      // in the per-shape A/B (profiles/README.md)
+      if (pair) pc = 2;
   }
   const bool mc = cl > 1;
   if (!A_MN)
@@ -652,7 +674,7 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
   else
     ok = make_tma_2d_bf16(&ma, d.a, d.M, d.K, d.lda, 64, BK);
   if (!B_MN)
-    ok = ok && make_tma_2d_bf16(&mb, d.b, d.K, d.N, d.ldb, BK, (pair || mc) ? BN / 2 : BN);
+    ok = ok && make_tma_2d_bf16(&mb, d.b, d.K, d.N, d.ldb, BK, pc == 2 ? BN / 4 : (pair || mc) ? BN / 2 : BN);
   else
     ok = ok && make_tma_2d_bf16(&mb, d.b, d.N, d.K, d.ldb, 64, BK);
   if (!ok) return cudaErrorInvalidValue;
@@ -685,8 +707,34 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(gemm_tc2_kernel<A_MN, B_MN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_tc2_kernel<A_MN, B_MN, 2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_BYTES);
   });
   const int g_num_sms = num_sms();
+  if (pair && pc == 2) {  // clusters of two CTA pairs sharing B
+    const int units = ((d.M + 4 * P_BM - 1) / (4 * P_BM)) * ((d.N + P_BN - 1) / P_BN);
+    // persistent clusters: no more than can be co-resident (4-CTA clusters need
+    // not tile every GPC), else the surplus would run as a second wave
+    static std::atomic<int> resident4[MAX_DEVICES];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int>& slot = resident4[dev < MAX_DEVICES ? dev : 0];
+    int res = slot.load(std::memory_order_relaxed);
+    if (res == 0) {
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3(4 * (g_num_sms / 4));
+      qc.blockDim = dim3(NUM_THREADS);
+      qc.dynamicSmemBytes = P_SMEM_BYTES;
+      if (cudaOccupancyMaxActiveClusters(&res, gemm_tc2_kernel<A_MN, B_MN, 2>, &qc) != cudaSuccess || res <= 0) {
+        cudaGetLastError();
+        res = g_num_sms / 4;
+      }
+      slot.store(res, std::memory_order_relaxed);
+    }
+    const int clusters = units < res ? units : res;
+    gemm_tc2_kernel<A_MN, B_MN, 2><<<4 * clusters, NUM_THREADS, P_SMEM_BYTES, stream>>>(ma, mb, d.M, d.N, d.K, ep);
+    return cudaGetLastError();
+  }
   if (pair) {  // CTA pairs on 256x256 tiles
     const int tiles = ((d.M + 2 * P_BM - 1) / (2 * P_BM)) * ((d.N + P_BN - 1) / P_BN);
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;

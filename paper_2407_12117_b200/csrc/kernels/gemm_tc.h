@@ -21,6 +21,7 @@ enum GemmVariant {
   GEMM_VARIANT_MC2 = 2,     // single-CTA tiles in 2-CTA clusters, B multicast
   GEMM_VARIANT_MC4 = 3,     // 2x2 clusters, A and B multicast
   GEMM_VARIANT_PAIR = 4,    // CTA-pair 256x256 tiles (cta_group::2)
+  GEMM_VARIANT_PAIR2 = 5,   // two CTA pairs per cluster sharing B by multicast (K-major B)
 };
 
 // Tile order: GEMM_RASTER_AUTO (serpentine bands) or the round-1 order (A/B tools).

@@ -105,6 +105,25 @@ def test_gemm_cta_pair_variant():
             test_gemm_layouts(*shp, lay, variant=4)
 
 
+def test_gemm_pair_cluster_variant_bitwise():
+    """variant 5 (two CTA pairs per cluster sharing B by multicast, the default
+    for the pair shapes) is bitwise equal to one pair per cluster (variant 4)
+    and matches fp32, with ragged M (the cluster's second pair past M) and N;
+    dgrad/wgrad layouts (MN-major B) fall back to variant 4's kernel."""
+    for shp in [(128, 256, 64), (200, 256, 192), (640, 288, 4096), (1024, 2048, 1024), (1536, 768, 512)]:
+        for lay in ("fwd", "dgrad", "wgrad"):
+            test_gemm_layouts(*shp, lay, variant=5)
+    for (M, N, K) in [(200, 512, 192), (640, 288, 512), (2048, 1024, 1024)]:
+        torch.manual_seed(M + N + K)
+        a, b = _rand(M, K), _rand(N, K)
+        outs = []
+        for var in (4, 5):
+            c = torch.empty(M, N, device="cuda", dtype=torch.float32)
+            _gemm(M, N, K, a, K, 0, b, K, 0, 1, c, N, variant=var)
+            outs.append(c)
+        assert torch.equal(outs[0], outs[1])
+
+
 def test_gemm_b_multicast_cluster_bitwise():
     """variant 2 (the default single-CTA kernel: 2-CTA clusters, B shared by TMA
     multicast) and 3 (2x2 clusters sharing A and B): bitwise equal to the
@@ -135,7 +154,7 @@ def test_gemm_b_multicast_cluster_bitwise():
 def test_gemm_raster_order_is_bitwise_neutral():
     """The serpentine tile order (product) and the round-1 order give bitwise
     equal outputs on every layout and kernel variant (tile order only)."""
-    for var in (0, 1, 2, 4):
+    for var in (0, 1, 2, 4, 5):
         for (M, N, K) in [(1152, 2048, 1024), (2560, 768, 512)]:
             torch.manual_seed(M + N + K + var)
             a, b, bs, as_ = _rand(M, K), _rand(N, K), _rand(K, N), _rand(K, M)

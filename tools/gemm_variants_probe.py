@@ -1,4 +1,4 @@
-"""Runs every GEMM kernel variant (memo_gemm_args.variant 1-4: single CTA,
+"""Runs every GEMM kernel variant (memo_gemm_args.variant 1-5: single CTA,
 2-CTA B-multicast cluster, 2x2 cluster, CTA pair) on the three operand layouts
 at small ragged shapes and checks each against torch fp32.  Meant to run under
 compute-sanitizer (tools/sanitize.sh): the clustered kernels' multicast TMA and
@@ -34,7 +34,7 @@ def main():
         B = (torch.randn(N, K, device="cuda") * 0.5).to(torch.bfloat16)
         At, Bt = A.t().contiguous(), B.t().contiguous()
         ref = A.float() @ B.float().t()
-        for variant in (1, 2, 3, 4):
+        for variant in (1, 2, 3, 4, 5):
             for lay, (a, lda, amn, b, ldb, bmn) in {"fwd": (A, K, 0, B, K, 0), "dgrad": (A, K, 0, Bt, N, 1),
                                                     "wgrad": (At, M, 1, Bt, N, 1)}.items():
                 c = torch.zeros(M, N, device="cuda")
