@@ -186,8 +186,8 @@ typedef struct memo_gemm_args {
   const void* rope;
   int64_t pos0;
   /* 0 = the product's kernel choice; 1 single-CTA, 2 2-CTA B-multicast cluster,
-   * 3 2x2 cluster, 4 CTA pair (cta_group::2), 5 two CTA pairs per cluster sharing B
-   * (K-major B; otherwise 4): forced, for equivalence tests */
+   * 3 2x2 cluster, 4 CTA pair (cta_group::2), 5 two CTA pairs per cluster sharing B:
+   * forced, for equivalence tests */
   int32_t variant;
   /* 0 = serpentine raster bands (product); 1 = the round-1 tile order (A/B) */
   int32_t raster;

@@ -552,6 +552,10 @@ __global__ void __cluster_dims__(2 * PC, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
             dev::tma_load_2d_cg2_mc(sb + pair * (P_B_BYTES / 2), &map_b, fb, kb * BK,
                                     n0 + static_cast<int>(pair) * (P_BN / 4), mask);
+          } else if (PC == 2) {
+            // MN-major B: the half's two 64-column boxes, one per pair, multicast
+            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
+            dev::tma_load_2d_cg2_mc(sb + pair * 8192, &map_b, fb, n0 + static_cast<int>(pair) * 64, kb * BK, mask);
           } else if (!B_MN) {
             dev::tma_load_2d_cg2(sb, &map_b, fb, kb * BK, n0);
           } else {
@@ -659,7 +663,7 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
     case GEMM_VARIANT_MC2: pair = false; cl = 2; break;
     case GEMM_VARIANT_MC4: pair = false; cl = 4; break;
     case GEMM_VARIANT_PAIR: pair = true; cl = 1; break;
-    case GEMM_VARIANT_PAIR2: pair = true; cl = 1; pc = B_MN ? 1 : 2; break;
+    case GEMM_VARIANT_PAIR2: pair = true; cl = 1; pc = 2; break;
     default:
       pair = !A_MN && !B_MN && d.K <= 4096 && d.N >= 8192;
       cl = pair ? 1 : 2;

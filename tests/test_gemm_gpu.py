@@ -108,8 +108,8 @@ def test_gemm_cta_pair_variant():
 def test_gemm_pair_cluster_variant_bitwise():
     """variant 5 (two CTA pairs per cluster sharing B by multicast, the default
     for the pair shapes) is bitwise equal to one pair per cluster (variant 4)
-    and matches fp32, with ragged M (the cluster's second pair past M) and N;
-    dgrad/wgrad layouts (MN-major B) fall back to variant 4's kernel."""
+    and matches fp32, with ragged M (the cluster's second pair past M) and N,
+    on all three layouts (MN-major B: one 64-column box per pair, multicast)."""
     for shp in [(128, 256, 64), (200, 256, 192), (640, 288, 4096), (1024, 2048, 1024), (1536, 768, 512)]:
         for lay in ("fwd", "dgrad", "wgrad"):
             test_gemm_layouts(*shp, lay, variant=5)
