@@ -2836,7 +2836,12 @@ __global__ void __launch_bounds__(32 * 12, 1)
 // AT: Q and dO live in TMEM (A operands) instead of shared memory.
 #endif  // MEMO_ATTN_ABLATIONS
 
-template <int D, bool AT>
+// CL2: CTA pairs (clusters of 2) on query tiles qt+1, qt of one head share
+// each K/V tile by TMA multicast: every CTA loads one 64-column chunk of K_j
+// and of V_j for both, halving the L2->SM traffic (1.1 TB per 128K launch
+// without it).  A stage is refilled once both CTAs have released it; the lower
+// tile's extra key tile (qt+1) is fully masked and contributes dS = 0.
+template <int D, bool AT, bool CL2 = false>
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     attn_bwd_dq_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dout,
                        const __grid_constant__ CUtensorMap map_q,
@@ -2867,7 +2872,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int n_tiles = S / TILE;
   const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
   const int hh = blockIdx.y;
-  const int n_kv = qt + 1;
+  const uint32_t crank = CL2 ? dev::cluster_ctarank() : 0u;  // rank 1 holds the lower tile
+  const int n_kv = qt + 1 + static_cast<int>(crank);
   const int n_g = 2 * n_kv;
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
@@ -2878,7 +2884,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     dev::mbar_init(qd_ready, AT ? 128 : 1);
     for (int s2 = 0; s2 < NS; ++s2) {
       dev::mbar_init(&kv_full[s2], 1);
-      dev::mbar_init(&kv_empty[s2], 1);
+      dev::mbar_init(&kv_empty[s2], CL2 ? 2 : 1);  // CL2: both CTAs' MMAs release a stage
     }
     for (int s2 = 0; s2 < 2; ++s2) {
       dev::mbar_init(&s_full[s2], 1);
@@ -2889,7 +2895,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   }
   if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
   dev::tc_fence_before();
-  __syncthreads();
+  if (CL2)
+    dev::cluster_sync();  // the peer's barriers exist before its first multicast lands here
+  else
+    __syncthreads();
   dev::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // buffer b: S half at b*128, dP half at b*128 + 64; dQ at 256; Q, dO as A operands after it
@@ -2908,12 +2917,29 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const int st = j % NS;
         dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
         dev::mbar_expect_tx(&kv_full[st], 2 * L::TILE_BYTES);
+        if (CL2) {  // half of K_j and V_j, to both CTAs
+          if (NC == 2) {  // D = 128: this CTA's 64-column chunk of each
+            const int c = static_cast<int>(crank);
+            dev::tma_load_2d_mc(smem + k_off(st) + c * CHUNK_BYTES, &map_k, &kv_full[st], hh * D + c * 64,
+                                j * TILE, 0x3);
+            dev::tma_load_2d_mc(smem + v_off(st) + c * CHUNK_BYTES, &map_v, &kv_full[st], hh * D + c * 64,
+                                j * TILE, 0x3);
+          } else if (crank == 0) {  // D = 64: one CTA loads K, the other V
+            dev::tma_load_2d_mc(smem + k_off(st), &map_k, &kv_full[st], hh * D, j * TILE, 0x3);
+          } else {
+            dev::tma_load_2d_mc(smem + v_off(st), &map_v, &kv_full[st], hh * D, j * TILE, 0x3);
+          }
+          continue;
+        }
         for (int c = 0; c < NC; ++c) {
           dev::tma_load_2d(smem + k_off(st) + c * CHUNK_BYTES, &map_k, &kv_full[st], hh * D + c * 64,
                            j * TILE);
           dev::tma_load_2d(smem + v_off(st) + c * CHUNK_BYTES, &map_v, &kv_full[st], hh * D + c * 64,
                            j * TILE);
         }
+      }
+      if (CL2) {  // producer tail: the peer's releases of the last stages land here asynchronously
+        for (int j = n_kv; j < n_kv + NS; ++j) dev::mbar_wait(&kv_empty[j % NS], ((j / NS) & 1) ^ 1);
       }
     }
   } else if (warp == 1) {
@@ -2959,7 +2985,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         for (int kk = 0; kk < HALF / 16; ++kk)
           dev::mma_bf16_ts_w(t_dq, tmem + b * 128 + 32 * (kk >> 1) + 8 * (kk & 1), mnmajor_step(km, kk),
                              idesc_g, (g | kk) != 0);
-        if (half == 1) dev::mma_commit_w(&kv_empty[st]);
+        if (half == 1) {
+          if (CL2)
+            dev::mma_commit_mc_w(&kv_empty[st], 0x3);  // the stage holds both CTAs' chunks
+          else
+            dev::mma_commit_w(&kv_empty[st]);
+        }
       }
       dev::mma_commit_w(fin);
     }
@@ -2986,6 +3017,16 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       dev::tc_fence_after();
       const uint32_t t_s = tmem + b * 128 + lane_off, t_dp = t_s + 64;
+      if (CL2 && j > qt) {  // the pair's extra key tile: fully masked, dS = 0
+        uint32_t z[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+        dev::tmem_st16(t_s + ch * 32, z);
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&ds_ready[b]);
+        continue;
+      }
       auto body = [&](auto diag_tag) {
         constexpr bool DIAG = decltype(diag_tag)::value;
         {
@@ -3036,7 +3077,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
     dev::tc_fence_before();
   }
-  __syncthreads();
+  if (CL2)
+    dev::cluster_sync();  // no multicast or remote release still targets this CTA
+  else
+    __syncthreads();
   if (warp == 1) {
     dev::tc_fence_after();
     dev::tmem_dealloc(tmem, 512);
@@ -3622,16 +3666,47 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   }
 #endif
   if (a.ev[2]) record_timing_event(a.ev[2], stream);
+  // dQ: CTA pairs (clusters of 2) sharing each K/V tile by multicast whenever
+  // the tile count is even (1 % faster at 128K, bitwise equal).  Ablation
+  // build: MEMO_ATTN_DQ_CL2=0 -> one CTA per query tile, MEMO_ATTN_DQ_TMEM_A=0 ->
+  // Q/dO as shared-memory operands.
+  bool dq_cl2 = (a.S / TILE) % 2 == 0;
 #ifdef MEMO_ATTN_ABLATIONS
-  if (abl_env("MEMO_ATTN_DQ_TMEM_A", 1) == 0)  // Q/dO as shared-memory operands
+  dq_cl2 = dq_cl2 && abl_env("MEMO_ATTN_DQ_CL2", 1) == 1;
+  if (abl_env("MEMO_ATTN_DQ_TMEM_A", 1) == 0) {  // Q/dO as shared-memory operands
     attn_bwd_dq_kernel<D, false><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
         a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
         a.softmax_scale, scale_log2);
-  else
+    dq_cl2 = false;
+  } else
 #endif
+  if (dq_cl2) {
+    static std::once_flag fcl;
+    std::call_once(fcl, [] {
+      cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           BwdSmem<D>::BYTES);
+    });
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(BWD_THREADS);
+    cfg.dynamicSmemBytes = BwdSmem<D>::BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dq_kernel<D, true, true>, a.q, a.dout, mq, mdo, mk, mv,
+                                             static_cast<const float*>(lse2), static_cast<const float*>(delta), a.dq,
+                                             a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale, scale_log2);
+    if (e != cudaSuccess) return e;
+  } else {
     attn_bwd_dq_kernel<D, true><<<grid, BWD_THREADS, BwdSmem<D>::BYTES, stream>>>(
         a.q, a.dout, mq, mdo, mk, mv, lse2, delta, a.dq, a.ld_dqkv, rope, a.pos0, a.S, a.H,
         a.softmax_scale, scale_log2);
+  }
   if (a.ev[3]) record_timing_event(a.ev[3], stream);
   return cudaGetLastError();
 }
