@@ -2584,7 +2584,229 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   }
 }
 
-#ifdef MEMO_ATTN_ABLATIONS  // decoupled P/dS dK/dV (ablation build only)
+#ifdef MEMO_ATTN_ABLATIONS  // 16-query and decoupled P/dS dK/dV (ablation build only)
+// ------------------------------------------------------------ dK/dV, 16-query steps
+// Ablation: bitwise equal, 268 vs 206 ms at 128K (M128 N16 MMAs run at 79 %).
+// Same math and operands as attn_bwd_dkdv_tm_kernel<D, 2>, with the pipeline cut
+// finer: 16-query steps and FOUR S^T/dP^T buffers in the same 128 TMEM columns
+//   [0,128) dV | [128,256) dK | [256,320) K | [320,384) V | [384 + 32b, +32) buf b
+//   buf: S^T [0,16) | dP^T [16,32); P^T packed into [0,8), dS^T into [16,24)
+// so the MMA warp queues S/dP three steps ahead of the dV/dK that wait for the
+// compute warps (768 tensor cycles of slack instead of 512).  The compute warps
+// form two groups of four (one per TMEM lane quarter) taking alternate steps,
+// each warp all 16 columns of its rows, so a warp has two steps' time per step.
+constexpr int Q16 = 16;
+
+template <int D>
+__global__ void __launch_bounds__(32 * 12, 1)
+    attn_bwd_dkdv_q16_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
+                             const __grid_constant__ CUtensorMap map_q,
+                             const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                             const float* __restrict__ delta, __nv_bfloat16* __restrict__ dk,
+                             __nv_bfloat16* __restrict__ dv, long long ld, const float2* __restrict__ rope,
+                             long long pos0, int S, int H, float scale, float scale_log2) {
+  using L = DkdvTmSmem<D>;
+  constexpr int NC = L::NC;
+  constexpr int NS = KV_NS;
+  constexpr int NB = 4;                // S^T/dP^T buffers
+  constexpr int SPT = TILE / Q16;      // steps per query tile
+  constexpr int AHEAD = NB - 1;        // S/dP issued this many steps ahead
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* kv_ready = bars + 0;
+  uint64_t* in_full = bars + 1;        // [NS]
+  uint64_t* in_empty = in_full + NS;   // [NS]
+  uint64_t* s_full = in_empty + NS;    // [NB]
+  uint64_t* p_ready = s_full + NB;     // [NB]
+  uint64_t* fin = p_ready + NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
+
+  const int n_tiles = S / TILE;
+  const int kt = blockIdx.x;  // key tile
+  const int hh = blockIdx.y;
+  const int n_q = n_tiles - kt;
+  const int n_g = n_q * SPT;
+  const uint32_t warp = dev::warp_id();
+  const uint32_t lane = dev::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&map_q);
+    dev::tma_prefetch_desc(&map_do);
+    dev::mbar_init(kv_ready, 256);
+    for (int s2 = 0; s2 < NS; ++s2) {
+      dev::mbar_init(&in_full[s2], 1);
+      dev::mbar_init(&in_empty[s2], 1);
+    }
+    for (int s2 = 0; s2 < NB; ++s2) {
+      dev::mbar_init(&s_full[s2], 1);
+      dev::mbar_init(&p_ready[s2], 128);
+    }
+    dev::mbar_init(fin, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_dv = tmem, t_dk = tmem + 128, t_k = tmem + 256, t_v = tmem + 320;
+  auto buf = [&](int b) { return tmem + 384 + 32 * b; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < n_q; ++i) {
+        const int qt = kt + i, st = i % NS;
+        dev::mbar_wait(&in_empty[st], ((i / NS) & 1) ^ 1);
+        dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
+        for (int c = 0; c < NC; ++c) {
+          dev::tma_load_2d(smem + L::RQ_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q, &in_full[st],
+                           hh * D + c * 64, qt * TILE);
+          dev::tma_load_2d(smem + L::RD_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_do, &in_full[st],
+                           hh * D + c * 64, qt * TILE);
+        }
+        float* vec = reinterpret_cast<float*>(smem + L::VEC_OFF + st * 1024);
+        const long long off = static_cast<long long>(hh) * S + qt * TILE;
+        dev::bulk_load(vec, lse2 + off, 512, &in_full[st]);
+        dev::bulk_load(vec + 128, delta + off, 512, &in_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = dev::idesc_bf16_f32(128, Q16, false, false);
+    constexpr uint32_t idesc_g = dev::idesc_bf16_f32(128, D, false, true);
+    dev::mbar_wait_w(kv_ready, 0);
+    dev::tc_fence_after();
+    auto issue_sd = [&](int g) {
+      const int i = g / SPT, qq = g % SPT, b = g % NB, st = i % NS;
+      if (qq == 0) {
+        dev::mbar_wait_w(&in_full[st], (i / NS) & 1);
+        dev::tc_fence_after();
+      }
+      const uint32_t roff = qq * Q16 * 128;  // 16 rows of 128 B inside every 64-col chunk
+      const uint64_t qd = kmajor_base(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
+      const uint64_t dod = kmajor_base(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        dev::mma_bf16_ts_w(buf(b), t_k + kk * 8, kmajor_step(qd, kk), idesc_s, kk > 0);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        dev::mma_bf16_ts_w(buf(b) + 16, t_v + kk * 8, kmajor_step(dod, kk), idesc_s, kk > 0);
+      dev::mma_commit_w(&s_full[b]);
+    };
+    for (int g = 0; g < AHEAD && g < n_g; ++g) issue_sd(g);
+    for (int g = 0; g < n_g; ++g) {
+      if (g + AHEAD < n_g) issue_sd(g + AHEAD);  // into the buffer dK(g-1) read: in order behind it
+      const int i = g / SPT, qq = g % SPT, b = g % NB, st = i % NS;
+      dev::mbar_wait_w(&p_ready[b], (g / NB) & 1);
+      dev::tc_fence_after();
+      const uint32_t roff = qq * Q16 * 128;
+      const uint64_t qm = mnmajor_base_c<CHUNK_BYTES>(dev::smem_u32(smem + L::RQ_OFF + st * L::TILE_BYTES) + roff);
+      const uint64_t dom = mnmajor_base_c<CHUNK_BYTES>(dev::smem_u32(smem + L::RD_OFF + st * L::TILE_BYTES) + roff);
+      dev::mma_bf16_ts_w(t_dv, buf(b), dom, idesc_g, g != 0);
+      dev::mma_bf16_ts_w(t_dk, buf(b) + 16, qm, idesc_g, g != 0);
+      if (qq == SPT - 1) dev::mma_commit_w(&in_empty[st]);
+    }
+    dev::mma_commit_w(fin);
+  } else if (warp >= 4) {
+    const uint32_t q4 = warp & 3;
+    const int grp = (warp - 4) >> 2;  // this group takes steps g with g % 2 == grp
+    const int r = q4 * 32 + lane;     // key row in tile
+    const int kidx = kt * TILE + r;
+    const uint32_t lane_off = (q4 * 32) << 16;
+    const long long hcols = static_cast<long long>(H) * D;
+    // K (group 0) / V (group 1) row r -> TMEM A operand
+    row_to_tmem<D>((grp == 0 ? kg : vg) + kidx * hcols + hh * D, (grp == 0 ? t_k : t_v) + lane_off);
+    dev::tmem_st_wait();
+    dev::tc_fence_before();
+    dev::mbar_arrive(kv_ready);
+    for (int g = grp; g < n_g; g += 2) {
+      const int i = g / SPT, qq = g % SPT, b = g % NB, st = i % NS;
+      if (qq < 2) dev::mbar_wait(&in_full[st], (i / NS) & 1);
+      const uint32_t l2 = dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * Q16) * 4;
+      const uint32_t dl = l2 + 512;
+      float4 lvv[4], dvv[4];
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        lvv[j4] = dev::lds_f4(l2 + 16 * j4);
+        dvv[j4] = dev::lds_f4(dl + 16 * j4);
+      }
+      dev::mbar_wait(&s_full[b], (g / NB) & 1);
+      dev::tc_fence_after();
+      uint32_t sr[16], dr[16];
+      dev::tmem_ld16(buf(b) + lane_off, sr);
+      dev::tmem_ld16(buf(b) + lane_off + 16, dr);
+      // no wait::ld: the P^T/dS^T stores below depend on every loaded value
+      uint32_t pp[8], dd[8];
+      auto body = [&](auto diag_tag) {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 lv = lvv[j4];
+          const float4 dv4 = dvv[j4];
+          const float lq[4] = {lv.x, lv.y, lv.z, lv.w};
+          const float dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+          float p4[4], d4[4];
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const uint64_t x2 = ffma2_v(f2_pack(__uint_as_float(sr[4 * j4 + e]), __uint_as_float(sr[4 * j4 + e + 1])),
+                                        scale_log2, f2_pack(lq[e], lq[e + 1]));
+            float pa = dev::ex2(f2_lo(x2));
+            float pb = dev::ex2(f2_hi(x2));
+            if (DIAG && qq * Q16 + 4 * j4 + e < r) pa = 0.f;
+            if (DIAG && qq * Q16 + 4 * j4 + e + 1 < r) pb = 0.f;
+            const uint64_t d2 = fmul2(f2_pack(pa, pb),
+                                      fadd2(f2_pack(__uint_as_float(dr[4 * j4 + e]), __uint_as_float(dr[4 * j4 + e + 1])),
+                                            f2_pack(dq4[e], dq4[e + 1])));
+            p4[e] = pa;
+            p4[e + 1] = pb;
+            d4[e] = f2_lo(d2);
+            d4[e + 1] = f2_hi(d2);
+          }
+          pp[2 * j4] = dev::pack_bf16(p4[0], p4[1]);
+          pp[2 * j4 + 1] = dev::pack_bf16(p4[2], p4[3]);
+          dd[2 * j4] = dev::pack_bf16(d4[0], d4[1]);
+          dd[2 * j4 + 1] = dev::pack_bf16(d4[2], d4[3]);
+        }
+      };
+      if (i == 0)
+        body(std::true_type{});
+      else
+        body(std::false_type{});
+      dev::tmem_st8(buf(b) + lane_off, pp);
+      dev::tmem_st8(buf(b) + lane_off + 16, dd);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_ready[b]);
+    }
+    dev::mbar_wait(fin, 0);
+    dev::tc_fence_after();
+    __nv_bfloat16* dvrow = dv + static_cast<long long>(kidx) * ld + hh * D;
+    __nv_bfloat16* dkrow = dk + static_cast<long long>(kidx) * ld + hh * D;
+#pragma unroll 1
+    for (int c = grp; c < D / 32; c += 2) {  // 32-column chunks of dV/dK spread over the two groups
+      uint32_t r32[32];
+      float x[32];
+      dev::tmem_ld32(t_dv + lane_off + c * 32, r32);
+      dev::tmem_ld_wait_regs(r32);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dvrow + c * 32, x, 1.f, nullptr);
+      dev::tmem_ld32(t_dk + lane_off + c * 32, r32);
+      dev::tmem_ld_wait_regs(r32);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(r32[e]);
+      store_grad32(dkrow + c * 32, x, scale, rope ? rope + (pos0 + kidx) * (D / 2) + c * 16 : nullptr);
+    }
+    dev::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------ dK/dV, decoupled P/dS
 // Ablation (measured 12 % SLOWER at 128K than attn_bwd_dkdv_tm_kernel<D, 2>:
 // 231-232 vs 206-207 ms, H=32, D=128, interleaved runs).  Same math and operands as attn_bwd_dkdv_tm_kernel
@@ -3605,6 +3827,17 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   // S^T/dP^T buffer (attn_bwd_dkdv_tm2_kernel: 231-232 vs 206-207 ms at 128K),
   // 8/9 one-step Q/dO stages (TS = 12 / 8)
   switch (abl_env("MEMO_ATTN_DKDV_VARIANT", 0)) {
+    case 10: {  // 16-query steps, four S/dP buffers (N=16 MMAs run at 79 %: 268 vs 206 ms)
+      static std::once_flag f16;
+      std::call_once(f16, [] {
+        cudaFuncSetAttribute(attn_bwd_dkdv_q16_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DkdvTmSmem<D>::BYTES);
+      });
+      attn_bwd_dkdv_q16_kernel<D><<<grid, 32 * 12, DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
+    }
     case 8:
     case 9: {
       // one-step Q/dO stages (TS = 12 / 8): loads run TS-1 steps ahead

@@ -77,6 +77,7 @@ int main() {
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
   long long* d;
   cudaMalloc(&d, n_sm * sizeof(long long));
+  run<16, true>(d, n_sm);
   run<32, true>(d, n_sm);
   run<64, true>(d, n_sm);
   run<128, true>(d, n_sm);
