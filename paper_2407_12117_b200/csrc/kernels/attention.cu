@@ -2194,7 +2194,12 @@ struct DkdvTsSmem {
 // EMU: every EMU-th column pair's exponentials run on the FMA pipe (exp2_fma)
 // instead of MUFU.EX2 (0: none).  The MUFU is the largest single item of the
 // compute warps' per-step critical path (tools/dkdv_prof.py).
-template <int D, int WPQ, int EMU = 0, bool SPLIT = false, int TS = 0>
+// CL2: CTA pairs (clusters of 2) on key tiles 2p, 2p+1 of one head share each
+// Q/dO tile by TMA multicast (each CTA loads one 64-column chunk of both, for
+// both CTAs); the upper key tile walks query tile 2p too, fully masked (P = 0,
+// dS = 0), so both CTAs consume the same stages.  A stage is refilled once both
+// CTAs' MMAs have released it.
+template <int D, int WPQ, int EMU = 0, bool SPLIT = false, int TS = 0, bool CL2 = false>
 __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     attn_bwd_dkdv_tm_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
                             const __grid_constant__ CUtensorMap map_q,
@@ -2223,10 +2228,13 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   constexpr int CW = 32 * 4 * WPQ;
   constexpr int COLS = QSTEP / WPQ;  // query columns per compute warp per step
 
+  static_assert(!CL2 || TS == 0, "CL2 shares whole Q/dO tiles");
   const int n_tiles = S / TILE;
   const int kt = blockIdx.x;  // key tile
   const int hh = blockIdx.y;
-  const int n_q = n_tiles - kt;
+  const uint32_t crank = CL2 ? dev::cluster_ctarank() : 0u;  // rank 1 holds the upper key tile
+  const int q_first = kt - static_cast<int>(crank);          // first query tile walked
+  const int n_q = n_tiles - q_first;
   const int n_g = n_q * (TILE / QSTEP);
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
@@ -2237,7 +2245,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     dev::mbar_init(kv_ready, CW);
     for (int s2 = 0; s2 < NS; ++s2) {
       dev::mbar_init(&in_full[s2], 1);
-      dev::mbar_init(&in_empty[s2], 1);
+      dev::mbar_init(&in_empty[s2], CL2 ? 2 : 1);  // CL2: both CTAs' MMAs release a stage
     }
     for (int s2 = 0; s2 < 2; ++s2) {
       dev::mbar_init(&s_full[s2], 1);
@@ -2249,7 +2257,10 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   }
   if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
   dev::tc_fence_before();
-  __syncthreads();
+  if (CL2)
+    dev::cluster_sync();  // the peer's barriers exist before its first multicast lands here
+  else
+    __syncthreads();
   dev::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_dv = tmem, t_dk = tmem + 128, t_k = tmem + 256, t_v = tmem + 320;
@@ -2278,12 +2289,27 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         }
       } else
       for (int i = 0; i < n_q; ++i) {
-        const int qt = kt + i, st = i % NS;
+        const int qt = q_first + i, st = i % NS;
         MEMO_PROF(long long pe = clock64();)
         dev::mbar_wait(&in_empty[st], ((i / NS) & 1) ^ 1);
         MEMO_PROF(if (i >= NS) pe_acc += clock64() - pe;)
         dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
         MEMO_PROF(pf_issue[st] = clock64();)
+        if (CL2) {  // half of Q_qt and dO_qt, to both CTAs
+          if (NC == 2) {  // D = 128: this CTA's 64-column chunk of each
+            const int c = static_cast<int>(crank);
+            dev::tma_load_2d_mc(smem + L::RQ_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q, &in_full[st],
+                                hh * D + c * 64, qt * TILE, 0x3);
+            dev::tma_load_2d_mc(smem + L::RD_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_do, &in_full[st],
+                                hh * D + c * 64, qt * TILE, 0x3);
+          } else if (crank == 0) {  // D = 64: one CTA loads Q, the other dO
+            dev::tma_load_2d_mc(smem + L::RQ_OFF + st * L::TILE_BYTES, &map_q, &in_full[st], hh * D, qt * TILE,
+                                0x3);
+          } else {
+            dev::tma_load_2d_mc(smem + L::RD_OFF + st * L::TILE_BYTES, &map_do, &in_full[st], hh * D, qt * TILE,
+                                0x3);
+          }
+        } else
         for (int c = 0; c < NC; ++c) {
           dev::tma_load_2d(smem + L::RQ_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q, &in_full[st],
                            hh * D + c * 64, qt * TILE);
@@ -2294,6 +2320,9 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         const long long off = static_cast<long long>(hh) * S + qt * TILE;
         dev::bulk_load(vec, lse2 + off, 512, &in_full[st]);
         dev::bulk_load(vec + 128, delta + off, 512, &in_full[st]);
+      }
+      if (CL2) {  // producer tail: the peer's releases of the last stages land here asynchronously
+        for (int i = n_q; i < n_q + NS; ++i) dev::mbar_wait(&in_empty[i % NS], ((i / NS) & 1) ^ 1);
       }
       MEMO_PROF(atomicAdd(&g_dkdv_prof[14], static_cast<unsigned long long>(pe_acc));)
     }
@@ -2373,7 +2402,12 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         for (int kk = 0; kk < QSTEP / 16; ++kk)
           dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(qm, kk), idesc_g,
                              (g | kk) != 0);
-        if (TS > 0 || qq == 3) dev::mma_commit_w(&in_empty[st]);
+        if (TS > 0 || qq == 3) {
+          if (CL2)
+            dev::mma_commit_mc_w(&in_empty[st], 0x3);  // the stage holds both CTAs' chunks
+          else
+            dev::mma_commit_w(&in_empty[st]);
+        }
       }
       dev::mma_commit_w(fin);
       MEMO_PROF(if (lane == 0) {
@@ -2400,7 +2434,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     for (int g = 0; g < n_g; ++g) {
       const int i = g >> 2, qq = g & 3, b = g & 1;
       const int st = TS > 0 ? g % NS : i % NS;
-      const bool diag = i == 0;
+      const bool diag = i == static_cast<int>(crank);
       if (TS > 0 || qq == 0) dev::mbar_wait(&in_full[st], TS > 0 ? (g / NS) & 1 : (i / NS) & 1);
       const uint32_t l2 = TS > 0 ? dev::smem_u32(smem + L::VEC_OFF + st * 256) + (COLS * ch) * 4
                                  : dev::smem_u32(smem + L::VEC_OFF + st * 1024) + (qq * QSTEP + COLS * ch) * 4;
@@ -2417,6 +2451,18 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       MEMO_PROF(long long prof_t1 = clock64(); cp_acc[2] += prof_t1 - prof_t0;)
       dev::tc_fence_after();
+      if (CL2 && i < static_cast<int>(crank)) {  // the pair's extra query tile: fully masked
+        static_assert(!CL2 || (COLS == 16 && !SPLIT), "CL2: the default compute layout only");
+        uint32_t z[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) z[e] = 0u;
+        dev::tmem_st8(buf(b) + lane_off + 16 * ch, z);
+        dev::tmem_st8(buf(b) + lane_off + 32 + 16 * ch, z);
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&p_ready[b]);
+        continue;
+      }
       uint32_t sr[COLS], dr[COLS];
       if constexpr (COLS == 16) {
         dev::tmem_ld16(buf(b) + lane_off + 16 * ch, sr);
@@ -2577,7 +2623,10 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     }
     dev::tc_fence_before();
   }
-  __syncthreads();
+  if (CL2)
+    dev::cluster_sync();  // no multicast or remote release still targets this CTA
+  else
+    __syncthreads();
   if (warp == 1) {
     dev::tc_fence_after();
     dev::tmem_dealloc(tmem, 512);
@@ -3796,6 +3845,8 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
 #ifdef MEMO_ATTN_ABLATIONS
     cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3819,6 +3870,11 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   const float scale_log2 = a.softmax_scale * kLog2e;
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   dim3 grid(a.S / TILE, a.H);
+#ifdef MEMO_ATTN_ABLATIONS
+  // MEMO_ATTN_DKDV_CL2=1: CTA pairs on key tiles 2p, 2p+1 sharing Q/dO by
+  // multicast (bitwise equal, 8 % SLOWER at 128K: 224.6-226.4 vs 208.5-211.2 ms)
+  const bool dkdv_cl2 = (a.S / TILE) % 2 == 0 && abl_env("MEMO_ATTN_DKDV_CL2", 0) == 1;
+#endif
   if (a.ev[1]) record_timing_event(a.ev[1], stream);
 #ifdef MEMO_ATTN_ABLATIONS
   // MEMO_ATTN_DKDV_VARIANT: 1 K/V in shared memory, 2 four warps per lane
@@ -3891,6 +3947,25 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
           scale_log2);
       break;
     default:
+      if (dkdv_cl2) {  // CTA pairs sharing each Q/dO tile by multicast
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(32 * (4 + 8));
+        cfg.dynamicSmemBytes = DkdvTmSmem<D>::BYTES;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true>, a.k, a.v,
+                                                 mq, mdo, (const float*)lse2, (const float*)delta, a.dk, a.dv,
+                                                 a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale, scale_log2);
+        if (e != cudaSuccess) return e;
+        break;
+      }
 #endif
       attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
           a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
