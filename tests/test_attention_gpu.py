@@ -87,7 +87,11 @@ def _rel(a, b):
     return ((a.float() - b.float()).norm() / b.float().norm()).item()
 
 
-@pytest.mark.parametrize("S,H,D", [(128, 1, 128), (256, 2, 128), (512, 2, 64), (1024, 2, 128)])
+# Even tile counts run the dQ kernel as CTA pairs sharing K/V (D=128: a chunk of
+# each per CTA; D=64: K from one CTA, V from the other); odd counts (128, 384,
+# 640) run one CTA per query tile.
+@pytest.mark.parametrize("S,H,D", [(128, 1, 128), (256, 2, 128), (512, 2, 64), (1024, 2, 128), (384, 2, 128),
+                                   (640, 1, 64)])
 def test_attn_bwd(S, H, D):
     torch.manual_seed(11 + S + D)
     q = torch.randn(S, H * D, device="cuda").to(torch.bfloat16)
