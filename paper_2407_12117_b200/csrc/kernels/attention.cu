@@ -2199,7 +2199,13 @@ struct DkdvTsSmem {
 // both CTAs); the upper key tile walks query tile 2p too, fully masked (P = 0,
 // dS = 0), so both CTAs consume the same stages.  A stage is refilled once both
 // CTAs' MMAs have released it.
-template <int D, int WPQ, int EMU = 0, bool SPLIT = false, int TS = 0, bool CL2 = false>
+// QH (ablation build): P^T/dS^T released per 16-query half (warp ch = 0 / 1 of
+// each lane quarter on its own barrier), so dV/dK over the first half can run
+// under the second half's math; QH = 2 also makes the two warps of an SMSP take
+// turns on the exponentials (ch 1 starts its MUFU work when ch 0 has issued
+// its own).  Bitwise equal; at 128K QH = 1 is within noise of the default
+// (205.4-206.1 vs 205.6-207.0 ms) and QH = 2 is 3 % slower (210.7-212.5 ms).
+template <int D, int WPQ, int EMU = 0, bool SPLIT = false, int TS = 0, bool CL2 = false, int QH = 0>
 __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     attn_bwd_dkdv_tm_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
                             const __grid_constant__ CUtensorMap map_q,
@@ -2249,8 +2255,8 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     }
     for (int s2 = 0; s2 < 2; ++s2) {
       dev::mbar_init(&s_full[s2], 1);
-      dev::mbar_init(&p_ready[s2], CW);
-      dev::mbar_init(&ds_ready[s2], CW);
+      dev::mbar_init(&p_ready[s2], QH ? CW / 2 : CW);   // QH: queries [0,16) of the step
+      dev::mbar_init(&ds_ready[s2], QH ? CW / 2 : CW);  // QH: queries [16,32); SPLIT: dS^T written
     }
     dev::mbar_init(fin, 1);
     dev::fence_barrier_init();
@@ -2391,6 +2397,17 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         const uint32_t sbytes = TS > 0 ? L::STAGE_BYTES : L::TILE_BYTES;
         const uint64_t qm = mnmajor_base_c<L::CH_BYTES>(dev::smem_u32(smem + L::RQ_OFF + st * sbytes) + roff);
         const uint64_t dom = mnmajor_base_c<L::CH_BYTES>(dev::smem_u32(smem + L::RD_OFF + st * sbytes) + roff);
+        if constexpr (QH) {  // one query half at a time: dV then dK per 16-query k-step
+#pragma unroll
+          for (int kk = 0; kk < QSTEP / 16; ++kk) {
+            if (kk > 0) {
+              dev::mbar_wait_w(&ds_ready[b], (g >> 1) & 1);
+              dev::tc_fence_after();
+            }
+            dev::mma_bf16_ts_w(t_dv, buf(b) + 16 * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
+            dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + 16 * kk, mnmajor_step(qm, kk), idesc_g, (g | kk) != 0);
+          }
+        } else {
 #pragma unroll
         for (int kk = 0; kk < QSTEP / 16; ++kk)
           dev::mma_bf16_ts_w(t_dv, buf(b) + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(dom, kk), idesc_g, (g | kk) != 0);
@@ -2402,6 +2419,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         for (int kk = 0; kk < QSTEP / 16; ++kk)
           dev::mma_bf16_ts_w(t_dk, buf(b) + 32 + (WPQ == 4 ? 8 : 16) * kk, mnmajor_step(qm, kk), idesc_g,
                              (g | kk) != 0);
+        }
         if (TS > 0 || qq == 3) {
           if (CL2)
             dev::mma_commit_mc_w(&in_empty[st], 0x3);  // the stage holds both CTAs' chunks
@@ -2478,6 +2496,16 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       if constexpr (COLS != 16) dev::tmem_ld_wait_regs(sr, dr);
       MEMO_PROF(cp_acc[6] += clock64() - prof_t1;)
       uint32_t pp[COLS / 2], dd[COLS / 2];
+      float scl = scale_log2;
+      const int turn_bar = 1 + static_cast<int>(q4) + 4 * (g & 1);  // per SMSP, alternating by step parity
+      if constexpr (QH) {
+        static_assert(!QH || (COLS == 16 && !SPLIT && TS == 0), "QH: the default compute layout only");
+        if (QH == 2 && ch == 1) {  // ch 0's exponentials first: every exponential below depends on this barrier
+          uint32_t zero;
+          asm volatile("bar.sync %1, 64;\n\tmov.b32 %0, 0;" : "=r"(zero) : "r"(turn_bar) : "memory");
+          scl += __uint_as_float(zero);
+        }
+      }
       auto body = [&](auto diag_tag) {
         constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
@@ -2490,7 +2518,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
 #pragma unroll
           for (int e = 0; e < 4; e += 2) {  // column pairs: FFMA2 / FADD2 / FMUL2
             const uint64_t x2 = ffma2_v(f2_pack(__uint_as_float(sr[4 * j4 + e]), __uint_as_float(sr[4 * j4 + e + 1])),
-                                        scale_log2, f2_pack(lq[e], lq[e + 1]));
+                                        scl, f2_pack(lq[e], lq[e + 1]));
             float pa, pb;
             if (EMU && ((2 * j4 + (e >> 1)) % (EMU ? EMU : 1)) == EMU - 1) {
               const uint64_t e2 = exp2_fma2(x2);
@@ -2581,6 +2609,10 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         body(std::true_type{});
       else
         body(std::false_type{});
+      if constexpr (QH) {
+        if (QH == 2 && ch == 0)  // after its last exponential (the packed P depends on all of them)
+          asm volatile("bar.arrive %0, 64;" ::"r"(turn_bar), "r"(pp[COLS / 2 - 1]) : "memory");
+      }
       if constexpr (COLS == 16) {
         // packed bf16 stays inside this warp's own 16-column slice
         dev::tmem_st8(buf(b) + lane_off + 16 * ch, pp);
@@ -2597,7 +2629,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       dev::tmem_st_wait();
       MEMO_PROF(cp_acc[7] += clock64() - prof_t2;)
       dev::tc_fence_before();
-      dev::mbar_arrive(&p_ready[b]);
+      dev::mbar_arrive(QH && ch == 1 ? &ds_ready[b] : &p_ready[b]);
       MEMO_PROF(cp_acc[3] += clock64() - prof_t1;)
     }
     MEMO_PROF(if (warp == 4 && lane == 0) for (int k2 : {2, 3, 6, 7})
@@ -3847,6 +3879,10 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
                          BwdSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, false, 2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTmSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, false, 1>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3883,6 +3919,16 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   // S^T/dP^T buffer (attn_bwd_dkdv_tm2_kernel: 231-232 vs 206-207 ms at 128K),
   // 8/9 one-step Q/dO stages (TS = 12 / 8)
   switch (abl_env("MEMO_ATTN_DKDV_VARIANT", 0)) {
+    case 12:
+      attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, false, 1><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
+    case 11:
+      attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, false, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+          scale_log2);
+      break;
     case 10: {  // 16-query steps, four S/dP buffers (N=16 MMAs run at 79 %: 268 vs 206 ms)
       static std::once_flag f16;
       std::call_once(f16, [] {
