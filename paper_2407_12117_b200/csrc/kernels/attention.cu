@@ -776,8 +776,12 @@ __device__ unsigned long long g_fwd_prof[24];
 // while the other three loads are in flight.  Safe here because nothing
 // reuses S's columns before this thread's P stores, which depend on every
 // loaded value.  0.5-1 % at 128K, bitwise equal (LDSB = false: ablation 33).
+// CL2 (the default when the pair count is even): CTA pairs (clusters of 2) on query-tile pairs pp and
+// pp-1 of one head share every K/V tile by multicast (each CTA loads one
+// 64-column chunk of K_j and of V_j for both); the lower CTA releases the upper
+// one's two extra key tiles without computing on them.
 template <int EMU_EVERY, bool SPLIT_P = true, bool NULL_SM = false, bool NULL_MMA = false, bool SEQ = false,
-          bool QSTORE = false, bool LDSB = true>
+          bool QSTORE = false, bool LDSB = true, bool CL2 = false>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ out,
@@ -804,6 +808,8 @@ __global__ void __launch_bounds__(384, 1)
   const int hh = blockIdx.y;
   const int qt0 = 2 * pp;
   const int n_kv = qt0 + 2;  // key tiles of group B; group A uses n_kv - 1
+  const uint32_t crank = CL2 ? dev::cluster_ctarank() : 0u;  // rank 1 holds the lower query-tile pair
+  const int n_load = n_kv + 2 * static_cast<int>(crank);    // key tiles the pair walks together
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
 
@@ -814,9 +820,9 @@ __global__ void __launch_bounds__(384, 1)
     dev::mbar_init(q_full, 1);
     for (int s2 = 0; s2 < 2; ++s2) {
       dev::mbar_init(&k_full[s2], 1);
-      dev::mbar_init(&k_empty[s2], 1);
+      dev::mbar_init(&k_empty[s2], CL2 ? 2 : 1);  // CL2: both CTAs release a stage
       dev::mbar_init(&v_full[s2], 1);
-      dev::mbar_init(&v_empty[s2], 1);
+      dev::mbar_init(&v_empty[s2], CL2 ? 2 : 1);
       dev::mbar_init(&s_full[s2], 1);
       dev::mbar_init(&p_full[2 * s2], 128);
       dev::mbar_init(&p_full[2 * s2 + 1], 128);
@@ -826,7 +832,10 @@ __global__ void __launch_bounds__(384, 1)
   }
   if (warp == 1) dev::tmem_alloc(tmem_slot, 512);
   dev::tc_fence_before();
-  __syncthreads();
+  if (CL2)
+    dev::cluster_sync();  // the peer's barriers exist before its first multicast lands here
+  else
+    __syncthreads();
   dev::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -839,19 +848,36 @@ __global__ void __launch_bounds__(384, 1)
           dev::tma_load_2d(smem + L::QA_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, qt0 * TILE);
           dev::tma_load_2d(smem + L::QB_OFF + c * CHUNK_BYTES, &map_q, q_full, hh * D + c * 64, (qt0 + 1) * TILE);
         }
-        for (int j = 0; j < n_kv; ++j) {
+        for (int j = 0; j < n_load; ++j) {
           const int st = j & 1;
           const uint32_t ph = (j >> 1) & 1;
+          const int c0 = CL2 ? static_cast<int>(crank) : 0, c1 = CL2 ? c0 + 1 : NC;  // CL2: this CTA's chunk
           dev::mbar_wait(&k_empty[st], ph ^ 1);
           dev::mbar_expect_tx(&k_full[st], L::TILE_BYTES);
-          for (int c = 0; c < NC; ++c)
-            dev::tma_load_2d(smem + L::K_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_k, &k_full[st],
-                             hh * D + c * 64, j * TILE);
+          for (int c = c0; c < c1; ++c) {
+            if (CL2)
+              dev::tma_load_2d_mc(smem + L::K_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_k, &k_full[st],
+                                  hh * D + c * 64, j * TILE, 0x3);
+            else
+              dev::tma_load_2d(smem + L::K_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_k, &k_full[st],
+                               hh * D + c * 64, j * TILE);
+          }
           dev::mbar_wait(&v_empty[st], ph ^ 1);
           dev::mbar_expect_tx(&v_full[st], L::TILE_BYTES);
-          for (int c = 0; c < NC; ++c)
-            dev::tma_load_2d(smem + L::V_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_v, &v_full[st],
-                             hh * D + c * 64, j * TILE);
+          for (int c = c0; c < c1; ++c) {
+            if (CL2)
+              dev::tma_load_2d_mc(smem + L::V_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_v, &v_full[st],
+                                  hh * D + c * 64, j * TILE, 0x3);
+            else
+              dev::tma_load_2d(smem + L::V_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_v, &v_full[st],
+                               hh * D + c * 64, j * TILE);
+          }
+        }
+        if (CL2) {  // producer tail: the peer's releases of the last stages land here asynchronously
+          for (int j = n_load; j < n_load + 2; ++j) {
+            dev::mbar_wait(&k_empty[j & 1], ((j >> 1) & 1) ^ 1);
+            dev::mbar_wait(&v_empty[j & 1], ((j >> 1) & 1) ^ 1);
+          }
         }
       }
     } else if (warp == 1) {
@@ -878,7 +904,12 @@ __global__ void __launch_bounds__(384, 1)
             dev::mma_bf16_ss_w(tmem + g * 128, kmajor_step(g ? qd[1] : qd[0], kk), kmajor_step(kd, kk), idesc_s,
                                kk > 0);
         dev::mma_commit_w(&s_full[g]);
-        if (g == 1) dev::mma_commit_w(&k_empty[st]);  // B is the last reader of K_j
+        if (g == 1) {  // B is the last reader of K_j
+          if (CL2)
+            dev::mma_commit_mc_w(&k_empty[st], 0x3);
+          else
+            dev::mma_commit_w(&k_empty[st]);
+        }
       };
       auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j, one key half at a time
         const int st = j & 1;
@@ -910,7 +941,12 @@ __global__ void __launch_bounds__(384, 1)
         // S_g(j+1) is issued after PV_g(j), so s_full already orders the
         // softmax's O rescale after PV_g(j); o_done only serves the epilogue.
         if (j == (g ? n_kv - 1 : nA - 1)) dev::mma_commit_w(&o_done[g]);
-        if (g == 1) dev::mma_commit_w(&v_empty[st]);
+        if (g == 1) {
+          if (CL2)
+            dev::mma_commit_mc_w(&v_empty[st], 0x3);
+          else
+            dev::mma_commit_w(&v_empty[st]);
+        }
       };
       issue_s(0, 0);
       issue_s(1, 0);
@@ -921,6 +957,15 @@ __global__ void __launch_bounds__(384, 1)
         }
         issue_pv(1, j);
         if (j + 1 < n_kv) issue_s(1, j + 1);
+      }
+      if (CL2) {  // the upper pair's two extra key tiles: release them for the peer, no MMAs
+        for (int j = n_kv; j < n_load; ++j) {
+          const int st = j & 1;
+          dev::mbar_wait_w(&k_full[st], (j >> 1) & 1);
+          dev::mma_commit_mc_w(&k_empty[st], 0x3);
+          dev::mbar_wait_w(&v_full[st], (j >> 1) & 1);
+          dev::mma_commit_mc_w(&v_empty[st], 0x3);
+        }
       }
       FWD_PROF(if (lane == 0) {
         atomicAdd(&g_fwd_prof[16], static_cast<unsigned long long>(pf_p));
@@ -1178,7 +1223,10 @@ __global__ void __launch_bounds__(384, 1)
     lse[static_cast<long long>(hh) * S + qidx] = (m + log2f(l)) * kLn2;
     dev::tc_fence_before();
   }
-  __syncthreads();
+  if (CL2)
+    dev::cluster_sync();  // no multicast or remote release still targets this CTA
+  else
+    __syncthreads();
   if (warp == 1) {
     dev::tc_fence_after();
     dev::tmem_dealloc(tmem, 512);
@@ -4204,7 +4252,35 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
     return cudaGetLastError();
   }
 #endif
-  if (a.D == 128 && a.S % (2 * TILE) == 0) {
+  bool fwd_cl2 = a.S % (4 * TILE) == 0;
+#ifdef MEMO_ATTN_ABLATIONS
+  fwd_cl2 = fwd_cl2 && abl_env("MEMO_ATTN_FWD_CL2", 1) == 1;
+#endif
+  if (a.D == 128 && fwd_cl2) {
+    // ping-pong on CTA pairs (clusters of 2) sharing each K/V tile by multicast
+    // whenever the query-tile pairs come in pairs: bitwise equal to one CTA per
+    // pair, 0.7 % faster at 128K (ablation build: MEMO_ATTN_FWD_CL2=0 -> one CTA)
+    static std::once_flag fcl;
+    std::call_once(fcl, [] {
+      cudaFuncSetAttribute(attn_fwd_pp_kernel<3, true, false, false, false, false, true, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+    });
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.S / (2 * TILE), a.H);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = FwdPpSmem::BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_fwd_pp_kernel<3, true, false, false, false, false, true, true>,
+                                             mq, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
+    if (e != cudaSuccess) return e;
+  } else if (a.D == 128 && a.S % (2 * TILE) == 0) {
     // ping-pong: two query tiles per CTA, setmaxnreg, 1/3 of the exponentials
     // on the FMA pipe (paired exp2_fma2)
     static std::once_flag f8;
