@@ -808,7 +808,9 @@ __global__ void __launch_bounds__(384, 1)
   const int hh = blockIdx.y;
   const int qt0 = 2 * pp;
   const int n_kv = qt0 + 2;  // key tiles of group B; group A uses n_kv - 1
-  const uint32_t crank = CL2 ? dev::cluster_ctarank() : 0u;  // rank 1 holds the lower query-tile pair
+  // rank in the 1-D cluster of 2 = blockIdx.x & 1 (rank 1 holds the lower query-tile pair); derived from
+  // blockIdx (not %cluster_ctarank) so ptxas keeps the loop state uniform
+  const uint32_t crank = CL2 ? (blockIdx.x & 1u) : 0u;
   const int n_load = n_kv + 2 * static_cast<int>(crank);    // key tiles the pair walks together
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
@@ -2242,18 +2244,19 @@ struct DkdvTsSmem {
 // EMU: every EMU-th column pair's exponentials run on the FMA pipe (exp2_fma)
 // instead of MUFU.EX2 (0: none).  The MUFU is the largest single item of the
 // compute warps' per-step critical path (tools/dkdv_prof.py).
-// CL2: CTA pairs (clusters of 2) on key tiles 2p, 2p+1 of one head share each
-// Q/dO tile by TMA multicast (each CTA loads one 64-column chunk of both, for
-// both CTAs); the upper key tile walks query tile 2p too, fully masked (P = 0,
-// dS = 0), so both CTAs consume the same stages.  A stage is refilled once both
-// CTAs' MMAs have released it.
+// CL2 (the default for an even tile count): CTA pairs (clusters of 2) on key
+// tiles 2p, 2p+1 of one head share each Q/dO tile by TMA multicast (each CTA
+// loads one 64-column chunk of both, for both CTAs); the upper key tile walks
+// query tile 2p too, fully masked (P = 0, dS = 0), so both CTAs consume the
+// same stages.  A stage is refilled once both CTAs' MMAs have released it.
 // QH (ablation build): P^T/dS^T released per 16-query half (warp ch = 0 / 1 of
 // each lane quarter on its own barrier), so dV/dK over the first half can run
 // under the second half's math; QH = 2 also makes the two warps of an SMSP take
 // turns on the exponentials (ch 1 starts its MUFU work when ch 0 has issued
 // its own).  Bitwise equal; at 128K QH = 1 is within noise of the default
 // (205.4-206.1 vs 205.6-207.0 ms) and QH = 2 is 3 % slower (210.7-212.5 ms).
-template <int D, int WPQ, int EMU = 0, bool SPLIT = false, int TS = 0, bool CL2 = false, int QH = 0>
+template <int D, int WPQ, int EMU = 0, bool SPLIT = false, int TS = 0, bool CL2 = false, int QH = 0,
+          bool CLNOMC = false>
 __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     attn_bwd_dkdv_tm_kernel(const __nv_bfloat16* __restrict__ kg, const __nv_bfloat16* __restrict__ vg,
                             const __grid_constant__ CUtensorMap map_q,
@@ -2282,11 +2285,12 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
   constexpr int CW = 32 * 4 * WPQ;
   constexpr int COLS = QSTEP / WPQ;  // query columns per compute warp per step
 
-  static_assert(!CL2 || TS == 0, "CL2 shares whole Q/dO tiles");
   const int n_tiles = S / TILE;
   const int kt = blockIdx.x;  // key tile
   const int hh = blockIdx.y;
-  const uint32_t crank = CL2 ? dev::cluster_ctarank() : 0u;  // rank 1 holds the upper key tile
+  // rank in the 1-D cluster of 2 = blockIdx.x & 1 (rank 1 holds the upper key tile); derived from
+  // blockIdx (not %cluster_ctarank) so ptxas keeps the loop state uniform
+  const uint32_t crank = CL2 ? (blockIdx.x & 1u) : 0u;
   const int q_first = kt - static_cast<int>(crank);          // first query tile walked
   const int n_q = n_tiles - q_first;
   const int n_g = n_q * (TILE / QSTEP);
@@ -2327,10 +2331,17 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       if constexpr (TS > 0) {
         for (int g = 0; g < n_g; ++g) {
           const int st = g % NS;
-          const int q0 = (kt + (g >> 2)) * TILE + (g & 3) * QSTEP;  // first query of the step
+          const int q0 = (q_first + (g >> 2)) * TILE + (g & 3) * QSTEP;  // first query of the step
           dev::mbar_wait(&in_empty[st], ((g / NS) & 1) ^ 1);
           dev::mbar_expect_tx(&in_full[st], 2 * L::STAGE_BYTES + 2 * QSTEP * 4);
-          for (int c = 0; c < NC; ++c) {
+          for (int c = CL2 ? static_cast<int>(crank) : 0; c < (CL2 ? static_cast<int>(crank) + 1 : NC); ++c) {
+            if (CL2) {  // this CTA's 64-column chunk of the step's Q and dO slices, to both CTAs
+              dev::tma_load_2d_mc(smem + L::RQ_OFF + st * L::STAGE_BYTES + c * L::CH_BYTES, &map_q, &in_full[st],
+                                  hh * D + c * 64, q0, 0x3);
+              dev::tma_load_2d_mc(smem + L::RD_OFF + st * L::STAGE_BYTES + c * L::CH_BYTES, &map_do, &in_full[st],
+                                  hh * D + c * 64, q0, 0x3);
+              continue;
+            }
             dev::tma_load_2d(smem + L::RQ_OFF + st * L::STAGE_BYTES + c * L::CH_BYTES, &map_q, &in_full[st],
                              hh * D + c * 64, q0);
             dev::tma_load_2d(smem + L::RD_OFF + st * L::STAGE_BYTES + c * L::CH_BYTES, &map_do, &in_full[st],
@@ -2349,7 +2360,7 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         MEMO_PROF(if (i >= NS) pe_acc += clock64() - pe;)
         dev::mbar_expect_tx(&in_full[st], 2 * L::TILE_BYTES + 1024);
         MEMO_PROF(pf_issue[st] = clock64();)
-        if (CL2) {  // half of Q_qt and dO_qt, to both CTAs
+        if (CL2 && !CLNOMC) {  // half of Q_qt and dO_qt, to both CTAs (CLNOMC: ablation, each loads all)
           if (NC == 2) {  // D = 128: this CTA's 64-column chunk of each
             const int c = static_cast<int>(crank);
             dev::tma_load_2d_mc(smem + L::RQ_OFF + st * L::TILE_BYTES + c * CHUNK_BYTES, &map_q, &in_full[st],
@@ -2376,7 +2387,8 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
         dev::bulk_load(vec + 128, delta + off, 512, &in_full[st]);
       }
       if (CL2) {  // producer tail: the peer's releases of the last stages land here asynchronously
-        for (int i = n_q; i < n_q + NS; ++i) dev::mbar_wait(&in_empty[i % NS], ((i / NS) & 1) ^ 1);
+        const int n_fill = TS > 0 ? n_g : n_q;
+        for (int i = n_fill; i < n_fill + NS; ++i) dev::mbar_wait(&in_empty[i % NS], ((i / NS) & 1) ^ 1);
       }
       MEMO_PROF(atomicAdd(&g_dkdv_prof[14], static_cast<unsigned long long>(pe_acc));)
     }
@@ -2497,7 +2509,24 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
     dev::tc_fence_before();
     dev::mbar_arrive(kv_ready);
     MEMO_PROF(long long cp_acc[8] = {};)
-    for (int g = 0; g < n_g; ++g) {
+    // CL2: the upper key tile's first query tile (shared with the lower one) is
+    // fully masked: P^T = dS^T = 0, peeled off so the main loop has no branch
+    const int g_start = CL2 ? static_cast<int>(crank) * (TILE / QSTEP) : 0;
+    for (int g = 0; g < g_start; ++g) {
+      static_assert(!CL2 || (COLS == 16 && !SPLIT), "CL2: the default compute layout only");
+      const int b = g & 1;
+      dev::mbar_wait(&s_full[b], (g >> 1) & 1);
+      dev::tc_fence_after();
+      uint32_t z[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) z[e] = 0u;
+      dev::tmem_st8(buf(b) + lane_off + 16 * ch, z);
+      dev::tmem_st8(buf(b) + lane_off + 32 + 16 * ch, z);
+      dev::tmem_st_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_ready[b]);
+    }
+    for (int g = g_start; g < n_g; ++g) {
       const int i = g >> 2, qq = g & 3, b = g & 1;
       const int st = TS > 0 ? g % NS : i % NS;
       const bool diag = i == static_cast<int>(crank);
@@ -2517,18 +2546,6 @@ __global__ void __launch_bounds__(32 * (4 + 4 * WPQ), 1)
       dev::mbar_wait(&s_full[b], (g >> 1) & 1);
       MEMO_PROF(long long prof_t1 = clock64(); cp_acc[2] += prof_t1 - prof_t0;)
       dev::tc_fence_after();
-      if (CL2 && i < static_cast<int>(crank)) {  // the pair's extra query tile: fully masked
-        static_assert(!CL2 || (COLS == 16 && !SPLIT), "CL2: the default compute layout only");
-        uint32_t z[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) z[e] = 0u;
-        dev::tmem_st8(buf(b) + lane_off + 16 * ch, z);
-        dev::tmem_st8(buf(b) + lane_off + 32 + 16 * ch, z);
-        dev::tmem_st_wait();
-        dev::tc_fence_before();
-        dev::mbar_arrive(&p_ready[b]);
-        continue;
-      }
       uint32_t sr[COLS], dr[COLS];
       if constexpr (COLS == 16) {
         dev::tmem_ld16(buf(b) + lane_off + 16 * ch, sr);
@@ -3223,7 +3240,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int n_tiles = S / TILE;
   const int qt = n_tiles - 1 - static_cast<int>(blockIdx.x);  // heavy tiles first
   const int hh = blockIdx.y;
-  const uint32_t crank = CL2 ? dev::cluster_ctarank() : 0u;  // rank 1 holds the lower tile
+  // rank in the 1-D cluster of 2 = blockIdx.x & 1 (rank 1 holds the lower tile); derived from
+  // blockIdx (not %cluster_ctarank) so ptxas keeps the loop state uniform
+  const uint32_t crank = CL2 ? (blockIdx.x & 1u) : 0u;
   const int n_kv = qt + 1 + static_cast<int>(crank);
   const int n_g = 2 * n_kv;
   const uint32_t warp = dev::warp_id();
@@ -3922,10 +3941,12 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
                          DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dq_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTmSmem<D>::BYTES);
 #ifdef MEMO_ATTN_ABLATIONS
     cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          BwdSmem<D>::BYTES);
-    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true>,
+    cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true, 0, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTmSmem<D>::BYTES);
     cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, false, 2>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTmSmem<D>::BYTES);
@@ -3954,10 +3975,16 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   const float scale_log2 = a.softmax_scale * kLog2e;
   const float2* rope = reinterpret_cast<const float2*>(a.rope);
   dim3 grid(a.S / TILE, a.H);
+  // dK/dV: CTA pairs on key tiles 2p, 2p+1 sharing each Q/dO tile by multicast
+  // whenever the tile count is even (bitwise equal; 3-4 % faster at 128K: half
+  // the L2 reads buys clock under the power cap).  Ablation build:
+  // MEMO_ATTN_DKDV_CL2=0 -> one CTA per key tile, 2 -> pairs without multicast,
+  // 3 -> the single-CTA kernel launched as clusters (placement only).
+  bool dkdv_cl2 = (a.S / TILE) % 2 == 0;
+  int clm = 1;
 #ifdef MEMO_ATTN_ABLATIONS
-  // MEMO_ATTN_DKDV_CL2=1: CTA pairs on key tiles 2p, 2p+1 sharing Q/dO by
-  // multicast (bitwise equal, 8 % SLOWER at 128K: 224.6-226.4 vs 208.5-211.2 ms)
-  const bool dkdv_cl2 = (a.S / TILE) % 2 == 0 && abl_env("MEMO_ATTN_DKDV_CL2", 0) == 1;
+  clm = abl_env("MEMO_ATTN_DKDV_CL2", 1);
+  dkdv_cl2 = dkdv_cl2 && clm >= 1;
 #endif
   if (a.ev[1]) record_timing_event(a.ev[1], stream);
 #ifdef MEMO_ATTN_ABLATIONS
@@ -3967,6 +3994,34 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
   // S^T/dP^T buffer (attn_bwd_dkdv_tm2_kernel: 231-232 vs 206-207 ms at 128K),
   // 8/9 one-step Q/dO stages (TS = 12 / 8)
   switch (abl_env("MEMO_ATTN_DKDV_VARIANT", 0)) {
+    case 13: {  // one-step Q/dO stages (TS = 12) on CTA pairs sharing them by multicast
+      CUtensorMap mq32, mdo32;
+      if (!make_tma_2d_bf16(&mq32, a.q, h, a.S, h, 64, QSTEP) || !make_tma_2d_bf16(&mdo32, a.dout, h, a.S, h, 64, QSTEP))
+        return cudaErrorInvalidValue;
+      if ((a.S / TILE) % 2 != 0) return cudaErrorInvalidValue;
+      static std::once_flag f13;
+      std::call_once(f13, [] {
+        cudaFuncSetAttribute(attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 12, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, DkdvTsSmem<D, 12>::BYTES);
+      });
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(32 * (4 + 8));
+      cfg.dynamicSmemBytes = DkdvTsSmem<D, 12>::BYTES;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 12, true>, a.k, a.v,
+                                               mq32, mdo32, (const float*)lse2, (const float*)delta, a.dk, a.dv,
+                                               a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale, scale_log2);
+      if (e != cudaSuccess) return e;
+      break;
+    }
     case 12:
       attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, false, 1><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
           a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
@@ -4041,6 +4096,7 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
           scale_log2);
       break;
     default:
+#endif
       if (dkdv_cl2) {  // CTA pairs sharing each Q/dO tile by multicast
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
@@ -4054,16 +4110,27 @@ cudaError_t launch_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true>, a.k, a.v,
-                                                 mq, mdo, (const float*)lse2, (const float*)delta, a.dk, a.dv,
-                                                 a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale, scale_log2);
-        if (e != cudaSuccess) return e;
-        break;
-      }
+        cudaError_t e;
+#ifdef MEMO_ATTN_ABLATIONS
+        if (clm == 3)  // the single-CTA kernel, launched as clusters of 2 (placement only)
+          e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_tm_kernel<D, 2>, a.k, a.v, mq, mdo, (const float*)lse2,
+                                 (const float*)delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H,
+                                 a.softmax_scale, scale_log2);
+        else if (clm == 2)  // pairs, each CTA loading whole tiles (no multicast)
+          e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true, 0, true>, a.k, a.v, mq,
+                                 mdo, (const float*)lse2, (const float*)delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0,
+                                 a.S, a.H, a.softmax_scale, scale_log2);
+        else
 #endif
-      attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
-          a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
-          scale_log2);
+          e = cudaLaunchKernelEx(&cfg, attn_bwd_dkdv_tm_kernel<D, 2, 0, false, 0, true>, a.k, a.v, mq, mdo,
+                                 (const float*)lse2, (const float*)delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S,
+                                 a.H, a.softmax_scale, scale_log2);
+        if (e != cudaSuccess) return e;
+      } else {
+        attn_bwd_dkdv_tm_kernel<D, 2><<<grid, 32 * (4 + 8), DkdvTmSmem<D>::BYTES, stream>>>(
+            a.k, a.v, mq, mdo, lse2, delta, a.dk, a.dv, a.ld_dqkv, rope, a.pos0, a.S, a.H, a.softmax_scale,
+            scale_log2);
+      }
 #ifdef MEMO_ATTN_ABLATIONS
   }
 #endif
