@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // each sharer.  The per-row K order is unchanged, so results equal the
   // unclustered kernel's bitwise.
   constexpr bool MC = CL > 1;
-  const uint32_t rank = MC ? dev::cluster_ctarank() : 0;
+  const uint32_t rank = MC ? blockIdx.x % CL : 0;  // = %cluster_ctarank for 1-D clusters; uniform for ptxas
   const uint32_t rm = CL == 4 ? (rank & 1) : rank;  // M position in the cluster; also B's half
   const uint32_t rn = CL == 4 ? (rank >> 1) : 0;    // N position in the cluster; also A's half
   const int first = static_cast<int>(blockIdx.x) / CL;
@@ -482,7 +482,7 @@ __global__ void __cluster_dims__(2 * PC, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = dev::warp_id();
   const uint32_t lane = dev::lane_id();
-  const uint32_t crank = dev::cluster_ctarank();
+  const uint32_t crank = blockIdx.x % (2 * PC);  // = %cluster_ctarank for 1-D clusters; uniform for ptxas
   const uint32_t rank = crank & 1;             // rank inside the CTA pair
   const uint32_t pair = crank >> 1;            // pair inside the cluster (PC = 2)
   const uint32_t leader = crank & ~1u;         // the pair's MMA-issuing CTA
