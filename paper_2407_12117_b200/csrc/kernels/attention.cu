@@ -4344,8 +4344,24 @@ cudaError_t attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_fwd_pp_kernel<3, true, false, false, false, false, true, true>,
-                                             mq, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
+    auto kern = attn_fwd_pp_kernel<3, true, false, false, false, false, true, true>;
+#ifdef MEMO_ATTN_ABLATIONS
+    // MEMO_ATTN_FWD_EMU=6/8/16: that share of the exponentials on the FMA pipe instead of 1/3
+    switch (abl_env("MEMO_ATTN_FWD_EMU", 3)) {
+      case 6: kern = attn_fwd_pp_kernel<6, true, false, false, false, false, true, true>; break;
+      case 8: kern = attn_fwd_pp_kernel<8, true, false, false, false, false, true, true>; break;
+      case 16: kern = attn_fwd_pp_kernel<16, true, false, false, false, false, true, true>; break;
+      default: break;
+    }
+    static std::once_flag femu;
+    std::call_once(femu, [] {
+      for (auto k : {attn_fwd_pp_kernel<6, true, false, false, false, false, true, true>,
+                     attn_fwd_pp_kernel<8, true, false, false, false, false, true, true>,
+                     attn_fwd_pp_kernel<16, true, false, false, false, false, true, true>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPpSmem::BYTES);
+    });
+#endif
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, a.o, a.lse, a.S, a.H, scale_log2);
     if (e != cudaSuccess) return e;
   } else if (a.D == 128 && a.S % (2 * TILE) == 0) {
     // ping-pong: two query tiles per CTA, setmaxnreg, 1/3 of the exponentials
