@@ -41,6 +41,9 @@ CONFIGS = {
              "Llama-7B arch, 4 layers, seq 131072, 1xB200, alpha tuned by planner"),
     "cfg1p": (4, 256, 4, 768, 512, 4096, "tiny 4-layer (h256, 4 heads, seq 4096), alpha=0.5"),
     "cfg5": (32, 4096, 32, 11008, 32000, 262144, "Llama-7B arch, 32 layers, seq 262144, 1xB200"),
+    # cfg5 at 32 layers needs 6.5 GB/layer of mandatory offload, more pinned memory than this
+    # host has (status 4); 20 layers is the deepest 256K stack that fits it
+    "cfg5s": (20, 4096, 32, 11008, 32000, 262144, "Llama-7B arch, 20 layers, seq 262144, 1xB200"),
     # the model family of BASELINE configs[3] (13B, 40 heads), sliced to 4 layers on one GPU
     "cfg4s": (4, 5120, 40, 13824, 32000, 131072,
               "Llama-13B arch, 4 layers, seq 131072, 1xB200, alpha tuned by planner"),
