@@ -671,6 +671,17 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
       // +0.6 % per cfg2 step in three alternating whole-step runs, QKV +10 %
       // in the per-shape A/B (profiles/README.md)
       if (pair) pc = 2;
+#ifdef MEMO_GEMM_ABLATIONS
+      {  // whole-step A/B only (_lib_gemmexp): MEMO_GEMM_MN_VARIANT forces the MN-major layouts' kernel
+        const char* ev = std::getenv("MEMO_GEMM_MN_VARIANT");
+        const int v = ev ? std::atoi(ev) : 0;
+        if ((A_MN || B_MN) && v > 0) {
+          pair = v >= GEMM_VARIANT_PAIR;
+          cl = v == GEMM_VARIANT_MC2 ? 2 : v == GEMM_VARIANT_MC4 ? 4 : 1;
+          pc = v == GEMM_VARIANT_PAIR2 ? 2 : 1;
+        }
+      }
+#endif
   }
   const bool mc = cl > 1;
   if (!A_MN)
