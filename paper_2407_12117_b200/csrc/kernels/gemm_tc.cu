@@ -680,6 +680,14 @@ cudaError_t launch(const GemmDesc& d, cudaStream_t stream) {
           cl = v == GEMM_VARIANT_MC2 ? 2 : v == GEMM_VARIANT_MC4 ? 4 : 1;
           pc = v == GEMM_VARIANT_PAIR2 ? 2 : 1;
         }
+        // MEMO_GEMM_KF_VARIANT: the same for the K-major shapes that take CTA pairs
+        const char* ek = std::getenv("MEMO_GEMM_KF_VARIANT");
+        const int vk = ek ? std::atoi(ek) : 0;
+        if (pair && !A_MN && !B_MN && vk > 0) {
+          pair = vk >= GEMM_VARIANT_PAIR;
+          cl = vk == GEMM_VARIANT_MC2 ? 2 : vk == GEMM_VARIANT_MC4 ? 4 : 1;
+          pc = vk == GEMM_VARIANT_PAIR2 ? 2 : 1;
+        }
       }
 #endif
   }
